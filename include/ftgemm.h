@@ -1,0 +1,193 @@
+/*
+ * ftgemm.h -- C ABI of the B200-native fused online-ABFT GEMM
+ * (arXiv 2305.01024, "Anatomy of High-Performance GEMM with Online Fault
+ * Tolerance on GPUs").  Library: paper_2305_01024_b200/libftgemm.so.
+ *
+ *   C = alpha * A * B + beta * C
+ *
+ * computed with the paper's checksum scheme (section 2.2,
+ * Eq. (1)-(3)): a column checksum e^T A of every M-tile and a row checksum B e
+ * of every N-tile are encoded (ftgemm_encode), carried through the same
+ * mainloop as C (the references C^c = (e^T A) B and C^r = A (B e)), and in the
+ * epilogue of every output tile the recomputed row / column sums of the FP32
+ * accumulator are compared with them; one corrupted element per tile is
+ * located at the intersection of the mismatching row and column and corrected
+ * from the row checksum (section 4.2.1, section 5.3),
+ * under the paper's single-event-upset fault model (section 4.1).
+ *
+ * Conventions (all entry points):
+ *   - Matrices are ROW-MAJOR: A is M x K (lda >= K), B is K x N (ldb >= N),
+ *     C is M x N (ldc >= N).  Leading dimensions are in elements.
+ *   - All pointers except those documented as host pointers are DEVICE
+ *     pointers owned by the caller.  The library allocates no device memory
+ *     and keeps no state between calls other than host-side caches.
+ *   - All sizes are int64_t.  Every call is asynchronous on `stream`
+ *     (a cudaStream_t passed as void*), except ftgemm_plan (pure host) and
+ *     ftgemm_report (synchronises the stream).
+ *   - Return value: FTGEMM_OK or an FTGEMM_ERR_* code; argument errors are
+ *     detected synchronously before anything is launched; the message is
+ *     available from ftgemm_last_error() (thread-local).  Faults that the ABFT
+ *     scheme detects are NOT errors: C is written and the report records them.
+ *   - There is no CPU fallback: when the device path cannot run the call,
+ *     the call fails.
+ */
+#ifndef FTGEMM_H_
+#define FTGEMM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FTGEMM_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define FTGEMM_API __attribute__((visibility("default")))
+#else
+#define FTGEMM_API
+#endif
+
+/* ---- return codes ---------------------------------------------------------- */
+#define FTGEMM_OK                 0
+#define FTGEMM_ERR_INVALID_VALUE  1   /* null pointer, dim < 1, ld < cols, bad enum, small workspace */
+#define FTGEMM_ERR_UNSUPPORTED    2   /* alignment (TMA needs 16-byte bases and row pitches), no sm_100 device */
+#define FTGEMM_ERR_CUDA           3   /* a CUDA runtime error (launch or asynchronous kernel fault) */
+
+/* ---- precision variants (north_star item 3) -------------------------------- */
+#define FTGEMM_F32_SIMT 0   /* FP32 in/out, FP32 FFMA on CUDA cores; the paper's SGEMM numerics
+                               (one fmaf per k, ascending k; section 3.1) */
+#define FTGEMM_TF32     1   /* FP32 in/out, tcgen05.mma kind::tf32, FP32 accumulate in TMEM */
+#define FTGEMM_BF16     2   /* BF16 in/out, tcgen05.mma kind::f16 (bf16), FP32 accumulate in TMEM */
+
+/* ---- fault-tolerance level -------------------------------------------------- */
+#define FTGEMM_FT_OFF     0  /* same tile shape family, checksums compiled out (the overhead baseline) */
+#define FTGEMM_FT_DETECT  1  /* verify + locate, report, leave C as computed (detect-only flavour) */
+#define FTGEMM_FT_CORRECT 2  /* verify + locate + correct (the paper's online ABFT) */
+
+/* ---- fault injection (section 5.3) ---------------------------- */
+#define FTGEMM_INJ_FLIP 0    /* acc bits ^= (1 << bit)            (register bit flip) */
+#define FTGEMM_INJ_ADD  1    /* acc += addend                      (the paper's "numerical offset") */
+#define FTGEMM_TGT_ACC     0 /* the output accumulator of element (row, col) */
+#define FTGEMM_TGT_ROW_REF 1 /* the carried row-checksum reference C^r of row `row` in col's tile */
+#define FTGEMM_TGT_COL_REF 2 /* the carried column-checksum reference C^c of column `col` in row's tile */
+
+/* One fault: applied once, to the FP32 accumulator, right after the MMA
+ * k-block that contains k_elem has been accumulated (k_elem is rounded UP to
+ * the end of its k-block of size plan.bk; values >= K address the last block). */
+typedef struct ftgemm_inject {
+    int64_t row, col, k_elem;
+    int32_t bit;        /* 0..31 for FLIP */
+    int32_t mode;       /* FTGEMM_INJ_* */
+    int32_t target;     /* FTGEMM_TGT_* */
+    float   addend;     /* for FTGEMM_INJ_ADD */
+} ftgemm_inject_t;      /* 40 bytes */
+
+/* ---- report ------------------------------------------------------------------ */
+#define FTGEMM_EV_CORRECTED      1  /* one row + one column flagged, consistent: element corrected */
+#define FTGEMM_EV_CHECKSUM_ONLY  2  /* one row only or one column only: the fault hit a reference; C untouched */
+#define FTGEMM_EV_UNCORRECTABLE  3  /* >= 2 rows or >= 2 columns, or inconsistent magnitudes; C untouched */
+#define FTGEMM_EV_LOCATED        4  /* FT_DETECT: single error located, not corrected */
+
+typedef struct ftgemm_event {
+    int64_t row, col;            /* global position (p*, q*); -1 when that side had no flag */
+    int32_t tile_m, tile_n;      /* check-tile coordinates */
+    int32_t kind;                /* FTGEMM_EV_* */
+    int32_t n_rows, n_cols;      /* number of flagged rows / columns in the tile */
+    int32_t reserved;
+    float   resid_row, resid_col;/* residual of the first flagged row / column */
+    float   tau_row, tau_col;    /* the thresholds they were compared against */
+} ftgemm_event_t;                /* 56 bytes */
+
+typedef struct ftgemm_counts {
+    int64_t tiles_checked;       /* tiles verified (FT level != OFF) */
+    int64_t tiles_detected;      /* tiles with >= 1 flagged row or column */
+    int64_t corrected, checksum_only, uncorrectable, located;
+    int64_t events;              /* events recorded or dropped */
+    int64_t dropped;             /* events that did not fit the ring */
+} ftgemm_counts_t;
+
+/* ---- plan --------------------------------------------------------------------
+ * The host-side instantiation table (north_star item 4): which compile-time
+ * kernel serves (dtype, M, N, K), the check-tile geometry the verification
+ * works on, and the workspace sizes.  Pure host function, no device access.  */
+typedef struct ftgemm_plan {
+    int32_t dtype;
+    int32_t shape_class;         /* FTGEMM_SHAPE_* */
+    int32_t bm, bn, bk;          /* MMA / CTA tile */
+    int32_t check_tile_m;        /* data rows per check tile (FT on)    */
+    int32_t check_tile_n;        /* data columns per check tile (FT on) */
+    int32_t off_tile_m, off_tile_n; /* data tile with FT_OFF */
+    int32_t stages, cta_group;
+    int32_t max_events, max_inject;
+    int32_t pad0;
+    int64_t tiles_m, tiles_n;    /* check-tile grid with FT on */
+    int64_t enc_bytes;           /* size of enc_ws (A part + B part)          */
+    int64_t enc_b_offset;        /* byte offset of the B part inside enc_ws   */
+    int64_t enc_b_bytes;         /* bytes of the B part (broadcast unit, multi-GPU) */
+    int64_t report_bytes;        /* size of report_ws                         */
+    float   u_acc, lambda1, lambda2;   /* threshold constants (R1) */
+    int32_t pad1;
+} ftgemm_plan_t;
+
+#define FTGEMM_SHAPE_SQUARE      0  /* 128 x 256 tcgen05 tile (128 x 128 SIMT) */
+#define FTGEMM_SHAPE_SMALL_N     1  /* 128 x 128 tcgen05 tile: narrow N or too few tiles for 148 SMs */
+
+/* Fill *out for a problem.  Errors: INVALID_VALUE (dims < 1, bad dtype, null out). */
+FTGEMM_API int ftgemm_plan(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* out);
+
+/* ---- encode (Eq. 1 / Eq. 2) -------------------------
+ * which = 1: encode A  ->  per check-tile i: Ac_i[k] = sum_{p in tile rows} A[p,k]
+ *                         (FP32), its exact split into three operand-format
+ *                         values (hi+mid+lo == Ac_i) for the tensor-core path,
+ *                         ||A[p,:]||_2 per row and ||Ac_i||_2.
+ * which = 2: encode B  ->  per check-tile j: Br_j[k] = sum_{q in tile cols} B[k,q],
+ *                         its split, ||B[:,q]||_2 per column and ||Br_j||_2.
+ * which = 3: both.  Writes only enc_ws (plan.enc_bytes, caller-allocated,
+ * 256-byte aligned); A and B are read-only.  The A part and the B part are
+ * disjoint ([0, enc_b_offset) and [enc_b_offset, +enc_b_bytes)), so a B
+ * encoded on one GPU can be broadcast with B and reused (weights).
+ * Errors: INVALID_VALUE, UNSUPPORTED (misaligned), CUDA.                      */
+FTGEMM_API int ftgemm_encode(int dtype, int64_t M, int64_t N, int64_t K,
+                  const void* A, int64_t lda, const void* B, int64_t ldb,
+                  void* enc_ws, int which, void* stream);
+
+/* ---- run --------------------------------------------------------------------
+ * C = alpha A B + beta C with online ABFT at ft_level.  A, B, C are device
+ * row-major matrices of the dtype's operand type (float for F32_SIMT/TF32,
+ * __nv_bfloat16 for BF16); C is read only when beta != 0.  enc_ws must hold
+ * the encode of these A and B (ignored for FT_OFF).  inj is a HOST array of
+ * n_inj faults (copied during the call; may be NULL when n_inj == 0;
+ * n_inj <= plan.max_inject).  report_ws (plan.report_bytes, device) receives
+ * counters and events; it accumulates across calls until ftgemm_report_reset.
+ * Faults and their corrections are recorded, never returned as errors.
+ * Errors: INVALID_VALUE, UNSUPPORTED (alignment: A, B, C bases 16-byte
+ * aligned; lda, ldb, ldc * sizeof(elem) multiples of 16), CUDA.               */
+FTGEMM_API int ftgemm_run(int dtype, int64_t M, int64_t N, int64_t K, float alpha,
+               const void* A, int64_t lda, const void* B, int64_t ldb,
+               float beta, void* C, int64_t ldc,
+               const void* enc_ws, int ft_level,
+               const ftgemm_inject_t* inj, int32_t n_inj,
+               void* report_ws, void* stream);
+
+/* ---- report ------------------------------------------------------------------
+ * Synchronises `stream`, then copies the counters into *counts (host) and up
+ * to max_events events into events (host array, may be NULL when
+ * max_events == 0).  Surfaces asynchronous kernel faults as FTGEMM_ERR_CUDA.   */
+FTGEMM_API int ftgemm_report(const void* report_ws, ftgemm_counts_t* counts,
+                  ftgemm_event_t* events, int32_t max_events, void* stream);
+
+/* Zero the counters and the event ring (asynchronous on stream). */
+FTGEMM_API int ftgemm_report_reset(void* report_ws, int64_t report_bytes, void* stream);
+
+/* Thread-local message of the last failing call ("" if none). */
+FTGEMM_API const char* ftgemm_last_error(void);
+
+/* ABI version (FTGEMM_ABI_VERSION) and the compiled device architecture (1000 = sm_100a). */
+FTGEMM_API int ftgemm_version(void);
+FTGEMM_API int ftgemm_device_arch(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FTGEMM_H_ */

@@ -1,0 +1,354 @@
+// api.cu -- the C ABI of libftgemm (include/ftgemm.h): plan table, argument
+// validation, TMA descriptor construction, fault-list preparation and kernel
+// dispatch.  Host code only; the arithmetic is in encode.cu / tc_gemm.cu /
+// simt_gemm.cu.  No CPU fallback exists: anything the device path cannot run is
+// rejected with an error code.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ftg {
+cudaError_t launch_encode(const Geometry& g, const EncLayout& L, int64_t M, int64_t N, int64_t K,
+                          const void* A, int64_t lda, const void* B, int64_t ldb, void* enc, int which,
+                          cudaStream_t st);
+}  // namespace ftg
+
+namespace ftg {
+cudaError_t launch_tc(bool tf32, int bn, bool ft, const CUtensorMap& mA, const CUtensorMap& mB,
+                      const TcArgs& a, cudaStream_t st);
+cudaError_t launch_simt(bool ft, const SimtArgs& a, cudaStream_t st);
+}  // namespace ftg
+
+using namespace ftg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+int fail_cuda(cudaError_t e, const char* where) {
+    return fail(FTGEMM_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+constexpr int kTcGroup = 16;    // must match tile_coords() in tc_gemm.cu
+
+bool valid_dtype(int d) { return d == FTGEMM_F32_SIMT || d == FTGEMM_TF32 || d == FTGEMM_BF16; }
+
+// The shape-class table (north_star item 4): compile-time instantiations
+// chosen per problem shape.
+void fill_plan(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* p) {
+    std::memset(p, 0, sizeof(*p));
+    p->dtype = dtype;
+    p->max_events = kMaxEvents;
+    p->max_inject = kMaxInject;
+    if (dtype == FTGEMM_F32_SIMT) {
+        p->shape_class = FTGEMM_SHAPE_SQUARE;
+        p->bm = 128; p->bn = 128; p->bk = 8;
+        p->check_tile_m = 128; p->check_tile_n = 128;
+        p->off_tile_m = 128; p->off_tile_n = 128;
+        p->stages = 2; p->cta_group = 1;
+        p->u_acc = std::ldexp(1.0f, -24); p->lambda1 = 16.0f; p->lambda2 = 32.0f;
+    } else {
+        const int bk = dtype == FTGEMM_TF32 ? 32 : 64;
+        const int64_t tiles256 = ((M + 124) / 125) * ((N + 251) / 252);
+        const bool small = tiles256 < 2 * kNumSMsB200 || N <= 512;
+        const int bn = small ? 128 : 256;
+        p->shape_class = small ? FTGEMM_SHAPE_SMALL_N : FTGEMM_SHAPE_SQUARE;
+        p->bm = 128; p->bn = bn; p->bk = bk;
+        p->check_tile_m = 125; p->check_tile_n = bn - 4;
+        p->off_tile_m = 128; p->off_tile_n = bn;
+        p->stages = bn == 256 ? 4 : 6; p->cta_group = 1;
+        p->u_acc = std::ldexp(1.0f, -23); p->lambda1 = 8.0f; p->lambda2 = 16.0f;
+    }
+    p->tiles_m = (M + p->check_tile_m - 1) / p->check_tile_m;
+    p->tiles_n = (N + p->check_tile_n - 1) / p->check_tile_n;
+}
+
+Geometry geometry(const ftgemm_plan_t& p, int64_t K) {
+    Geometry g{};
+    g.dtype = p.dtype;
+    g.bm = p.bm; g.bn = p.bn; g.bk = p.bk;
+    g.bmd = p.check_tile_m; g.bnd = p.check_tile_n;
+    g.tiles_m = (int)p.tiles_m; g.tiles_n = (int)p.tiles_n;
+    g.kp = (int)(((K + p.bk - 1) / p.bk) * p.bk);
+    g.nkc = (g.kp + 255) / 256;
+    g.elt = p.dtype == FTGEMM_BF16 ? 2 : 4;
+    g.split = p.dtype != FTGEMM_F32_SIMT;
+    return g;
+}
+
+int check_device() {
+    static int cached = -1;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    if (cached >= 0) return cached;
+    int dev = 0, major = 0, minor = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess) {
+        cudaGetLastError();
+        return cached = 0;
+    }
+    return cached = (major == 10 && minor == 0) ? 1 : 0;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+int make_map(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t outer,
+             uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
+             CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return fail(FTGEMM_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {row_bytes};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(FTGEMM_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return FTGEMM_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int check_dims(int dtype, int64_t M, int64_t N, int64_t K) {
+    if (!valid_dtype(dtype)) return fail(FTGEMM_ERR_INVALID_VALUE, "unknown dtype %d", dtype);
+    if (M < 1 || N < 1 || K < 1) return fail(FTGEMM_ERR_INVALID_VALUE, "dims must be >= 1 (M=%lld N=%lld K=%lld)",
+                                             (long long)M, (long long)N, (long long)K);
+    if (M >= (1ll << 31) || N >= (1ll << 31) || K >= (1ll << 31))
+        return fail(FTGEMM_ERR_UNSUPPORTED, "dims must be < 2^31");
+    return FTGEMM_OK;
+}
+
+// schedule key of a check tile (the order the kernel walks tiles in)
+int tile_key(const ftgemm_plan_t& p, int ti, int tj) {
+    if (p.dtype == FTGEMM_F32_SIMT) return ti * (int)p.tiles_n + tj;
+    const int G = kTcGroup;
+    const int grp = ti / G, first = grp * G;
+    const int gsz = std::min<int>(G, (int)p.tiles_m - first);
+    return grp * G * (int)p.tiles_n + tj * gsz + (ti - first);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ftgemm_version(void) { return FTGEMM_ABI_VERSION; }
+int ftgemm_device_arch(void) { return 1000; }
+const char* ftgemm_last_error(void) { return g_err.c_str(); }
+
+int ftgemm_plan(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* out) {
+    if (!out) return fail(FTGEMM_ERR_INVALID_VALUE, "null plan pointer");
+    int e = check_dims(dtype, M, N, K);
+    if (e) return e;
+    fill_plan(dtype, M, N, K, out);
+    const Geometry g = geometry(*out, K);
+    const EncLayout L = enc_layout(g, M, N);
+    out->enc_bytes = (int64_t)L.total;
+    out->enc_b_offset = (int64_t)L.b_off;
+    out->enc_b_bytes = (int64_t)L.b_bytes;
+    out->report_bytes = (int64_t)report_bytes();
+    g_err.clear();
+    return FTGEMM_OK;
+}
+
+int ftgemm_encode(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B,
+                  int64_t ldb, void* enc_ws, int which, void* stream) {
+    int e = check_dims(dtype, M, N, K);
+    if (e) return e;
+    if (which < 1 || which > 3) return fail(FTGEMM_ERR_INVALID_VALUE, "which must be 1, 2 or 3");
+    if (!enc_ws) return fail(FTGEMM_ERR_INVALID_VALUE, "null enc_ws");
+    if ((which & 1) && (!A || lda < K)) return fail(FTGEMM_ERR_INVALID_VALUE, "bad A / lda");
+    if ((which & 2) && (!B || ldb < N)) return fail(FTGEMM_ERR_INVALID_VALUE, "bad B / ldb");
+    const int elt = dtype == FTGEMM_BF16 ? 2 : 4;
+    if ((which & 1) && (!aligned16(A) || (lda * elt) % 16)) return fail(FTGEMM_ERR_UNSUPPORTED, "A must be 16-byte aligned with 16-byte row pitch");
+    if ((which & 2) && (!aligned16(B) || (ldb * elt) % 16)) return fail(FTGEMM_ERR_UNSUPPORTED, "B must be 16-byte aligned with 16-byte row pitch");
+    if ((reinterpret_cast<uintptr_t>(enc_ws) & 255) != 0) return fail(FTGEMM_ERR_INVALID_VALUE, "enc_ws must be 256-byte aligned");
+    if (!check_device()) return fail(FTGEMM_ERR_UNSUPPORTED, "no sm_100 (B200) device");
+    ftgemm_plan_t p;
+    fill_plan(dtype, M, N, K, &p);
+    const Geometry g = geometry(p, K);
+    const EncLayout L = enc_layout(g, M, N);
+    cudaError_t ce = launch_encode(g, L, M, N, K, A, lda, B, ldb, enc_ws, which, (cudaStream_t)stream);
+    if (ce != cudaSuccess) return fail_cuda(ce, "encode launch");
+    g_err.clear();
+    return FTGEMM_OK;
+}
+
+int ftgemm_run(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const void* A, int64_t lda,
+               const void* B, int64_t ldb, float beta, void* C, int64_t ldc, const void* enc_ws, int ft_level,
+               const ftgemm_inject_t* inj, int32_t n_inj, void* report_ws, void* stream) {
+    int e = check_dims(dtype, M, N, K);
+    if (e) return e;
+    if (!A || !B || !C) return fail(FTGEMM_ERR_INVALID_VALUE, "null A, B or C");
+    if (lda < K || ldb < N || ldc < N) return fail(FTGEMM_ERR_INVALID_VALUE, "leading dimension too small");
+    if (ft_level < FTGEMM_FT_OFF || ft_level > FTGEMM_FT_CORRECT) return fail(FTGEMM_ERR_INVALID_VALUE, "bad ft_level");
+    if (n_inj < 0 || n_inj > kMaxInject || (n_inj > 0 && !inj)) return fail(FTGEMM_ERR_INVALID_VALUE, "bad injection list");
+    if (ft_level == FTGEMM_FT_OFF && n_inj > 0) return fail(FTGEMM_ERR_INVALID_VALUE, "fault injection needs ft_level DETECT or CORRECT");
+    if (ft_level != FTGEMM_FT_OFF && (!enc_ws || !report_ws)) return fail(FTGEMM_ERR_INVALID_VALUE, "FT needs enc_ws and report_ws");
+    if (!std::isfinite(alpha) || !std::isfinite(beta)) return fail(FTGEMM_ERR_INVALID_VALUE, "alpha/beta must be finite");
+    const int elt = dtype == FTGEMM_BF16 ? 2 : 4;
+    if (!aligned16(A) || !aligned16(B) || !aligned16(C) || (lda * elt) % 16 || (ldb * elt) % 16 || (ldc * elt) % 16)
+        return fail(FTGEMM_ERR_UNSUPPORTED, "A, B, C must be 16-byte aligned with 16-byte row pitches");
+    if (!check_device()) return fail(FTGEMM_ERR_UNSUPPORTED, "no sm_100 (B200) device");
+
+    ftgemm_plan_t p;
+    fill_plan(dtype, M, N, K, &p);
+    const bool ft = ft_level != FTGEMM_FT_OFF;
+    const Geometry g = geometry(p, K);
+    const EncLayout L = enc_layout(g, M, N);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int num_kb = (int)((K + p.bk - 1) / p.bk);
+
+    // ---- faults: resolve to (tile key, k-block, in-tile position), sort ----
+    const DevInject* dinj = nullptr;
+    if (n_inj > 0) {
+        std::vector<DevInject> v((size_t)n_inj);
+        std::vector<int> per_tile;
+        for (int i = 0; i < n_inj; ++i) {
+            const ftgemm_inject_t& f = inj[i];
+            if (f.row < 0 || f.row >= M || f.col < 0 || f.col >= N || f.k_elem < 0 ||
+                f.bit < 0 || f.bit > 31 || f.mode < 0 || f.mode > 1 || f.target < 0 || f.target > 2)
+                return fail(FTGEMM_ERR_INVALID_VALUE, "injection %d out of range", i);
+            const int ti = (int)(f.row / p.check_tile_m), tj = (int)(f.col / p.check_tile_n);
+            DevInject d;
+            d.tile = tile_key(p, ti, tj);
+            d.kb = (int)std::min<int64_t>(f.k_elem / p.bk, num_kb - 1);
+            d.p = (int)(f.row - (int64_t)ti * p.check_tile_m);
+            d.q = (int)(f.col - (int64_t)tj * p.check_tile_n);
+            d.bit = f.bit; d.mode = f.mode; d.target = f.target; d.addend = f.addend;
+            v[i] = d;
+        }
+        std::stable_sort(v.begin(), v.end(), [](const DevInject& x, const DevInject& y) {
+            return x.tile != y.tile ? x.tile < y.tile : x.kb < y.kb;
+        });
+        if (dtype == FTGEMM_F32_SIMT) {
+            int run = 1;
+            for (int i = 1; i < n_inj; ++i) {
+                run = v[i].tile == v[i - 1].tile ? run + 1 : 1;
+                if (run > 8) return fail(FTGEMM_ERR_INVALID_VALUE, "at most 8 faults per SIMT tile");
+            }
+        }
+        char* dst = reinterpret_cast<char*>(report_ws) + report_inject_offset();
+        cudaError_t ce = cudaMemcpyAsync(dst, v.data(), sizeof(DevInject) * v.size(), cudaMemcpyHostToDevice, st);
+        if (ce != cudaSuccess) return fail_cuda(ce, "fault-list upload");
+        dinj = reinterpret_cast<const DevInject*>(dst);
+    }
+
+    const char* enc = reinterpret_cast<const char*>(enc_ws);
+    const float tau_u = p.u_acc, l1 = p.lambda1, l2 = p.lambda2, sqk = std::sqrt((float)K);
+    cudaError_t ce;
+    if (dtype == FTGEMM_F32_SIMT) {
+        SimtArgs a{};
+        a.M = (int)M; a.N = (int)N; a.K = (int)K; a.num_kb = num_kb;
+        a.tiles_m = (int)p.tiles_m; a.tiles_n = (int)p.tiles_n; a.ft_level = ft_level;
+        a.alpha = alpha; a.beta = beta;
+        a.A = (const float*)A; a.lda = lda; a.B = (const float*)B; a.ldb = ldb; a.C = (float*)C; a.ldc = ldc;
+        if (ft) {
+            a.Ac = (const float*)(enc + L.ac); a.Br = (const float*)(enc + L.br); a.kp = g.kp;
+            a.rownorm = (const float*)(enc + L.rownorm); a.colnorm = (const float*)(enc + L.colnorm);
+            a.acnorm = (const float*)(enc + L.acnorm); a.brnorm = (const float*)(enc + L.brnorm);
+        }
+        a.tau_u = tau_u; a.tau_l1 = l1; a.tau_l2 = l2; a.sqrtK = sqk;
+        a.rep = (ReportDev*)report_ws; a.inj = dinj; a.n_inj = n_inj;
+        ce = launch_simt(ft, a, st);
+    } else {
+        const bool tf32 = dtype == FTGEMM_TF32;
+        const CUtensorMapDataType dt = tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+        const int bmd = ft ? p.check_tile_m : p.off_tile_m;
+        const int bnd = ft ? p.check_tile_n : p.off_tile_n;
+        const uint32_t boxn = 128 / elt;
+        CUtensorMap mA, mB;
+        if ((e = make_map(&mA, dt, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * elt, (uint32_t)p.bk, (uint32_t)p.bm))) return e;
+        if ((e = make_map(&mB, dt, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb * elt, boxn, (uint32_t)p.bk,
+                          tf32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B))) return e;
+        TcArgs a{};
+        a.M = (int)M; a.N = (int)N; a.K = (int)K; a.num_kb = num_kb;
+        a.tiles_m = (int)((M + bmd - 1) / bmd); a.tiles_n = (int)((N + bnd - 1) / bnd);
+        a.num_tiles = a.tiles_m * a.tiles_n;
+        a.ft_level = ft_level; a.alpha = alpha; a.beta = beta; a.C = C; a.ldc = ldc;
+        if (ft) {
+            a.Y = enc + L.y; a.X = enc + L.x; a.kp = g.kp;
+            a.rownorm = (const float*)(enc + L.rownorm); a.colnorm = (const float*)(enc + L.colnorm);
+            a.acnorm = (const float*)(enc + L.acnorm); a.brnorm = (const float*)(enc + L.brnorm);
+        }
+        a.tau_u = tau_u; a.tau_l1 = l1; a.tau_l2 = l2; a.sqrtK = sqk;
+        a.rep = (ReportDev*)report_ws; a.inj = dinj; a.n_inj = n_inj;
+        if (const char* d = getenv("FTGEMM_DBG")) a.dbg = atoi(d);
+        ce = launch_tc(tf32, p.bn, ft, mA, mB, a, st);
+    }
+    if (ce != cudaSuccess) return fail_cuda(ce, "kernel launch");
+    g_err.clear();
+    return FTGEMM_OK;
+}
+
+int ftgemm_report(const void* report_ws, ftgemm_counts_t* counts, ftgemm_event_t* events, int32_t max_events,
+                  void* stream) {
+    if (!report_ws || !counts || max_events < 0 || (max_events > 0 && !events))
+        return fail(FTGEMM_ERR_INVALID_VALUE, "bad report arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t ce = cudaStreamSynchronize(st);
+    if (ce != cudaSuccess) return fail_cuda(ce, "stream (asynchronous kernel fault)");
+    unsigned long long c[8];
+    ce = cudaMemcpy(c, report_ws, sizeof(c), cudaMemcpyDeviceToHost);
+    if (ce != cudaSuccess) return fail_cuda(ce, "report copy");
+    counts->tiles_checked = (int64_t)c[CNT_CHECKED];
+    counts->tiles_detected = (int64_t)c[CNT_DETECTED];
+    counts->corrected = (int64_t)c[CNT_CORRECTED];
+    counts->checksum_only = (int64_t)c[CNT_CHECKSUM_ONLY];
+    counts->uncorrectable = (int64_t)c[CNT_UNCORRECTABLE];
+    counts->located = (int64_t)c[CNT_LOCATED];
+    counts->events = (int64_t)c[CNT_EVENTS];
+    counts->dropped = (int64_t)c[CNT_DROPPED];
+    const int64_t stored = std::min<int64_t>(counts->events, kMaxEvents);
+    const int64_t n = std::min<int64_t>(stored, max_events);
+    if (n > 0) {
+        ce = cudaMemcpy(events, reinterpret_cast<const char*>(report_ws) + offsetof(ReportDev, events),
+                        sizeof(ftgemm_event_t) * (size_t)n, cudaMemcpyDeviceToHost);
+        if (ce != cudaSuccess) return fail_cuda(ce, "event copy");
+    }
+    g_err.clear();
+    return FTGEMM_OK;
+}
+
+int ftgemm_report_reset(void* report_ws, int64_t report_bytes_, void* stream) {
+    if (!report_ws || report_bytes_ < (int64_t)sizeof(ReportDev)) return fail(FTGEMM_ERR_INVALID_VALUE, "bad report workspace");
+    cudaError_t ce = cudaMemsetAsync(report_ws, 0, sizeof(ReportDev), (cudaStream_t)stream);
+    if (ce != cudaSuccess) return fail_cuda(ce, "report reset");
+    g_err.clear();
+    return FTGEMM_OK;
+}
+
+}  // extern "C"

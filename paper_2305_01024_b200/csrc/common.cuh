@@ -1,0 +1,118 @@
+// common.cuh -- device-side data layouts shared by the encode, fused-GEMM and
+// host API translation units of libftgemm (never by the oracle).
+#pragma once
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "../../include/ftgemm.h"
+
+namespace ftg {
+
+constexpr int kNumSMsB200 = 148;
+constexpr int kMaxEvents = 4096;
+constexpr int kMaxInject = 65536;
+
+// ---- report workspace (device) --------------------------------------------
+struct DevInject {        // one fault, resolved to (check tile, k-block, in-tile position)
+    int32_t tile, kb, p, q;
+    int32_t bit, mode, target;
+    float addend;
+};
+static_assert(sizeof(DevInject) == 32, "DevInject layout");
+
+struct ReportDev {
+    unsigned long long counts[8];     // order of ftgemm_counts_t
+    unsigned long long pad[8];
+    ftgemm_event_t events[kMaxEvents];
+};
+enum { CNT_CHECKED = 0, CNT_DETECTED, CNT_CORRECTED, CNT_CHECKSUM_ONLY, CNT_UNCORRECTABLE,
+       CNT_LOCATED, CNT_EVENTS, CNT_DROPPED };
+
+inline size_t report_bytes() { return sizeof(ReportDev) + (size_t)kMaxInject * sizeof(DevInject); }
+inline size_t report_inject_offset() { return sizeof(ReportDev); }
+
+// ---- kernel arguments (plain data, passed by value) ------------------------
+struct TcArgs {
+    int M, N, K, num_kb;
+    int tiles_m, tiles_n, num_tiles;
+    int ft_level;
+    float alpha, beta;
+    void* C; int64_t ldc;
+    const void* Y; const void* X; int kp;
+    const float* rownorm; const float* colnorm; const float* acnorm; const float* brnorm;
+    float tau_u, tau_l1, tau_l2, sqrtK;
+    ReportDev* rep;
+    const DevInject* inj; int n_inj;
+    int dbg;   // development bisection flags (0 in production)
+};
+
+struct SimtArgs {
+    int M, N, K, num_kb;
+    int tiles_m, tiles_n, ft_level;
+    float alpha, beta;
+    const float* A; int64_t lda;
+    const float* B; int64_t ldb;
+    float* C; int64_t ldc;
+    const float* Ac; const float* Br; int kp;
+    const float* rownorm; const float* colnorm; const float* acnorm; const float* brnorm;
+    float tau_u, tau_l1, tau_l2, sqrtK;
+    ReportDev* rep;
+    const DevInject* inj; int n_inj;
+};
+
+// ---- tile geometry of a plan ---------------------------------------------
+struct Geometry {
+    int dtype;            // FTGEMM_*
+    int bm, bn, bk;       // CTA / MMA tile
+    int bmd, bnd;         // data rows / cols per check tile (FT on)
+    int tiles_m, tiles_n; // check-tile grid (FT on)
+    int kp;               // K padded to bk
+    int nkc;              // 256-wide K chunks (encode partial norms)
+    int elt;              // operand element bytes
+    int split;            // 1 when Y/X split operands exist (tensor-core paths)
+};
+
+// Encode workspace layout (byte offsets; each region 256-byte aligned).
+struct EncLayout {
+    size_t ac, y, rownorm, acnorm, rn2;       // A part
+    size_t b_off;                             // start of the B part
+    size_t br, x, colnorm, brnorm, cn2;       // absolute offsets
+    size_t a_bytes, b_bytes, total;
+};
+
+inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+inline EncLayout enc_layout(const Geometry& g, int64_t M, int64_t N) {
+    EncLayout L{};
+    size_t o = 0;
+    L.ac = o;      o = align256(o + sizeof(float) * (size_t)g.tiles_m * g.kp);
+    L.y = o;       o = align256(o + (g.split ? (size_t)g.elt * g.tiles_m * 3 * g.kp : 0));
+    L.rownorm = o; o = align256(o + sizeof(float) * (size_t)M);
+    L.acnorm = o;  o = align256(o + sizeof(float) * (size_t)g.tiles_m);
+    L.rn2 = o;     o = align256(o + sizeof(float) * (size_t)g.nkc * M);
+    L.a_bytes = o;
+    L.b_off = o;
+    L.br = o;      o = align256(o + sizeof(float) * (size_t)g.tiles_n * g.kp);
+    L.x = o;       o = align256(o + (g.split ? (size_t)g.elt * g.tiles_n * g.kp * 4 : 0));
+    L.colnorm = o; o = align256(o + sizeof(float) * (size_t)N);
+    L.brnorm = o;  o = align256(o + sizeof(float) * (size_t)g.tiles_n);
+    L.cn2 = o;     o = align256(o + sizeof(float) * (size_t)g.nkc * N);
+    L.b_bytes = o - L.b_off;
+    L.total = o;
+    return L;
+}
+
+// ---- operand conversions ---------------------------------------------------
+// TF32 operand semantics of tcgen05.mma kind::tf32 on FP32 bit patterns:
+// the low 13 mantissa bits are ignored (truncation).  Pinned on the device by
+// tests/test_gpu_parity.py::test_tf32_operand_semantics.
+__device__ __forceinline__ float tf32_trunc(float x) {
+    return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+__device__ __forceinline__ float bf16_to_f32(uint16_t h) { return __uint_as_float((uint32_t)h << 16); }
+__device__ __forceinline__ uint16_t f32_to_bf16_rn(float x) {
+    return __bfloat16_as_ushort(__float2bfloat16_rn(x));
+}
+
+}  // namespace ftg

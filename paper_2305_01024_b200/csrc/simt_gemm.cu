@@ -1,0 +1,352 @@
+// simt_gemm.cu -- exact-semantics FP32 SIMT fused ABFT SGEMM (north_star item 3).
+//
+// The paper's threadblock-level FT-SGEMM (section 4.2.3) on
+// CUDA cores, with the paper's SGEMM structure (section 3.1 and
+// the "huge" row of Table 1: m_tb = n_tb = 128, k_tb = 8,
+// 8 x 8 outputs per thread, 256 threads, double-buffered shared memory).
+// Every output is accumulated with one fmaf per k in ascending k, so a clean
+// element is bit-identical to the oracle's FP32SEQ mode.
+//
+// Checksums (Eq. (3)): the encoded e^T A_i and B_j e (from the
+// encode kernel) are staged with each k-block next to A_tb and B_tb -- the
+// paper fuses their loads with the prefetch -- and carried by
+// the CTA through the same k-loop:
+//     threads 0..127  : C^r_ref[p] += A_tb[p,k] * (B_j e)[k]     (row p = tid)
+//     threads 128..255: C^c_ref[q] += (e^T A_i)[k] * B_tb[k,q]   (col q = tid-128)
+// i.e. 2 x 128 x 8 extra FMAs per 128 x 128 x 8 k-block (1.6 %).  After the
+// k-loop the tile's row and column sums are reduced (shuffles + shared memory),
+// compared with the references, and a single error is located and corrected
+// from the row checksum.
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace ftg {
+
+constexpr int SB = 128, SK = 8;
+
+__device__ __forceinline__ int simt_inj_lower(const DevInject* inj, int n, int t) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (inj[mid].tile < t) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ float simt_fault(float x, const DevInject& f) {
+    if (f.mode == FTGEMM_INJ_ADD) return x + f.addend;
+    return __uint_as_float(__float_as_uint(x) ^ (1u << (f.bit & 31)));
+}
+
+template <bool FT>
+__global__ void __launch_bounds__(256, 2) simt_ftgemm_kernel(const SimtArgs a) {
+    __shared__ __align__(16) float As[2][SK][SB];      // A tile, k-major (transposed)
+    __shared__ __align__(16) float Bs[2][SK][SB];
+    __shared__ float acs[2][SK], brs[2][SK];           // e^T A_i, B_j e for the k-block
+    __shared__ float red_col[8][SB];                   // column partial sums per warp
+    __shared__ float srow_s[SB], rref_s[SB], cref_s[SB], rres[SB], rtau[SB], cres[SB], ctau[SB];
+    __shared__ int sflag[5];
+    __shared__ DevInject sinj[8];
+    __shared__ int s_ninj;
+
+    const int tid = threadIdx.x;
+    const int tx = tid & 15, ty = tid >> 4;
+    // tile raster: group 8 M-tiles for L2 reuse
+    int ti, tj;
+    {
+        const int t = blockIdx.x;
+        constexpr int G = 8;
+        const int per = G * a.tiles_n;
+        const int grp = t / per, first = grp * G;
+        const int gsz = min(G, a.tiles_m - first);
+        const int loc = t - grp * per;
+        ti = first + loc % gsz;
+        tj = loc / gsz;
+    }
+    const int tile = ti * a.tiles_n + tj;
+    const int r0 = ti * SB, c0 = tj * SB;
+    const int bm = min(SB, a.M - r0), bn = min(SB, a.N - c0);
+
+    // faults of this tile (at most 8 handled per tile; the host enforces it)
+    if (FT && tid == 0) {
+        int n = 0;
+        if (a.n_inj > 0) {
+            const int lo = simt_inj_lower(a.inj, a.n_inj, tile);
+            const int hi = simt_inj_lower(a.inj, a.n_inj, tile + 1);
+            for (int i = lo; i < hi && n < 8; ++i) sinj[n++] = a.inj[i];
+        }
+        s_ninj = n;
+    }
+
+    // global -> register staging for one k-block
+    const int a_row = tid >> 1, a_k = (tid & 1) * 4;     // 128 rows x 8 k
+    const int b_k = tid >> 5, b_col = (tid & 31) * 4;    // 8 k x 128 cols
+    float4 ra, rb;
+    float rchk = 0.0f;
+    auto load_regs = [&](int kb) {
+        const int k0 = kb * SK;
+        const int gr = r0 + a_row, gk = k0 + a_k;
+        if (gr < a.M && gk + 3 < a.K) {
+            ra = __ldg(reinterpret_cast<const float4*>(a.A + (int64_t)gr * a.lda + gk));
+        } else {
+            float t4[4];
+            for (int e = 0; e < 4; ++e) t4[e] = (gr < a.M && gk + e < a.K) ? __ldg(a.A + (int64_t)gr * a.lda + gk + e) : 0.0f;
+            ra = make_float4(t4[0], t4[1], t4[2], t4[3]);
+        }
+        const int bk = k0 + b_k, gc = c0 + b_col;
+        if (bk < a.K && gc + 3 < a.N) {
+            rb = __ldg(reinterpret_cast<const float4*>(a.B + (int64_t)bk * a.ldb + gc));
+        } else {
+            float t4[4];
+            for (int e = 0; e < 4; ++e) t4[e] = (bk < a.K && gc + e < a.N) ? __ldg(a.B + (int64_t)bk * a.ldb + gc + e) : 0.0f;
+            rb = make_float4(t4[0], t4[1], t4[2], t4[3]);
+        }
+        if (FT) {
+            if (tid < SK) rchk = __ldg(a.Ac + (int64_t)ti * a.kp + k0 + tid);
+            else if (tid < 2 * SK) rchk = __ldg(a.Br + (int64_t)tj * a.kp + k0 + tid - SK);
+        }
+    };
+    auto store_regs = [&](int buf) {
+        As[buf][a_k + 0][a_row] = ra.x;
+        As[buf][a_k + 1][a_row] = ra.y;
+        As[buf][a_k + 2][a_row] = ra.z;
+        As[buf][a_k + 3][a_row] = ra.w;
+        *reinterpret_cast<float4*>(&Bs[buf][b_k][b_col]) = rb;
+        if (FT) {
+            if (tid < SK) acs[buf][tid] = rchk;
+            else if (tid < 2 * SK) brs[buf][tid - SK] = rchk;
+        }
+    };
+
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+    float ref = 0.0f;   // row ref (tid < 128) or col ref (tid >= 128)
+
+    load_regs(0);
+    store_regs(0);
+    __syncthreads();
+    int ninj = FT ? s_ninj : 0;
+    int next_inj = 0;
+
+    for (int kb = 0; kb < a.num_kb; ++kb) {
+        const int buf = kb & 1;
+        if (kb + 1 < a.num_kb) load_regs(kb + 1);
+#pragma unroll
+        for (int k = 0; k < SK; ++k) {
+            const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][k][ty * 4]);
+            const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][k][64 + ty * 4]);
+            const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][k][tx * 4]);
+            const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][k][64 + tx * 4]);
+            const float af[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float bf[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(af[i], bf[j], acc[i][j]);
+            if (FT) {
+                if (tid < SB) ref = fmaf(As[buf][k][tid], brs[buf][k], ref);
+                else ref = fmaf(acs[buf][k], Bs[buf][k][tid - SB], ref);
+            }
+        }
+        // fault injection after this k-block, warp-uniform check
+        if (FT) {
+            while (next_inj < ninj && sinj[next_inj].kb == kb) {
+                const DevInject f = sinj[next_inj];
+                if (f.target == FTGEMM_TGT_ACC) {
+                    const int pi = f.p, qj = f.q;
+                    const int ii = (pi & 64) ? 4 + ((pi - 64) - ty * 4) : (pi - ty * 4);
+                    const int jj = (qj & 64) ? 4 + ((qj - 64) - tx * 4) : (qj - tx * 4);
+                    const bool own_r = ((pi & 63) >> 2) == ty, own_c = ((qj & 63) >> 2) == tx;
+                    if (own_r && own_c) {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i)
+#pragma unroll
+                            for (int j = 0; j < 8; ++j)
+                                if (i == ii && j == jj) acc[i][j] = simt_fault(acc[i][j], f);
+                    }
+                } else if (f.target == FTGEMM_TGT_ROW_REF) {
+                    if (tid == f.p) ref = simt_fault(ref, f);
+                } else {
+                    if (tid == SB + f.q) ref = simt_fault(ref, f);
+                }
+                ++next_inj;
+            }
+        }
+        if (kb + 1 < a.num_kb) store_regs(buf ^ 1);
+        __syncthreads();
+    }
+
+    int kind = 0, pstar = -1, qstar = -1;
+    if (FT) {
+        // ---- verification ----
+        if (tid == 0) { sflag[0] = 0; sflag[1] = 0; sflag[2] = 1 << 30; sflag[3] = 1 << 30; }
+        float rs[8], cs[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            float s = 0.0f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) s += acc[i][j];
+            rs[i] = s;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float s = 0.0f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) s += acc[i][j];
+            cs[j] = s;
+        }
+        // rows: reduce across the 16 tx of the same ty (same warp, lanes xor 1..8)
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int o = 1; o < 16; o <<= 1) rs[i] += __shfl_xor_sync(0xffffffffu, rs[i], o);
+        // cols: reduce ty pairs inside the warp (xor 16), then across 8 warps via smem
+#pragma unroll
+        for (int j = 0; j < 8; ++j) cs[j] += __shfl_xor_sync(0xffffffffu, cs[j], 16);
+        const int wid = tid >> 5;
+        if (tx == 0) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) srow_s[(i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4)] = rs[i];
+        }
+        if ((tid & 31) < 16) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) red_col[wid][(j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4)] = cs[j];
+        }
+        if (tid < SB) rref_s[tid] = ref; else cref_s[tid - SB] = ref;
+        __syncthreads();
+        if (tid < SB) {
+            const int p = tid;
+            if (p < bm) {
+                const float rr = ref;
+                const float r = srow_s[p] - rr;
+                const float tr = a.tau_u * (a.tau_l1 * a.sqrtK * fabsf(rr) +
+                                            a.tau_l2 * __ldg(a.rownorm + r0 + p) * __ldg(a.brnorm + tj));
+                rres[p] = r; rtau[p] = tr;
+                if (!(fabsf(r) <= tr)) { atomicAdd(&sflag[0], 1); atomicMin(&sflag[2], p); }
+            }
+        } else {
+            const int q = tid - SB;
+            if (q < bn) {
+                float sc = 0.0f;
+#pragma unroll
+                for (int w = 0; w < 8; ++w) sc += red_col[w][q];
+                const float rc = ref;
+                const float c = sc - rc;
+                const float tc = a.tau_u * (a.tau_l1 * a.sqrtK * fabsf(rc) +
+                                            a.tau_l2 * __ldg(a.acnorm + ti) * __ldg(a.colnorm + c0 + q));
+                cres[q] = c; ctau[q] = tc;
+                if (!(fabsf(c) <= tc)) { atomicAdd(&sflag[1], 1); atomicMin(&sflag[3], q); }
+            }
+        }
+        __syncthreads();
+        const int nr = sflag[0], nc = sflag[1];
+        pstar = nr ? sflag[2] : -1;
+        qstar = nc ? sflag[3] : -1;
+        if (nr == 1 && nc == 1) {
+            const float rr = rres[pstar], cc = cres[qstar];
+            const float big = fmaxf(fabsf(rr), fabsf(cc));
+            const float guard = rtau[pstar] + ctau[qstar] + 2.0f * a.tau_u * (float)(bm + bn) * big;
+            const bool consistent = !(fabsf(rr - cc) > guard);
+            kind = consistent ? (a.ft_level == FTGEMM_FT_CORRECT ? FTGEMM_EV_CORRECTED : FTGEMM_EV_LOCATED)
+                              : FTGEMM_EV_UNCORRECTABLE;
+        } else if ((nr == 1 && nc == 0) || (nr == 0 && nc == 1)) {
+            kind = FTGEMM_EV_CHECKSUM_ONLY;
+        } else if (nr || nc) {
+            kind = FTGEMM_EV_UNCORRECTABLE;
+        }
+        if (kind == FTGEMM_EV_CORRECTED) {
+            // exclusive row sum of p*, reconstruct acc[p*, q*] = ref_row - sum_{q != q*}
+            const bool own_r = ((pstar & 63) >> 2) == ty;
+            const int ii = (pstar & 64) ? 4 + ((pstar - 64) - ty * 4) : (pstar - ty * 4);
+            float part = 0.0f;
+            if (own_r) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    if (i == ii) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const int q = (j < 4) ? tx * 4 + j : 64 + tx * 4 + j - 4;
+                            if (q != qstar) part += acc[i][j];
+                        }
+                    }
+            }
+#pragma unroll
+            for (int o = 1; o < 16; o <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+            const bool own_c = ((qstar & 63) >> 2) == tx;
+            const int jj = (qstar & 64) ? 4 + ((qstar - 64) - tx * 4) : (qstar - tx * 4);
+            if (own_r && own_c) {
+                const float val = rref_s[pstar] - part;
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (i == ii && j == jj) acc[i][j] = val;
+            }
+        }
+        if (tid == 0) {
+            unsigned long long* cnt = a.rep->counts;
+            atomicAdd(&cnt[CNT_CHECKED], 1ull);
+            if (kind) {
+                atomicAdd(&cnt[CNT_DETECTED], 1ull);
+                const int ci = kind == FTGEMM_EV_CORRECTED ? CNT_CORRECTED
+                             : kind == FTGEMM_EV_CHECKSUM_ONLY ? CNT_CHECKSUM_ONLY
+                             : kind == FTGEMM_EV_LOCATED ? CNT_LOCATED : CNT_UNCORRECTABLE;
+                atomicAdd(&cnt[ci], 1ull);
+                const unsigned long long slot = atomicAdd(&cnt[CNT_EVENTS], 1ull);
+                if (slot < (unsigned long long)kMaxEvents) {
+                    ftgemm_event_t& e = a.rep->events[slot];
+                    e.row = pstar >= 0 ? (int64_t)(r0 + pstar) : -1;
+                    e.col = qstar >= 0 ? (int64_t)(c0 + qstar) : -1;
+                    e.tile_m = ti; e.tile_n = tj; e.kind = kind;
+                    e.n_rows = nr; e.n_cols = nc; e.reserved = 0;
+                    e.resid_row = pstar >= 0 ? rres[pstar] : 0.0f;
+                    e.resid_col = qstar >= 0 ? cres[qstar] : 0.0f;
+                    e.tau_row = pstar >= 0 ? rtau[pstar] : 0.0f;
+                    e.tau_col = qstar >= 0 ? ctau[qstar] : 0.0f;
+                } else {
+                    atomicAdd(&cnt[CNT_DROPPED], 1ull);
+                }
+            }
+        }
+    }
+
+    // ---- epilogue: C = fmaf(alpha, acc, beta * C_in) ----
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int p = (i < 4) ? ty * 4 + i : 64 + ty * 4 + i - 4;
+        const int gr = r0 + p;
+        if (p >= bm) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int q = h * 64 + tx * 4;
+            const int gc = c0 + q;
+            float* Cp = a.C + (int64_t)gr * a.ldc + gc;
+            float o[4];
+            if (q + 3 < bn) {
+                float4 cin = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (a.beta != 0.0f) cin = *reinterpret_cast<const float4*>(Cp);
+                const float ci[4] = {cin.x, cin.y, cin.z, cin.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) o[j] = fmaf(a.alpha, acc[i][h * 4 + j], a.beta != 0.0f ? a.beta * ci[j] : 0.0f);
+                *reinterpret_cast<float4*>(Cp) = make_float4(o[0], o[1], o[2], o[3]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (q + j < bn) Cp[j] = fmaf(a.alpha, acc[i][h * 4 + j], a.beta != 0.0f ? a.beta * Cp[j] : 0.0f);
+            }
+        }
+    }
+}
+
+cudaError_t launch_simt(bool ft, const SimtArgs& a, cudaStream_t st) {
+    const int grid = a.tiles_m * a.tiles_n;
+    if (ft) simt_ftgemm_kernel<true><<<grid, 256, 0, st>>>(a);
+    else simt_ftgemm_kernel<false><<<grid, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace ftg

@@ -1,0 +1,545 @@
+// tc_gemm.cu -- fused online-ABFT GEMM on the 5th-generation tensor cores
+// (tcgen05 / TMEM / TMA) for sm_100a, BF16 and TF32 operands, FP32 accumulate.
+//
+// The paper's threadblock-level fused ABFT (section 4.2.3,
+// Fig. tb_abft) re-derived for tcgen05: instead of carrying e^T A B and A B e in
+// registers next to a SIMT outer product, the checksum vectors are APPENDED to
+// the MMA operand tiles, so the single tensor-core mainloop that computes C
+// also computes the carried references (Eq. (3)):
+//
+//     A tile (128 x BK, K-major)     rows 0..124  = A data (TMA)
+//                                    rows 125..127 = Y_i = split(e^T A_i)  (encode)
+//     B tile (BK x BN, N-major)      cols 0..BN-5  = B data (TMA)
+//                                    cols BN-4..BN-2 = X_j = split(B_j e),  col BN-1 = 0
+//     D = A_tile * B_tile in TMEM  =  [[ C_ij , C_ij^r (3 partial cols) ],
+//                                      [ C_ij^c (3 partial rows), unused ]]
+//
+// so the check tile is 125 x (BN-4) data elements and verification needs no
+// extra MMA instructions.  Warp roles (one CTA per SM, persistent):
+//   warp 0      TMA producer (A box 128 rows, B boxes of 128 bytes x BK)
+//   warp 1      MMA issuer (one elected thread, tcgen05.mma, commits)
+//   warp 2      TMEM allocator
+//   warp 3      checksum fix-up (FT): writes Y rows / X columns into the landed
+//               stage (swizzled), then releases it to the MMA
+//   warps 4..7  epilogue: TMEM -> registers; row sums (thread = row), column
+//               sums (warp transpose-reduce + smem), residuals vs thresholds,
+//               locate, correct, alpha/beta, store;
+//               also service mid-mainloop fault injections
+// The accumulator is double-buffered in TMEM (2 x BN columns), so the epilogue
+// of tile t (verification included) overlaps the mainloop of tile t+1.
+#include <cstdint>
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace ftg {
+
+template <bool kTF32, int BN_, bool FT>
+struct TcCfg {
+    static constexpr int BM = 128;
+    static constexpr int BN = BN_;
+    static constexpr int ELT = kTF32 ? 4 : 2;
+    static constexpr int BK = 128 / ELT;           // one 128-byte swizzle row of K
+    static constexpr int UK = 32 / ELT;            // K per tcgen05.mma
+    static constexpr int BOXN = 128 / ELT;         // B columns per TMA box
+    static constexpr int NBOX = BN / BOXN;
+    static constexpr int A_BYTES = BM * 128;
+    static constexpr int B_BOX_BYTES = BK * 128;
+    static constexpr int B_BYTES = NBOX * B_BOX_BYTES;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int STAGES = (BN == 256) ? 4 : 6;
+    static constexpr int BMD = FT ? BM - 3 : BM;   // data rows of a check tile
+    static constexpr int BND = FT ? BN - 4 : BN;   // data cols of a check tile
+    static constexpr int TMEM_COLS = 2 * BN;
+    static constexpr int NCHUNK = BN / 32;
+    // epilogue shared memory
+    static constexpr int STG_FLOATS = 4 * 32 * 33;
+    static constexpr int EPI_BYTES = (STG_FLOATS + 4 * BN + BN + 2 * BN + 2 * BM) * 4 + 64;
+    static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 256;
+};
+
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& ti, int& tj) {
+    constexpr int G = 16;   // group of M-tiles swept together (L2 reuse of B)
+    const int per_group = G * tiles_n;
+    const int grp = t / per_group;
+    const int first = grp * G;
+    const int gsz = min(G, tiles_m - first);
+    const int loc = t - grp * per_group;
+    ti = first + loc % gsz;
+    tj = loc / gsz;
+}
+
+// first index of inj[] with tile >= t (inj sorted by tile, then kb)
+__device__ __forceinline__ int inj_lower(const DevInject* inj, int n, int t) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (inj[mid].tile < t) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ float transpose_reduce32(float (&w)[32], uint32_t lane) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        const bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < off; ++i) {
+            float send = upper ? w[i] : w[i + off];
+            float keep = upper ? w[i + off] : w[i];
+            w[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+    return w[0];
+}
+
+// Column offset of the data inside the MMA tile of check-tile column tj.
+// BF16 check tiles are 252 columns wide (BN-4) but TMA boxes must start on a
+// 16-byte (8-element) boundary, so tile starts alternate between 0 and 4 mod 8:
+// even tiles load [col0, col0+BN) and carry X in MMA columns BN-4..BN-1; odd
+// tiles load [col0-4, col0+BN-4) and carry X in MMA columns 0..3.  TF32 tiles
+// (1008-byte starts) never need the shift.
+template <bool kTF32, bool FT>
+__device__ __forceinline__ int data_off(int tj) { return (FT && !kTF32 && (tj & 1)) ? 4 : 0; }
+
+__device__ __forceinline__ uint32_t apply_fault(uint32_t bits, const DevInject& f) {
+    if (f.mode == FTGEMM_INJ_ADD) return __float_as_uint(__uint_as_float(bits) + f.addend);
+    return bits ^ (1u << (f.bit & 31));
+}
+
+template <bool kTF32, int BN, bool FT>
+__global__ void __launch_bounds__(256, 1)
+tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcArgs a) {
+    using Cfg = TcCfg<kTF32, BN, FT>;
+    constexpr int S = Cfg::STAGES;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* stage_base = smem;
+    float* stg = reinterpret_cast<float*>(smem + S * Cfg::STAGE_BYTES);       // [4][32][33]
+    float* colsum = stg + Cfg::STG_FLOATS;                                    // [4][BN]
+    float* refsum = colsum + 4 * BN;                                          // [BN]
+    float* cres = refsum + BN;                                                // [BN]
+    float* ctau = cres + BN;                                                  // [BN]
+    float* rres = ctau + BN;                                                  // [BM]
+    float* rtau = rres + Cfg::BM;                                             // [BM]
+    int* sflag = reinterpret_cast<int*>(rtau + Cfg::BM);                      // nr, nc, p*, q*, corr
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * Cfg::STAGE_BYTES + Cfg::EPI_BYTES);
+    uint64_t* full = bars;              // [S]  MMA may consume
+    uint64_t* empty = bars + S;         // [S]  producer may refill
+    uint64_t* tfull = bars + 2 * S;     // [S]  TMA landed (FT: fix-up may write)
+    uint64_t* tm_full = bars + 3 * S;   // [2]
+    uint64_t* tm_empty = tm_full + 2;   // [2]
+    uint64_t* inj_req = tm_empty + 2;
+    uint64_t* inj_done = inj_req + 1;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(inj_done + 1);
+
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lane = lane_id();
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+            mbar_init(&tfull[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tm_full[b], 1);
+            mbar_init(&tm_empty[b], 4);
+        }
+        mbar_init(inj_req, 1);
+        mbar_init(inj_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<Cfg::TMEM_COLS>(tmem_holder);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer ----
+        if (lane == 0) {
+            int s = 0; uint32_t ph = 0;
+            // The A box always spans the full 128 MMA rows: in FT mode rows 125..127
+            // (the next tile's first rows) are overwritten by the fix-up warp with the
+            // checksum rows once the TMA has landed (TMA boxes cannot end mid swizzle atom).
+            constexpr uint32_t bytes = Cfg::A_BYTES + Cfg::B_BYTES;
+            for (int t = blockIdx.x; t < a.num_tiles; t += gridDim.x) {
+                int ti, tj;
+                tile_coords(t, a.tiles_m, a.tiles_n, ti, tj);
+                const int row0 = ti * Cfg::BMD;
+                const int col0 = tj * Cfg::BND - data_off<kTF32, FT>(tj);
+                for (int kb = 0; kb < a.num_kb; ++kb) {
+                    mbar_wait(&empty[s], ph ^ 1);
+                    uint64_t* bar = FT ? &tfull[s] : &full[s];
+                    mbar_arrive_expect_tx(bar, bytes);
+                    uint8_t* sa = stage_base + s * Cfg::STAGE_BYTES;
+                    uint8_t* sb = sa + Cfg::A_BYTES;
+                    tma_load_2d(sa, &tmA, bar, kb * Cfg::BK, row0);
+#pragma unroll
+                    for (int b = 0; b < Cfg::NBOX; ++b)
+                        tma_load_2d(sb + b * Cfg::B_BOX_BYTES, &tmB, bar, col0 + b * Cfg::BOXN, kb * Cfg::BK);
+                    if (++s == S) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------- MMA issuer -----
+        if (lane == 0) {
+            constexpr uint32_t idesc = instr_desc(kTF32, Cfg::BM, BN, false, true);
+            int s = 0; uint32_t ph = 0; uint32_t injph = 0;
+            int lt = 0;
+            for (int t = blockIdx.x; t < a.num_tiles; t += gridDim.x, ++lt) {
+                const int acc = lt & 1;
+                const uint32_t accph = (lt >> 1) & 1;
+                mbar_wait(&tm_empty[acc], accph ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem_base + acc * BN;
+                int ii = 0, ie = 0;
+                if (FT && a.n_inj > 0) {
+                    ii = inj_lower(a.inj, a.n_inj, t);
+                    ie = inj_lower(a.inj, a.n_inj, t + 1);
+                }
+                for (int kb = 0; kb < a.num_kb; ++kb) {
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(stage_base + s * Cfg::STAGE_BYTES);
+                    const uint32_t sb = sa + Cfg::A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < Cfg::BK / Cfg::UK; ++kk) {
+                        const uint64_t ad = smem_desc_sw128(sa + kk * 32, 16, 1024);
+                        // B is N-major: bf16 -> SW128 (8-row atoms), tf32 -> SW128_BASE32B (4-row atoms)
+                        const uint64_t bd = kTF32
+                            ? smem_desc_sw128<1>(sb + kk * Cfg::UK * 128, Cfg::B_BOX_BYTES, 512)
+                            : smem_desc_sw128<2>(sb + kk * Cfg::UK * 128, Cfg::B_BOX_BYTES, 1024);
+                        umma<kTF32>(d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                    }
+                    umma_commit(&empty[s]);
+                    if (FT && ii < ie && a.inj[ii].kb == kb) {
+                        // hand the accumulator to the epilogue warps for the fault(s)
+                        umma_commit(inj_req);
+                        mbar_wait(inj_done, injph);
+                        injph ^= 1;
+                        tc_fence_after();
+                        while (ii < ie && a.inj[ii].kb == kb) ++ii;
+                    }
+                    if (++s == S) { s = 0; ph ^= 1; }
+                }
+                umma_commit(&tm_full[acc]);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 3) {
+        // ------------------------------------------- checksum fix-up (FT) --
+        if constexpr (FT) {
+            int s = 0; uint32_t ph = 0;
+            for (int t = blockIdx.x; t < a.num_tiles; t += gridDim.x) {
+                int ti, tj;
+                tile_coords(t, a.tiles_m, a.tiles_n, ti, tj);
+                for (int kb = 0; kb < a.num_kb; ++kb) {
+                    // Y rows: 3 rows x 128 bytes, lanes 0..23 one 16-byte chunk each
+                    uint4 yv = make_uint4(0, 0, 0, 0);
+                    const int yr = lane >> 3, ych = lane & 7;
+                    if (lane < 24) {
+                        const uint8_t* src = reinterpret_cast<const uint8_t*>(a.Y) +
+                            (((int64_t)ti * 3 + yr) * a.kp + (int64_t)kb * Cfg::BK) * Cfg::ELT + ych * 16;
+                        yv = __ldg(reinterpret_cast<const uint4*>(src));
+                    }
+                    // X: per k-row 4 values (hi, mid, lo, 0)
+                    uint2 xv0 = make_uint2(0, 0), xv1 = make_uint2(0, 0);
+                    uint4 xq = make_uint4(0, 0, 0, 0);
+                    if constexpr (!kTF32) {
+                        const uint16_t* src = reinterpret_cast<const uint16_t*>(a.X) + ((int64_t)tj * a.kp + (int64_t)kb * Cfg::BK) * 4;
+                        xv0 = __ldg(reinterpret_cast<const uint2*>(src + lane * 4));
+                        xv1 = __ldg(reinterpret_cast<const uint2*>(src + (lane + 32) * 4));
+                    } else {
+                        const float* src = reinterpret_cast<const float*>(a.X) + ((int64_t)tj * a.kp + (int64_t)kb * Cfg::BK) * 4;
+                        xq = __ldg(reinterpret_cast<const uint4*>(src + lane * 4));
+                    }
+                    mbar_wait(&tfull[s], ph);
+                    if (a.dbg & 1) { __syncwarp(); if (lane == 0) mbar_arrive(&full[s]); if (++s == S) { s = 0; ph ^= 1; } continue; }
+                    uint8_t* sa = stage_base + s * Cfg::STAGE_BYTES;
+                    const bool xfirst = data_off<kTF32, FT>(tj) != 0;   // X in MMA cols 0..3
+                    uint8_t* sb_x = sa + Cfg::A_BYTES + (xfirst ? 0 : (Cfg::NBOX - 1) * Cfg::B_BOX_BYTES);
+                    if (lane < 24) {
+                        const int row = Cfg::BMD + yr;
+                        *reinterpret_cast<uint4*>(sa + row * 128 + ((ych ^ (row & 7)) << 4)) = yv;
+                    }
+                    if constexpr (!kTF32) {
+                        // X = 8 bytes of a k-row: logical 16-byte chunk 7 bytes 8..15, or chunk 0 bytes 0..7
+                        const int r0 = lane, r1 = lane + 32, lc = xfirst ? 0 : 7, bo = xfirst ? 0 : 8;
+                        *reinterpret_cast<uint2*>(sb_x + r0 * 128 + ((lc ^ (r0 & 7)) << 4) + bo) = xv0;
+                        *reinterpret_cast<uint2*>(sb_x + r1 * 128 + ((lc ^ (r1 & 7)) << 4) + bo) = xv1;
+                    } else {
+                        // 128B_ATOM_32B swizzle: 32-byte chunk index ^= (row & 3); cols BN-4.. are
+                        // bytes 16..31 of logical chunk 3
+                        const int r0 = lane;
+                        *reinterpret_cast<uint4*>(sb_x + r0 * 128 + ((3 ^ (r0 & 3)) << 5) + 16) = xq;
+                    }
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&full[s]);
+                    if (++s == S) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        // ----------------------------------------------------- epilogue -----
+        const int ew = warp - 4;                 // TMEM lane quadrant
+        const int rloc = ew * 32 + (int)lane;    // row of the 128-row tile
+        const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
+        const int et = threadIdx.x - 128;        // 0..127
+        float* mystg = stg + ew * 32 * 33;
+        uint32_t injph = 0;
+        unsigned long long n_checked = 0;
+        int lt = 0;
+        for (int t = blockIdx.x; t < a.num_tiles; t += gridDim.x, ++lt) {
+            int ti, tj;
+            tile_coords(t, a.tiles_m, a.tiles_n, ti, tj);
+            const int r0 = ti * Cfg::BMD, c0 = tj * Cfg::BND;
+            const int bm = min(Cfg::BMD, a.M - r0), bn = min(Cfg::BND, a.N - c0);
+            const int doff = data_off<kTF32, FT>(tj);          // data col q <-> MMA col q + doff
+            const int xoff = doff ? 0 : BN - 4;                // row-reference split columns
+            const int acc = lt & 1;
+            const uint32_t accph = (lt >> 1) & 1;
+            const uint32_t tb = tmem_base + acc * BN;
+
+            // ---- mid-mainloop fault injection ----
+            if (FT && a.n_inj > 0) {
+                int ii = inj_lower(a.inj, a.n_inj, t);
+                const int ie = inj_lower(a.inj, a.n_inj, t + 1);
+                while (ii < ie) {
+                    const int kb = a.inj[ii].kb;
+                    mbar_wait(inj_req, injph);
+                    injph ^= 1;
+                    tc_fence_after();
+                    for (; ii < ie && a.inj[ii].kb == kb; ++ii) {
+                        const DevInject f = a.inj[ii];
+                        int trow, tcol;
+                        if (f.target == FTGEMM_TGT_ROW_REF) { trow = f.p; tcol = xoff; }
+                        else if (f.target == FTGEMM_TGT_COL_REF) { trow = Cfg::BMD; tcol = f.q + doff; }
+                        else { trow = f.p; tcol = f.q + doff; }
+                        if ((trow >> 5) == ew) {
+                            const uint32_t addr = tb + lane_off + (uint32_t)tcol;
+                            uint32_t v = tmem_ld1(addr);
+                            if ((int)lane == (trow & 31)) v = apply_fault(v, f);
+                            tmem_st1(addr, v);
+                        }
+                    }
+                    tc_fence_before();
+                    named_bar_sync(1, 128);
+                    if (et == 0) mbar_arrive(inj_done);
+                }
+            }
+
+            mbar_wait(&tm_full[acc], accph);
+            tc_fence_after();
+
+            int kind = 0, pstar = -1, qstar = -1;
+            float corr = 0.0f;
+            if (FT && !(a.dbg & 2)) {
+                // ---- pass 1: row sums, row refs, column partial sums ----
+                named_bar_sync(1, 128);          // previous tile's readers of sflag are done
+                if (et == 0) { sflag[0] = 0; sflag[1] = 0; sflag[2] = 1 << 30; sflag[3] = 1 << 30; }
+                const bool rvalid = rloc < bm;
+                float srow = 0.0f, rref = 0.0f;
+#pragma unroll 1
+                for (int c = 0; c < Cfg::NCHUNK; ++c) {
+                    float v[32];
+                    tmem_ld32(tb + lane_off + c * 32, v);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const int mcol = c * 32 + i;
+                        if (mcol >= doff && mcol < doff + Cfg::BND) srow += v[i];
+                    }
+                    if (xoff == 0 && c == 0) rref = (v[0] + v[1]) + v[2];
+                    if (xoff != 0 && c == Cfg::NCHUNK - 1) rref = (v[28] + v[29]) + v[30];
+                    float w[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) w[i] = rvalid ? v[i] : 0.0f;
+                    colsum[ew * BN + c * 32 + lane] = transpose_reduce32(w, lane);
+                    if (ew == 3) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) w[i] = (rloc >= Cfg::BMD) ? v[i] : 0.0f;
+                        refsum[c * 32 + lane] = transpose_reduce32(w, lane);
+                    }
+                }
+                named_bar_sync(1, 128);
+                // ---- row residuals ----
+                if (rvalid) {
+                    const float r = srow - rref;
+                    const float tr = a.tau_u * (a.tau_l1 * a.sqrtK * fabsf(rref) +
+                                                a.tau_l2 * __ldg(a.rownorm + r0 + rloc) * __ldg(a.brnorm + tj));
+                    rres[rloc] = r; rtau[rloc] = tr;
+                    if (!(fabsf(r) <= tr)) { atomicAdd(&sflag[0], 1); atomicMin(&sflag[2], rloc); }
+                }
+                // ---- column residuals ----
+                for (int col = et; col < bn; col += 128) {
+                    const int mc = col + doff;
+                    const float sc = (colsum[mc] + colsum[BN + mc]) + (colsum[2 * BN + mc] + colsum[3 * BN + mc]);
+                    const float rc = refsum[mc];
+                    const float c = sc - rc;
+                    const float tc = a.tau_u * (a.tau_l1 * a.sqrtK * fabsf(rc) +
+                                                a.tau_l2 * __ldg(a.acnorm + ti) * __ldg(a.colnorm + c0 + col));
+                    cres[col] = c; ctau[col] = tc;
+                    if (!(fabsf(c) <= tc)) { atomicAdd(&sflag[1], 1); atomicMin(&sflag[3], col); }
+                }
+                named_bar_sync(1, 128);
+                // ---- decide (R3-R5) ----
+                const int nr = sflag[0], nc = sflag[1];
+                pstar = nr ? sflag[2] : -1;
+                qstar = nc ? sflag[3] : -1;
+                if (nr == 1 && nc == 1) {
+                    const float rr = rres[pstar], cc = cres[qstar];
+                    const float big = fmaxf(fabsf(rr), fabsf(cc));
+                    const float guard = rtau[pstar] + ctau[qstar] + 2.0f * a.tau_u * (float)(bm + bn) * big;
+                    const bool consistent = !(fabsf(rr - cc) > guard);
+                    kind = consistent ? (a.ft_level == FTGEMM_FT_CORRECT ? FTGEMM_EV_CORRECTED : FTGEMM_EV_LOCATED)
+                                      : FTGEMM_EV_UNCORRECTABLE;
+                } else if ((nr == 1 && nc == 0) || (nr == 0 && nc == 1)) {
+                    kind = FTGEMM_EV_CHECKSUM_ONLY;
+                } else if (nr || nc) {
+                    kind = FTGEMM_EV_UNCORRECTABLE;
+                }
+                if (kind == FTGEMM_EV_CORRECTED) {
+                    // reconstruct from the row checksum, excluding the bad element
+                    if ((pstar >> 5) == ew) {
+                        float sx = 0.0f;
+#pragma unroll 1
+                        for (int c = 0; c < Cfg::NCHUNK; ++c) {
+                            float v[32];
+                            tmem_ld32(tb + lane_off + c * 32, v);
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) {
+                                const int mcol = c * 32 + i;
+                                if (mcol >= doff && mcol < doff + Cfg::BND && mcol != qstar + doff) sx += v[i];
+                            }
+                        }
+                        if (rloc == pstar) sflag[4] = __float_as_int(rref - sx);
+                    }
+                    named_bar_sync(1, 128);
+                    corr = __int_as_float(sflag[4]);
+                }
+                if (et == 0) {
+                    ++n_checked;
+                    if (kind) {
+                        unsigned long long* cnt = a.rep->counts;
+                        atomicAdd(&cnt[CNT_DETECTED], 1ull);
+                        const int ci = kind == FTGEMM_EV_CORRECTED ? CNT_CORRECTED
+                                     : kind == FTGEMM_EV_CHECKSUM_ONLY ? CNT_CHECKSUM_ONLY
+                                     : kind == FTGEMM_EV_LOCATED ? CNT_LOCATED : CNT_UNCORRECTABLE;
+                        atomicAdd(&cnt[ci], 1ull);
+                        const unsigned long long slot = atomicAdd(&cnt[CNT_EVENTS], 1ull);
+                        if (slot < (unsigned long long)kMaxEvents) {
+                            ftgemm_event_t& e = a.rep->events[slot];
+                            e.row = pstar >= 0 ? (int64_t)(r0 + pstar) : -1;
+                            e.col = qstar >= 0 ? (int64_t)(c0 + qstar) : -1;
+                            e.tile_m = ti; e.tile_n = tj; e.kind = kind;
+                            e.n_rows = nr; e.n_cols = nc; e.reserved = 0;
+                            e.resid_row = pstar >= 0 ? rres[pstar] : 0.0f;
+                            e.resid_col = qstar >= 0 ? cres[qstar] : 0.0f;
+                            e.tau_row = pstar >= 0 ? rtau[pstar] : 0.0f;
+                            e.tau_col = qstar >= 0 ? ctau[qstar] : 0.0f;
+                        } else {
+                            atomicAdd(&cnt[CNT_DROPPED], 1ull);
+                        }
+                    }
+                }
+            }
+
+            // ---- pass 2: alpha/beta epilogue and coalesced store ----
+            const bool do_corr = FT && kind == FTGEMM_EV_CORRECTED && rloc == pstar;
+#pragma unroll 1
+            for (int c = 0; c < Cfg::NCHUNK; ++c) {
+                float v[32];
+                tmem_ld32(tb + lane_off + c * 32, v);
+                if (c == Cfg::NCHUNK - 1) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tm_empty[acc]);
+                }
+                if (do_corr && ((qstar + doff) >> 5) == c) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) if (i == ((qstar + doff) & 31)) v[i] = corr;
+                }
+#pragma unroll
+                for (int i = 0; i < 32; ++i) mystg[lane * 33 + i] = v[i];
+                __syncwarp();
+                const int cl = 2 * (lane & 15);                  // column pair inside the chunk
+                const int col = c * 32 + cl - doff;              // data column inside the tile
+                const int gcol = c0 + col;
+#pragma unroll 4
+                for (int rr = 0; rr < 32; rr += 2) {
+                    const int r = rr + (int)(lane >> 4);
+                    const int trow = ew * 32 + r;
+                    const int grow = r0 + trow;
+                    if (trow < bm && col >= 0 && col < bn) {
+                        float o0 = a.alpha * mystg[r * 33 + cl];
+                        float o1 = a.alpha * mystg[r * 33 + cl + 1];
+                        const bool pair = (col + 1 < bn);
+                        if constexpr (kTF32) {
+                            float* Cp = reinterpret_cast<float*>(a.C) + (int64_t)grow * a.ldc + gcol;
+                            if (a.beta != 0.0f) {
+                                o0 = fmaf(a.beta, Cp[0], o0);
+                                if (pair) o1 = fmaf(a.beta, Cp[1], o1);
+                            }
+                            if (pair) *reinterpret_cast<float2*>(Cp) = make_float2(o0, o1);
+                            else Cp[0] = o0;
+                        } else {
+                            uint16_t* Cp = reinterpret_cast<uint16_t*>(a.C) + (int64_t)grow * a.ldc + gcol;
+                            if (a.beta != 0.0f) {
+                                o0 = fmaf(a.beta, bf16_to_f32(Cp[0]), o0);
+                                if (pair) o1 = fmaf(a.beta, bf16_to_f32(Cp[1]), o1);
+                            }
+                            if (pair) {
+                                const uint32_t pk = (uint32_t)f32_to_bf16_rn(o0) | ((uint32_t)f32_to_bf16_rn(o1) << 16);
+                                *reinterpret_cast<uint32_t*>(Cp) = pk;
+                            } else {
+                                Cp[0] = f32_to_bf16_rn(o0);
+                            }
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        if (FT && et == 0 && n_checked) atomicAdd(&a.rep->counts[CNT_CHECKED], n_checked);
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+    }
+}
+
+// ---------------------------------------------------------------- launch ---
+template <bool kTF32, int BN, bool FT>
+cudaError_t launch_tc_t(const CUtensorMap& mA, const CUtensorMap& mB, const TcArgs& a, cudaStream_t st) {
+    using Cfg = TcCfg<kTF32, BN, FT>;
+    auto kern = tc_ftgemm_kernel<kTF32, BN, FT>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const int grid = a.num_tiles < kNumSMsB200 ? a.num_tiles : kNumSMsB200;
+    kern<<<grid, 256, Cfg::SMEM_BYTES, st>>>(mA, mB, a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tc(bool tf32, int bn, bool ft, const CUtensorMap& mA, const CUtensorMap& mB,
+                      const TcArgs& a, cudaStream_t st) {
+    if (tf32) {
+        if (bn == 256) return ft ? launch_tc_t<true, 256, true>(mA, mB, a, st) : launch_tc_t<true, 256, false>(mA, mB, a, st);
+        return ft ? launch_tc_t<true, 128, true>(mA, mB, a, st) : launch_tc_t<true, 128, false>(mA, mB, a, st);
+    }
+    if (bn == 256) return ft ? launch_tc_t<false, 256, true>(mA, mB, a, st) : launch_tc_t<false, 256, false>(mA, mB, a, st);
+    return ft ? launch_tc_t<false, 128, true>(mA, mB, a, st) : launch_tc_t<false, 128, false>(mA, mB, a, st);
+}
+
+}  // namespace ftg

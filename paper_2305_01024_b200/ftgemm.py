@@ -1,0 +1,243 @@
+"""Thin Python binding of libftgemm (include/ftgemm.h) — argument marshalling only.
+
+Every step of the path runs in the CUDA kernels behind the C ABI; this module
+converts torch tensors to device pointers / sizes / streams and ctypes structs
+back to Python objects.  There is no CPU fallback: if the shared library is
+missing or the device is not an sm_100 GPU, calls raise.
+
+PyTorch is used only for device memory (the workspaces are torch tensors) and
+streams (torch.cuda.current_stream()).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libftgemm.so")
+
+F32_SIMT, TF32, BF16 = 0, 1, 2
+DTYPES = {"f32_simt": F32_SIMT, "tf32": TF32, "bf16": BF16}
+FT_OFF, FT_DETECT, FT_CORRECT = 0, 1, 2
+INJ_FLIP, INJ_ADD = 0, 1
+TGT_ACC, TGT_ROW_REF, TGT_COL_REF = 0, 1, 2
+EV_CORRECTED, EV_CHECKSUM_ONLY, EV_UNCORRECTABLE, EV_LOCATED = 1, 2, 3, 4
+ERR = {0: "OK", 1: "INVALID_VALUE", 2: "UNSUPPORTED", 3: "CUDA"}
+
+
+class Inject(C.Structure):
+    _fields_ = [("row", C.c_int64), ("col", C.c_int64), ("k_elem", C.c_int64),
+                ("bit", C.c_int32), ("mode", C.c_int32), ("target", C.c_int32), ("addend", C.c_float)]
+
+
+class Event(C.Structure):
+    _fields_ = [("row", C.c_int64), ("col", C.c_int64), ("tile_m", C.c_int32), ("tile_n", C.c_int32),
+                ("kind", C.c_int32), ("n_rows", C.c_int32), ("n_cols", C.c_int32), ("reserved", C.c_int32),
+                ("resid_row", C.c_float), ("resid_col", C.c_float), ("tau_row", C.c_float), ("tau_col", C.c_float)]
+
+
+class Counts(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("tiles_checked", "tiles_detected", "corrected", "checksum_only",
+                                         "uncorrectable", "located", "events", "dropped")]
+
+
+class PlanStruct(C.Structure):
+    _fields_ = [("dtype", C.c_int32), ("shape_class", C.c_int32), ("bm", C.c_int32), ("bn", C.c_int32),
+                ("bk", C.c_int32), ("check_tile_m", C.c_int32), ("check_tile_n", C.c_int32),
+                ("off_tile_m", C.c_int32), ("off_tile_n", C.c_int32), ("stages", C.c_int32),
+                ("cta_group", C.c_int32), ("max_events", C.c_int32), ("max_inject", C.c_int32),
+                ("pad0", C.c_int32), ("tiles_m", C.c_int64), ("tiles_n", C.c_int64), ("enc_bytes", C.c_int64),
+                ("enc_b_offset", C.c_int64), ("enc_b_bytes", C.c_int64), ("report_bytes", C.c_int64),
+                ("u_acc", C.c_float), ("lambda1", C.c_float), ("lambda2", C.c_float), ("pad1", C.c_int32)]
+
+
+SYMBOLS = ("ftgemm_plan", "ftgemm_encode", "ftgemm_run", "ftgemm_report", "ftgemm_report_reset",
+           "ftgemm_last_error", "ftgemm_version", "ftgemm_device_arch")
+
+_lib = None
+
+
+def lib():
+    """Load libftgemm.so (raises if it has not been built — no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2305_01024_b200.build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        i64, i32, vp = C.c_int64, C.c_int32, C.c_void_p
+        L.ftgemm_plan.argtypes = [C.c_int, i64, i64, i64, C.POINTER(PlanStruct)]
+        L.ftgemm_encode.argtypes = [C.c_int, i64, i64, i64, vp, i64, vp, i64, vp, C.c_int, vp]
+        L.ftgemm_run.argtypes = [C.c_int, i64, i64, i64, C.c_float, vp, i64, vp, i64, C.c_float, vp, i64,
+                                 vp, C.c_int, vp, i32, vp, vp]
+        L.ftgemm_report.argtypes = [vp, C.POINTER(Counts), vp, i32, vp]
+        L.ftgemm_report_reset.argtypes = [vp, i64, vp]
+        L.ftgemm_last_error.restype = C.c_char_p
+        for n in SYMBOLS:
+            if n != "ftgemm_last_error":
+                getattr(L, n).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+class FtgemmError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        msg = lib().ftgemm_last_error().decode()
+        super().__init__(f"{where}: {ERR.get(code, code)}: {msg}")
+        self.code = code
+
+
+def _check(code: int, where: str):
+    if code != 0:
+        raise FtgemmError(code, where)
+
+
+def _dt(dtype) -> int:
+    return DTYPES[dtype] if isinstance(dtype, str) else int(dtype)
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+@dataclass
+class Plan:
+    dtype: int
+    shape_class: int
+    bm: int
+    bn: int
+    bk: int
+    check_tile_m: int
+    check_tile_n: int
+    off_tile_m: int
+    off_tile_n: int
+    stages: int
+    cta_group: int
+    max_events: int
+    max_inject: int
+    tiles_m: int
+    tiles_n: int
+    enc_bytes: int
+    enc_b_offset: int
+    enc_b_bytes: int
+    report_bytes: int
+    u_acc: float
+    lambda1: float
+    lambda2: float
+
+
+def plan(dtype, M: int, N: int, K: int) -> Plan:
+    p = PlanStruct()
+    _check(lib().ftgemm_plan(_dt(dtype), M, N, K, C.byref(p)), "ftgemm_plan")
+    return Plan(**{f: getattr(p, f) for f in Plan.__dataclass_fields__})
+
+
+def alloc_workspaces(pl: Plan, device="cuda"):
+    """enc_ws and report_ws as torch device tensors (PyTorch owns device memory)."""
+    enc = torch.empty(max(pl.enc_bytes, 256), dtype=torch.uint8, device=device)
+    rep = torch.zeros(pl.report_bytes, dtype=torch.uint8, device=device)
+    return enc, rep
+
+
+def encode(dtype, A: torch.Tensor | None, B: torch.Tensor | None, enc_ws: torch.Tensor, *, M: int, N: int, K: int,
+           which: int = 3, stream=None):
+    _check(lib().ftgemm_encode(_dt(dtype), M, N, K,
+                               A.data_ptr() if A is not None else None, A.stride(0) if A is not None else K,
+                               B.data_ptr() if B is not None else None, B.stride(0) if B is not None else N,
+                               enc_ws.data_ptr(), which, _stream(stream)), "ftgemm_encode")
+
+
+def _inj_array(injections):
+    inj = list(injections or ())
+    if not inj:
+        return None, 0
+    arr = (Inject * len(inj))()
+    for i, x in enumerate(inj):
+        if isinstance(x, dict):
+            x = (x["row"], x["col"], x["k_elem"], x.get("bit", 0), x.get("mode", INJ_FLIP),
+                 x.get("target", TGT_ACC), x.get("addend", 0.0))
+        arr[i] = Inject(*x)
+    return arr, len(inj)
+
+
+def run(dtype, A: torch.Tensor, B: torch.Tensor, C_: torch.Tensor, *, alpha: float = 1.0, beta: float = 0.0,
+        enc_ws: torch.Tensor | None = None, ft_level: int = FT_CORRECT, injections=(),
+        report_ws: torch.Tensor | None = None, stream=None):
+    M, K = A.shape
+    N = B.shape[1]
+    arr, n = _inj_array(injections)
+    _check(lib().ftgemm_run(_dt(dtype), M, N, K, alpha, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0),
+                            beta, C_.data_ptr(), C_.stride(0),
+                            enc_ws.data_ptr() if enc_ws is not None else None, ft_level,
+                            C.cast(arr, C.c_void_p) if arr is not None else None, n,
+                            report_ws.data_ptr() if report_ws is not None else None, _stream(stream)),
+           "ftgemm_run")
+
+
+def report(report_ws: torch.Tensor, max_events: int = 4096, stream=None):
+    cnt = Counts()
+    evs = (Event * max(1, max_events))()
+    _check(lib().ftgemm_report(report_ws.data_ptr(), C.byref(cnt), C.cast(evs, C.c_void_p), max_events,
+                               _stream(stream)), "ftgemm_report")
+    counts = {f: getattr(cnt, f) for f, _ in Counts._fields_}
+    out = []
+    for i in range(min(counts["events"], max_events)):
+        e = evs[i]
+        out.append(dict(row=e.row, col=e.col, tile_m=e.tile_m, tile_n=e.tile_n, kind=e.kind, n_rows=e.n_rows,
+                        n_cols=e.n_cols, resid_row=e.resid_row, resid_col=e.resid_col, tau_row=e.tau_row,
+                        tau_col=e.tau_col))
+    out.sort(key=lambda e: (e["tile_m"], e["tile_n"], e["kind"], e["row"], e["col"]))
+    return counts, out
+
+
+def report_reset(report_ws: torch.Tensor, stream=None):
+    _check(lib().ftgemm_report_reset(report_ws.data_ptr(), report_ws.numel(), _stream(stream)), "ftgemm_report_reset")
+
+
+class FTGemm:
+    """Convenience object: plan + workspaces for one (dtype, M, N, K).
+
+    g = FTGemm("bf16", M, N, K); g.encode(A, B); g.run(A, B, C); counts, events = g.report()
+    """
+
+    def __init__(self, dtype, M: int, N: int, K: int, device="cuda"):
+        self.dtype = _dt(dtype)
+        self.M, self.N, self.K = M, N, K
+        self.plan = plan(self.dtype, M, N, K)
+        self.enc_ws, self.report_ws = alloc_workspaces(self.plan, device)
+
+    def encode(self, A=None, B=None, which: int = 3, stream=None):
+        encode(self.dtype, A, B, self.enc_ws, M=self.M, N=self.N, K=self.K, which=which, stream=stream)
+
+    def run(self, A, B, C_, *, alpha=1.0, beta=0.0, ft_level=FT_CORRECT, injections=(), stream=None):
+        run(self.dtype, A, B, C_, alpha=alpha, beta=beta, enc_ws=self.enc_ws, ft_level=ft_level,
+            injections=injections, report_ws=self.report_ws, stream=stream)
+
+    def __call__(self, A, B, C_=None, **kw):
+        if C_ is None:
+            C_ = torch.empty(self.M, self.N, dtype=A.dtype, device=A.device)
+        if kw.get("ft_level", FT_CORRECT) != FT_OFF:
+            self.encode(A, B, stream=kw.get("stream"))
+        self.run(A, B, C_, **kw)
+        return C_
+
+    def report(self, max_events: int = 4096, stream=None):
+        return report(self.report_ws, max_events, stream)
+
+    def reset(self, stream=None):
+        report_reset(self.report_ws, stream)
+
+    @property
+    def enc_b(self) -> torch.Tensor:
+        """The B part of enc_ws (the unit broadcast with B across ranks)."""
+        p = self.plan
+        return self.enc_ws[p.enc_b_offset:p.enc_b_offset + p.enc_b_bytes]
+
+    @property
+    def enc_a(self) -> torch.Tensor:
+        return self.enc_ws[:self.plan.enc_b_offset]
