@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""bench.py -- FT-GEMM TFLOPS and % overhead vs non-FT / cuBLAS at 0..N errors/min.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[2], "cfg3"): BF16 tcgen05 ABFT GEMM 8192^3,
+C = A B (alpha 1, beta 0), inputs U[-1,1) rounded to BF16 (synthetic, seeded).
+One STEP = the whole hot path of SURVEY.md §8(a): encode A (a1), encode B (a2),
+the fused FT GEMM with verify / locate / correct (a3-a7) at ft_level CORRECT,
+with faults injected by a seeded schedule at ERRORS_PER_MIN (a4); the report
+counters (a8) accumulate on the device and are read and checked after the timed
+region.  N > 1 (torchrun): M-block partition (weak scaling): every rank owns an
+8192 x 8192 block of A and C, B (8192 x 8192) is generated on rank 0 and
+broadcast ONCE over NCCL before timing; each rank's step is the same as the
+1-GPU step.  Timing: W warm-up steps, then K steps bracketed by a barrier +
+cuda.synchronize on both sides, CUDA events on the launch stream, max over
+ranks.  Inputs (A + B = 256 MiB per rank) are larger than the 126 MB L2.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FT-GEMM TFLOPS & % overhead vs non-FT/cuBLAS at 0..N errors/min, 1-8 B200"
+M_PER_RANK, N_DIM, K_DIM = 8192, 8192, 8192
+ERRORS_PER_MIN = 500.0           # "hundreds of errors per minute" (north_star)
+SWEEP_RATES = (0.0, 1.0, 10.0, 100.0, 500.0)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-sweep", action="store_true", help="skip the injection-rate sweep and comparators")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-oracle sample budget")
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ----------------------------------------------------------- CPU oracle leg ---
+def cpu_oracle_sample(budget_s: float):
+    """Time the oracle (as it stands) on a bounded tile sample of the workload:
+    whole check tiles (125 x 248 x 8192) of the 8192^3 problem, FP64, all host
+    cores.  Returns (TFLOPS, cores, description)."""
+    import numpy as np
+    import oracle
+    import synth
+    oracle.build()
+    tm, tn, K = 125, 248, K_DIM
+    rate_probe_tiles = 1
+    done_tiles, flops, t_spent = 0, 0.0, 0.0
+    tiles = []
+    ti = tj = 0
+    t0 = time.time()
+    while True:
+        rows = (ti * tm, ti * tm + tm)
+        cols = (tj * tn, tj * tn + tn)
+        A = synth.matrix(synth.BASE_SEED + synth.SEED_A, M_PER_RANK, K, dtype="bf16", r0=rows[0], r1=rows[1])
+        B = synth.matrix(synth.BASE_SEED + synth.SEED_B, K, N_DIM, dtype="bf16", c0=cols[0], c1=cols[1])
+        t1 = time.time()
+        oracle.ftgemm(A, B, out="bf16", tile_m=tm, tile_n=tn, bk=64, u_acc=2.0 ** -23, lambda1=8.0, lambda2=16.0)
+        t_spent += time.time() - t1
+        flops += 2.0 * tm * tn * K
+        done_tiles += 1
+        tiles.append((ti, tj))
+        ti, tj = (ti + 7) % 65, (tj + 5) % 33
+        if time.time() - t0 > budget_s or done_tiles >= 4096:
+            break
+        del rate_probe_tiles
+        rate_probe_tiles = 0
+    tflops = flops / t_spent / 1e12
+    return tflops, oracle.num_threads(), (f"{done_tiles} check tiles of 125x248x8192 (BF16 values, FP64 oracle incl. "
+                                           f"encode/verify), {flops / 1e9:.1f} GFLOP in {t_spent:.1f}s")
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    tflops, cores, desc = cpu_oracle_sample(min(args.cpu_seconds, 60.0))
+    steps = args.steps
+    ms = 2.0 * M_PER_RANK * N_DIM * K_DIM / (tflops * 1e12) * 1e3
+    line = {"impl": "reference", "metric": METRIC, "value": tflops, "unit": "TFLOPS", "n_gpus": args.gpus,
+            "steps": steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg3: BF16 ABFT GEMM 8192^3 (tile-sampled CPU oracle)", "M": M_PER_RANK,
+                       "N": N_DIM, "K": K_DIM},
+            "cpu_baseline": {"value": tflops, "unit": "TFLOPS", "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": {"value": tflops, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "the reference arm is the paper-derived CPU oracle (no reference implementation exists)"}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------- clocks ---
+class ClockSampler:
+    def __init__(self, index: int):
+        self.proc = None
+        self.path = f"/tmp/ftgemm_clocks_{os.getpid()}.csv"
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "50"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for ln in open(self.path):
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), float(parts[3]), parts[4:]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        smax = max(r[1] for r in rows)
+        loaded = [r for r in rows if r[2] > 300.0] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in loaded:
+            for n, v in zip(names, r[3][1:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": smax,
+                "samples": len(loaded), "power_w_max": max(r[2] for r in rows), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------ ours ---
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2305_01024_b200 import ftgemm as F
+    from paper_2305_01024_b200 import distributed as D
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    Mr, N, K = M_PER_RANK, N_DIM, K_DIM
+    flops_rank = 2.0 * Mr * N * K
+
+    # ---- inputs: A block by global row index, B on rank 0 + one broadcast ----
+    A_h = synth.matrix(synth.BASE_SEED + synth.SEED_A, Mr * world, K, dtype="bf16", r0=rank * Mr, r1=(rank + 1) * Mr)
+    A = synth.to_torch(A_h, "bf16").to(dev)
+    del A_h
+    g = F.FTGemm("bf16", Mr, N, K, device=dev)
+    pl = g.plan
+    bcast_ms = 0.0
+    if rank == 0:
+        B = synth.to_torch(synth.matrix(synth.BASE_SEED + synth.SEED_B, K, N, dtype="bf16"), "bf16").to(dev)
+    else:
+        B = torch.empty(K, N, dtype=torch.bfloat16, device=dev)
+    if world > 1:
+        bcast_ms = D.broadcast_b(g, B, src=0)
+    C = torch.empty(Mr, N, dtype=torch.bfloat16, device=dev)
+
+    # ---- seeded fault schedule at a rate (errors / minute) ----
+    rng = np.random.default_rng(synth.BASE_SEED + synth.SEED_PLAN + rank)
+    tiles_total = pl.tiles_m * pl.tiles_n
+
+    def site():
+        t = int(rng.integers(tiles_total))
+        ti, tj = divmod(t, pl.tiles_n)
+        bm = min(pl.check_tile_m, Mr - ti * pl.check_tile_m)
+        bn = min(pl.check_tile_n, N - tj * pl.check_tile_n)
+        return (ti * pl.check_tile_m + int(rng.integers(bm)), tj * pl.check_tile_n + int(rng.integers(bn)),
+                int(rng.integers(K)), 30, F.INJ_FLIP, F.TGT_ACC, 0.0)
+
+    def schedule(rate, nsteps, step_ms):
+        lam = rate * step_ms / 60000.0
+        return [[site() for _ in range(int(rng.poisson(lam)))] for _ in range(nsteps)]
+
+    def step(inj=()):
+        g.encode(A, B)
+        g.run(A, B, C, ft_level=F.FT_CORRECT, injections=inj)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(fn_list, warm: int):
+        """fn_list: per-step callables; returns ms/step (max over ranks)."""
+        for i in range(warm):
+            fn_list[i % len(fn_list)]()
+        barrier(); torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for fn in fn_list:
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        barrier(); torch.cuda.synchronize()
+        return max_over_ranks(e0.elapsed_time(e1) / len(fn_list))
+
+    # ---- warm-up + rough step time for the schedule ----
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    g.reset()
+    est = timed([step] * 5, 0)
+
+    # ---- main timed region: K steps at ERRORS_PER_MIN, kernel events per step ----
+    sched = schedule(ERRORS_PER_MIN, args.steps, est)
+    n_injected = sum(len(s) for s in sched)
+    g.reset()
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    g.reset()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    barrier(); torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        g.encode(A, B)
+        kev[i][0].record(stream)
+        g.run(A, B, C, ft_level=F.FT_CORRECT, injections=sched[i])
+        kev[i][1].record(stream)
+    e1.record(stream)
+    e1.synchronize()
+    barrier(); torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms_step = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    ms_kernel = max_over_ranks(sum(a.elapsed_time(b) for a, b in kev) / args.steps)
+    counts, events = g.report()
+    ok_faults = counts["corrected"] == n_injected and counts["uncorrectable"] == 0 and counts["checksum_only"] == 0
+    value = flops_rank * world / (ms_step * 1e-3) / 1e12
+    launches_per_step = 5   # encode_a, finalize(A), encode_b, finalize(B), fused GEMM
+
+    extra = {}
+    if not args.no_sweep:
+        reps = max(10, args.steps)
+        t_off = timed([lambda: g.run(A, B, C, ft_level=F.FT_OFF)] * reps, 3)
+        t_run = timed([lambda: g.run(A, B, C, ft_level=F.FT_CORRECT)] * reps, 3)
+        t_enc = timed([lambda: g.encode(A, B)] * reps, 3)
+        t_enc_a = timed([lambda: g.encode(A, None, which=1)] * reps, 3)
+        t_cublas = timed([lambda: torch.matmul(A, B, out=C)] * reps, 3)
+        one = [site() for _ in range(1)]
+        t_one = timed([lambda: g.run(A, B, C, ft_level=F.FT_CORRECT, injections=one)] * reps, 3)
+        stress = []
+        for ti in range(pl.tiles_m):
+            for tj in range(pl.tiles_n):
+                r = ti * pl.check_tile_m + (ti * 7 + tj) % min(pl.check_tile_m, Mr - ti * pl.check_tile_m)
+                c = tj * pl.check_tile_n + (tj * 5 + ti) % min(pl.check_tile_n, N - tj * pl.check_tile_n)
+                stress.append((r, c, (ti * 131 + tj * 17) % K, 30, F.INJ_FLIP, F.TGT_ACC, 0.0))
+        g.reset()
+        t_stress = timed([lambda: g.run(A, B, C, ft_level=F.FT_CORRECT, injections=stress)] * 3, 1)
+        cs, _ = g.report(0)
+        stress_ok = cs["corrected"] == 4 * len(stress) and cs["uncorrectable"] == 0
+        sweep = {}
+        for rate in SWEEP_RATES:
+            nst = max(reps, int(math.ceil(2 * 60000.0 / max(rate, 1e-9) / est)) if rate >= 100 else reps)
+            nst = min(nst, 600)
+            sc = schedule(rate, nst, est)
+            fns = [(lambda inj: (lambda: step(inj)))(s) for s in sc]
+            t = timed(fns, 2)
+            sweep[str(int(rate))] = {"ms_per_step": t, "tflops": flops_rank * world / (t * 1e-3) / 1e12,
+                                     "steps": nst, "injected": sum(len(s) for s in sc),
+                                     "overhead_vs_ft_off_pct": 100.0 * (t - t_off) / t_off,
+                                     "overhead_vs_cublas_pct": 100.0 * (t - t_cublas) / t_cublas}
+        extra = {
+            "ft_off_ms": t_off, "ft_off_tflops": flops_rank * world / (t_off * 1e-3) / 1e12,
+            "cublas_ms": t_cublas, "cublas_tflops": flops_rank * world / (t_cublas * 1e-3) / 1e12,
+            "ft_run_only_ms": t_run, "encode_ms": t_enc, "encode_a_ms": t_enc_a,
+            "encode_gbs": (2 * Mr * K + 2 * K * N) / (t_enc * 1e-3) / 1e9,
+            "overhead_vs_ft_off_pct": 100.0 * (ms_step - t_off) / t_off,
+            "overhead_vs_cublas_pct": 100.0 * (ms_step - t_cublas) / t_cublas,
+            "overhead_run_only_vs_ft_off_pct": 100.0 * (t_run - t_off) / t_off,
+            "overhead_pre_encoded_B_vs_ft_off_pct": 100.0 * (t_run + t_enc_a - t_off) / t_off,
+            "one_fault_call_ms": t_one, "stress_one_fault_per_tile_ms": t_stress, "stress_faults": len(stress),
+            "stress_all_corrected": bool(stress_ok), "rate_sweep_errors_per_min": sweep,
+        }
+
+    # ---- e2e: public API with host buffers, H2D inputs + D2H result per step ----
+    A_pin = A.cpu().pin_memory(); B_pin = B.cpu().pin_memory()
+    C_pin = torch.empty(Mr, N, dtype=torch.bfloat16).pin_memory()
+    e2e_steps = max(3, min(args.steps, 10))
+
+    def e2e_step():
+        A.copy_(A_pin, non_blocking=True)
+        B.copy_(B_pin, non_blocking=True)
+        g.encode(A, B)
+        g.run(A, B, C, ft_level=F.FT_CORRECT)
+        C_pin.copy_(C, non_blocking=True)
+    t_e2e = timed([e2e_step] * e2e_steps, 2)
+    e2e = {"value": flops_rank * world / (t_e2e * 1e-3) / 1e12, "unit": "TFLOPS",
+           "h2d_bytes_per_step": A.numel() * 2 + B.numel() * 2, "d2h_bytes_per_step": C.numel() * 2,
+           "ms_per_step": t_e2e}
+
+    peaks, kind = load_peaks()
+    peak = peaks["bf16_tflops"]
+    achieved = flops_rank / (ms_kernel * 1e-3) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("fused_gemm_bf16_8192_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": "tc_ftgemm_kernel<bf16,256,FT>", "peak_kind": f"{kind} bf16 burst",
+                "algorithmic_flops_per_launch": flops_rank}
+
+    if rank == 0:
+        cpu = None
+        if world == 1:
+            tfl, cores, desc = cpu_oracle_sample(args.cpu_seconds)
+            cpu = {"value": tfl, "unit": "TFLOPS", "cores": cores, "kind": "oracle", "sample": desc}
+        line = {"metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": {"workload": "cfg3: BF16 tcgen05 ABFT GEMM 8192^3 per GPU (M-block partition for N>1)",
+                           "M": Mr * world, "N": N, "K": K, "alpha": 1.0, "beta": 0.0, "ft_level": "CORRECT",
+                           "errors_per_min": ERRORS_PER_MIN, "check_tile": [pl.check_tile_m, pl.check_tile_n],
+                           "mma_tile": [pl.bm, pl.bn, pl.bk], "l2": "inputs larger than L2 (A+B 256 MiB/rank)",
+                           "parallelism": f"mblock{world}" if world > 1 else "single"},
+                "faults": {"injected": n_injected, **{k: v for k, v in counts.items() if v}, "all_corrected": ok_faults},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+                "clocks": clk, "kernel_ms": ms_kernel, "b_broadcast_ms": bcast_ms, **extra}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -91,9 +91,11 @@ Geometry geometry(const ftgemm_plan_t& p, int64_t K) {
     g.bmd = p.check_tile_m; g.bnd = p.check_tile_n;
     g.tiles_m = (int)p.tiles_m; g.tiles_n = (int)p.tiles_n;
     g.kp = (int)(((K + p.bk - 1) / p.bk) * p.bk);
-    g.nkc = (g.kp + 255) / 256;
+    g.nkb = g.kp / p.bk;
     g.elt = p.dtype == FTGEMM_BF16 ? 2 : 4;
-    g.split = p.dtype != FTGEMM_F32_SIMT;
+    g.tc = p.dtype != FTGEMM_F32_SIMT;
+    g.nkc_a = (g.kp + 255) / 256;
+    g.nkc_b = g.tc ? g.nkb : (g.kp + 255) / 256;
     return g;
 }
 
@@ -291,22 +293,27 @@ int ftgemm_run(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const vo
         const int bnd = ft ? p.check_tile_n : p.off_tile_n;
         const uint32_t boxn = 128 / elt;
         CUtensorMap mA, mB;
-        if ((e = make_map(&mA, dt, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * elt, (uint32_t)p.bk, (uint32_t)p.bm))) return e;
-        if ((e = make_map(&mB, dt, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb * elt, boxn, (uint32_t)p.bk,
-                          tf32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B))) return e;
+        if ((e = make_map(&mA, dt, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * elt, (uint32_t)p.bk, (uint32_t)bmd))) return e;
+        if (ft) {
+            // the encoded operand B^r (K-major, tiles_n * bn rows of kp) from the encode workspace
+            if ((e = make_map(&mB, dt, enc + L.bt, (uint64_t)g.kp, (uint64_t)g.tiles_n * p.bn, (uint64_t)g.kp * elt,
+                              (uint32_t)p.bk, (uint32_t)p.bn))) return e;
+        } else {
+            if ((e = make_map(&mB, dt, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb * elt, boxn, (uint32_t)p.bk,
+                              tf32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B))) return e;
+        }
         TcArgs a{};
         a.M = (int)M; a.N = (int)N; a.K = (int)K; a.num_kb = num_kb;
         a.tiles_m = (int)((M + bmd - 1) / bmd); a.tiles_n = (int)((N + bnd - 1) / bnd);
         a.num_tiles = a.tiles_m * a.tiles_n;
         a.ft_level = ft_level; a.alpha = alpha; a.beta = beta; a.C = C; a.ldc = ldc;
         if (ft) {
-            a.Y = enc + L.y; a.X = enc + L.x; a.kp = g.kp;
+            a.Y = enc + L.y; a.kp = g.kp;
             a.rownorm = (const float*)(enc + L.rownorm); a.colnorm = (const float*)(enc + L.colnorm);
             a.acnorm = (const float*)(enc + L.acnorm); a.brnorm = (const float*)(enc + L.brnorm);
         }
         a.tau_u = tau_u; a.tau_l1 = l1; a.tau_l2 = l2; a.sqrtK = sqk;
         a.rep = (ReportDev*)report_ws; a.inj = dinj; a.n_inj = n_inj;
-        if (const char* d = getenv("FTGEMM_DBG")) a.dbg = atoi(d);
         ce = launch_tc(tf32, p.bn, ft, mA, mB, a, st);
     }
     if (ce != cudaSuccess) return fail_cuda(ce, "kernel launch");

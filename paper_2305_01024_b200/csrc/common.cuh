@@ -39,12 +39,11 @@ struct TcArgs {
     int ft_level;
     float alpha, beta;
     void* C; int64_t ldc;
-    const void* Y; const void* X; int kp;
+    const void* Y; int kp;
     const float* rownorm; const float* colnorm; const float* acnorm; const float* brnorm;
     float tau_u, tau_l1, tau_l2, sqrtK;
     ReportDev* rep;
     const DevInject* inj; int n_inj;
-    int dbg;   // development bisection flags (0 in production)
 };
 
 struct SimtArgs {
@@ -68,16 +67,25 @@ struct Geometry {
     int bmd, bnd;         // data rows / cols per check tile (FT on)
     int tiles_m, tiles_n; // check-tile grid (FT on)
     int kp;               // K padded to bk
-    int nkc;              // 256-wide K chunks (encode partial norms)
+    int nkb;              // kp / bk (MMA k-blocks)
+    int nkc_a;            // K chunks of the A-encode partial row norms (256 wide)
+    int nkc_b;            // K chunks of the B-encode partial column norms
     int elt;              // operand element bytes
-    int split;            // 1 when Y/X split operands exist (tensor-core paths)
+    int tc;               // 1 for the tensor-core paths (split operands, B^r)
 };
 
 // Encode workspace layout (byte offsets; each region 256-byte aligned).
+//   A part: Ac (FP32 e^T A per tile), Ypack (tensor-core paths: the 3 split rows
+//           of e^T A per (tile, k-block), 3 x 128 bytes, already in the smem
+//           SWIZZLE_128B order of MMA rows 125..127), row norms, tile norms.
+//   B part: Br (FP32 B e per tile), Bt (tensor-core paths: the encoded operand
+//           B^r = [B_j, B_j e] of PAPER.md Eq. (2) per check tile j, stored
+//           K-major as bn rows x kp: rows 0..bnd-1 = columns of B_j, rows
+//           bnd..bnd+2 = split(B_j e), row bn-1 = 0), column norms, tile norms.
 struct EncLayout {
     size_t ac, y, rownorm, acnorm, rn2;       // A part
     size_t b_off;                             // start of the B part
-    size_t br, x, colnorm, brnorm, cn2;       // absolute offsets
+    size_t br, bt, colnorm, brnorm, cn2;      // absolute offsets
     size_t a_bytes, b_bytes, total;
 };
 
@@ -87,17 +95,17 @@ inline EncLayout enc_layout(const Geometry& g, int64_t M, int64_t N) {
     EncLayout L{};
     size_t o = 0;
     L.ac = o;      o = align256(o + sizeof(float) * (size_t)g.tiles_m * g.kp);
-    L.y = o;       o = align256(o + (g.split ? (size_t)g.elt * g.tiles_m * 3 * g.kp : 0));
+    L.y = o;       o = align256(o + (g.tc ? (size_t)g.tiles_m * g.nkb * 384 : 0));
     L.rownorm = o; o = align256(o + sizeof(float) * (size_t)M);
     L.acnorm = o;  o = align256(o + sizeof(float) * (size_t)g.tiles_m);
-    L.rn2 = o;     o = align256(o + sizeof(float) * (size_t)g.nkc * M);
+    L.rn2 = o;     o = align256(o + sizeof(float) * (size_t)g.nkc_a * M);
     L.a_bytes = o;
     L.b_off = o;
     L.br = o;      o = align256(o + sizeof(float) * (size_t)g.tiles_n * g.kp);
-    L.x = o;       o = align256(o + (g.split ? (size_t)g.elt * g.tiles_n * g.kp * 4 : 0));
+    L.bt = o;      o = align256(o + (g.tc ? (size_t)g.elt * g.tiles_n * g.bn * g.kp : 0));
     L.colnorm = o; o = align256(o + sizeof(float) * (size_t)N);
     L.brnorm = o;  o = align256(o + sizeof(float) * (size_t)g.tiles_n);
-    L.cn2 = o;     o = align256(o + sizeof(float) * (size_t)g.nkc * N);
+    L.cn2 = o;     o = align256(o + sizeof(float) * (size_t)g.nkc_b * N);
     L.b_bytes = o - L.b_off;
     L.total = o;
     return L;

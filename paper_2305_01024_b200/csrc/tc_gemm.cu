@@ -3,27 +3,28 @@
 //
 // The paper's threadblock-level fused ABFT (section 4.2.3,
 // Fig. tb_abft) re-derived for tcgen05: instead of carrying e^T A B and A B e in
-// registers next to a SIMT outer product, the checksum vectors are APPENDED to
-// the MMA operand tiles, so the single tensor-core mainloop that computes C
-// also computes the carried references (Eq. (3)):
+// registers next to a SIMT outer product, the encoded operands of Eq. (1)/(2)
+// are fed to the tensor core as part of the MMA tiles, so the
+// single tensor-core mainloop that computes C also computes the carried
+// references of Eq. (3):
 //
-//     A tile (128 x BK, K-major)     rows 0..124  = A data (TMA)
-//                                    rows 125..127 = Y_i = split(e^T A_i)  (encode)
-//     B tile (BK x BN, N-major)      cols 0..BN-5  = B data (TMA)
-//                                    cols BN-4..BN-2 = X_j = split(B_j e),  col BN-1 = 0
-//     D = A_tile * B_tile in TMEM  =  [[ C_ij , C_ij^r (3 partial cols) ],
-//                                      [ C_ij^c (3 partial rows), unused ]]
+//     A tile (128 x BK, K-major)   rows 0..124  = A_i           (TMA, 125-row box)
+//                                  rows 125..127 = split(e^T A_i) (bulk copy of the
+//                                                 pre-swizzled encode output)
+//     B tile (BN x BK, K-major)    = B^r_j = [B_j, split(B_j e), 0] materialised by
+//                                    the encode kernel (rows 0..BN-5 = B_j^T)
+//     D = A_tile B_tile^T in TMEM = [[ C_ij , C^r_ij (3 partial cols) ],
+//                                    [ C^c_ij (3 partial rows), unused ]]
 //
-// so the check tile is 125 x (BN-4) data elements and verification needs no
-// extra MMA instructions.  Warp roles (one CTA per SM, persistent):
-//   warp 0      TMA producer (A box 128 rows, B boxes of 128 bytes x BK)
-//   warp 1      MMA issuer (one elected thread, tcgen05.mma, commits)
+// so the check tile is 125 x (BN-4) and verification needs no extra MMA.
+// With FT off the same kernel family reads A and the row-major B directly
+// (B N-major, 128 x BN data tiles).  Warp roles (one CTA per SM, persistent):
+//   warp 0      TMA producer
+//   warp 1      MMA issuer (one thread: tcgen05.mma, tcgen05.commit)
 //   warp 2      TMEM allocator
-//   warp 3      checksum fix-up (FT): writes Y rows / X columns into the landed
-//               stage (swizzled), then releases it to the MMA
 //   warps 4..7  epilogue: TMEM -> registers; row sums (thread = row), column
 //               sums (warp transpose-reduce + smem), residuals vs thresholds,
-//               locate, correct, alpha/beta, store;
+//               locate, correct, alpha/beta, store; they
 //               also service mid-mainloop fault injections
 // The accumulator is double-buffered in TMEM (2 x BN columns), so the epilogue
 // of tile t (verification included) overlaps the mainloop of tile t+1.
@@ -46,6 +47,7 @@ struct TcCfg {
     static constexpr int A_BYTES = BM * 128;
     static constexpr int B_BOX_BYTES = BK * 128;
     static constexpr int B_BYTES = NBOX * B_BOX_BYTES;
+    static constexpr int Y_BYTES = 384;            // 3 split rows x 128 bytes
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int STAGES = (BN == 256) ? 4 : 6;
     static constexpr int BMD = FT ? BM - 3 : BM;   // data rows of a check tile
@@ -93,15 +95,6 @@ __device__ __forceinline__ float transpose_reduce32(float (&w)[32], uint32_t lan
     return w[0];
 }
 
-// Column offset of the data inside the MMA tile of check-tile column tj.
-// BF16 check tiles are 252 columns wide (BN-4) but TMA boxes must start on a
-// 16-byte (8-element) boundary, so tile starts alternate between 0 and 4 mod 8:
-// even tiles load [col0, col0+BN) and carry X in MMA columns BN-4..BN-1; odd
-// tiles load [col0-4, col0+BN-4) and carry X in MMA columns 0..3.  TF32 tiles
-// (1008-byte starts) never need the shift.
-template <bool kTF32, bool FT>
-__device__ __forceinline__ int data_off(int tj) { return (FT && !kTF32 && (tj & 1)) ? 4 : 0; }
-
 __device__ __forceinline__ uint32_t apply_fault(uint32_t bits, const DevInject& f) {
     if (f.mode == FTGEMM_INJ_ADD) return __float_as_uint(__uint_as_float(bits) + f.addend);
     return bits ^ (1u << (f.bit & 31));
@@ -113,7 +106,9 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     using Cfg = TcCfg<kTF32, BN, FT>;
     constexpr int S = Cfg::STAGES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte aligned base (SWIZZLE_128B atoms); pointer arithmetic on the
+    // __shared__ array keeps the shared address space visible to the compiler
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* stage_base = smem;
     float* stg = reinterpret_cast<float*>(smem + S * Cfg::STAGE_BYTES);       // [4][32][33]
     float* colsum = stg + Cfg::STG_FLOATS;                                    // [4][BN]
@@ -124,10 +119,9 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     float* rtau = rres + Cfg::BM;                                             // [BM]
     int* sflag = reinterpret_cast<int*>(rtau + Cfg::BM);                      // nr, nc, p*, q*, corr
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * Cfg::STAGE_BYTES + Cfg::EPI_BYTES);
-    uint64_t* full = bars;              // [S]  MMA may consume
+    uint64_t* full = bars;              // [S]  stage landed (TMA + bulk bytes)
     uint64_t* empty = bars + S;         // [S]  producer may refill
-    uint64_t* tfull = bars + 2 * S;     // [S]  TMA landed (FT: fix-up may write)
-    uint64_t* tm_full = bars + 3 * S;   // [2]
+    uint64_t* tm_full = bars + 2 * S;   // [2]  accumulator complete
     uint64_t* tm_empty = tm_full + 2;   // [2]
     uint64_t* inj_req = tm_empty + 2;
     uint64_t* inj_done = inj_req + 1;
@@ -142,7 +136,6 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
-            mbar_init(&tfull[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tm_full[b], 1);
@@ -162,25 +155,29 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         // ------------------------------------------------ TMA producer ----
         if (lane == 0) {
             int s = 0; uint32_t ph = 0;
-            // The A box always spans the full 128 MMA rows: in FT mode rows 125..127
-            // (the next tile's first rows) are overwritten by the fix-up warp with the
-            // checksum rows once the TMA has landed (TMA boxes cannot end mid swizzle atom).
-            constexpr uint32_t bytes = Cfg::A_BYTES + Cfg::B_BYTES;
+            // FT: A box of 125 data rows + 384-byte bulk copy of the split rows into
+            // rows 125..127; B^r box of BN rows (K-major).  FT off: 128-row A box and
+            // the row-major B in NBOX N-major boxes.
+            constexpr uint32_t bytes = FT ? (Cfg::BMD * 128 + Cfg::Y_BYTES + Cfg::B_BYTES) : (Cfg::A_BYTES + Cfg::B_BYTES);
             for (int t = blockIdx.x; t < a.num_tiles; t += gridDim.x) {
                 int ti, tj;
                 tile_coords(t, a.tiles_m, a.tiles_n, ti, tj);
                 const int row0 = ti * Cfg::BMD;
-                const int col0 = tj * Cfg::BND - data_off<kTF32, FT>(tj);
                 for (int kb = 0; kb < a.num_kb; ++kb) {
                     mbar_wait(&empty[s], ph ^ 1);
-                    uint64_t* bar = FT ? &tfull[s] : &full[s];
-                    mbar_arrive_expect_tx(bar, bytes);
+                    mbar_arrive_expect_tx(&full[s], bytes);
                     uint8_t* sa = stage_base + s * Cfg::STAGE_BYTES;
                     uint8_t* sb = sa + Cfg::A_BYTES;
-                    tma_load_2d(sa, &tmA, bar, kb * Cfg::BK, row0);
+                    tma_load_2d(sa, &tmA, &full[s], kb * Cfg::BK, row0);
+                    if constexpr (FT) {
+                        bulk_load(sa + Cfg::BMD * 128, reinterpret_cast<const uint8_t*>(a.Y) +
+                                  ((int64_t)ti * a.num_kb + kb) * Cfg::Y_BYTES, Cfg::Y_BYTES, &full[s]);
+                        tma_load_2d(sb, &tmB, &full[s], kb * Cfg::BK, tj * BN);
+                    } else {
 #pragma unroll
-                    for (int b = 0; b < Cfg::NBOX; ++b)
-                        tma_load_2d(sb + b * Cfg::B_BOX_BYTES, &tmB, bar, col0 + b * Cfg::BOXN, kb * Cfg::BK);
+                        for (int b = 0; b < Cfg::NBOX; ++b)
+                            tma_load_2d(sb + b * Cfg::B_BOX_BYTES, &tmB, &full[s], tj * BN + b * Cfg::BOXN, kb * Cfg::BK);
+                    }
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
             }
@@ -188,7 +185,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     } else if (warp == 1) {
         // ------------------------------------------------- MMA issuer -----
         if (lane == 0) {
-            constexpr uint32_t idesc = instr_desc(kTF32, Cfg::BM, BN, false, true);
+            constexpr uint32_t idesc = instr_desc(kTF32, Cfg::BM, BN, false, !FT);
             int s = 0; uint32_t ph = 0; uint32_t injph = 0;
             int lt = 0;
             for (int t = blockIdx.x; t < a.num_tiles; t += gridDim.x, ++lt) {
@@ -210,10 +207,11 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
                     for (int kk = 0; kk < Cfg::BK / Cfg::UK; ++kk) {
                         const uint64_t ad = smem_desc_sw128(sa + kk * 32, 16, 1024);
-                        // B is N-major: bf16 -> SW128 (8-row atoms), tf32 -> SW128_BASE32B (4-row atoms)
-                        const uint64_t bd = kTF32
-                            ? smem_desc_sw128<1>(sb + kk * Cfg::UK * 128, Cfg::B_BOX_BYTES, 512)
-                            : smem_desc_sw128<2>(sb + kk * Cfg::UK * 128, Cfg::B_BOX_BYTES, 1024);
+                        // FT: B^r is K-major like A.  FT off: B is N-major, bf16 -> SW128
+                        // (8-row atoms), tf32 -> SW128_BASE32B (4-row atoms).
+                        const uint64_t bd = FT ? smem_desc_sw128<2>(sb + kk * 32, 16, 1024)
+                                          : kTF32 ? smem_desc_sw128<1>(sb + kk * Cfg::UK * 128, Cfg::B_BOX_BYTES, 512)
+                                                  : smem_desc_sw128<2>(sb + kk * Cfg::UK * 128, Cfg::B_BOX_BYTES, 1024);
                         umma<kTF32>(d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
                     }
                     umma_commit(&empty[s]);
@@ -231,60 +229,6 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             }
         }
         __syncwarp();
-    } else if (warp == 3) {
-        // ------------------------------------------- checksum fix-up (FT) --
-        if constexpr (FT) {
-            int s = 0; uint32_t ph = 0;
-            for (int t = blockIdx.x; t < a.num_tiles; t += gridDim.x) {
-                int ti, tj;
-                tile_coords(t, a.tiles_m, a.tiles_n, ti, tj);
-                for (int kb = 0; kb < a.num_kb; ++kb) {
-                    // Y rows: 3 rows x 128 bytes, lanes 0..23 one 16-byte chunk each
-                    uint4 yv = make_uint4(0, 0, 0, 0);
-                    const int yr = lane >> 3, ych = lane & 7;
-                    if (lane < 24) {
-                        const uint8_t* src = reinterpret_cast<const uint8_t*>(a.Y) +
-                            (((int64_t)ti * 3 + yr) * a.kp + (int64_t)kb * Cfg::BK) * Cfg::ELT + ych * 16;
-                        yv = __ldg(reinterpret_cast<const uint4*>(src));
-                    }
-                    // X: per k-row 4 values (hi, mid, lo, 0)
-                    uint2 xv0 = make_uint2(0, 0), xv1 = make_uint2(0, 0);
-                    uint4 xq = make_uint4(0, 0, 0, 0);
-                    if constexpr (!kTF32) {
-                        const uint16_t* src = reinterpret_cast<const uint16_t*>(a.X) + ((int64_t)tj * a.kp + (int64_t)kb * Cfg::BK) * 4;
-                        xv0 = __ldg(reinterpret_cast<const uint2*>(src + lane * 4));
-                        xv1 = __ldg(reinterpret_cast<const uint2*>(src + (lane + 32) * 4));
-                    } else {
-                        const float* src = reinterpret_cast<const float*>(a.X) + ((int64_t)tj * a.kp + (int64_t)kb * Cfg::BK) * 4;
-                        xq = __ldg(reinterpret_cast<const uint4*>(src + lane * 4));
-                    }
-                    mbar_wait(&tfull[s], ph);
-                    if (a.dbg & 1) { __syncwarp(); if (lane == 0) mbar_arrive(&full[s]); if (++s == S) { s = 0; ph ^= 1; } continue; }
-                    uint8_t* sa = stage_base + s * Cfg::STAGE_BYTES;
-                    const bool xfirst = data_off<kTF32, FT>(tj) != 0;   // X in MMA cols 0..3
-                    uint8_t* sb_x = sa + Cfg::A_BYTES + (xfirst ? 0 : (Cfg::NBOX - 1) * Cfg::B_BOX_BYTES);
-                    if (lane < 24) {
-                        const int row = Cfg::BMD + yr;
-                        *reinterpret_cast<uint4*>(sa + row * 128 + ((ych ^ (row & 7)) << 4)) = yv;
-                    }
-                    if constexpr (!kTF32) {
-                        // X = 8 bytes of a k-row: logical 16-byte chunk 7 bytes 8..15, or chunk 0 bytes 0..7
-                        const int r0 = lane, r1 = lane + 32, lc = xfirst ? 0 : 7, bo = xfirst ? 0 : 8;
-                        *reinterpret_cast<uint2*>(sb_x + r0 * 128 + ((lc ^ (r0 & 7)) << 4) + bo) = xv0;
-                        *reinterpret_cast<uint2*>(sb_x + r1 * 128 + ((lc ^ (r1 & 7)) << 4) + bo) = xv1;
-                    } else {
-                        // 128B_ATOM_32B swizzle: 32-byte chunk index ^= (row & 3); cols BN-4.. are
-                        // bytes 16..31 of logical chunk 3
-                        const int r0 = lane;
-                        *reinterpret_cast<uint4*>(sb_x + r0 * 128 + ((3 ^ (r0 & 3)) << 5) + 16) = xq;
-                    }
-                    fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&full[s]);
-                    if (++s == S) { s = 0; ph ^= 1; }
-                }
-            }
-        }
     } else if (warp >= 4) {
         // ----------------------------------------------------- epilogue -----
         const int ew = warp - 4;                 // TMEM lane quadrant
@@ -300,8 +244,8 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             tile_coords(t, a.tiles_m, a.tiles_n, ti, tj);
             const int r0 = ti * Cfg::BMD, c0 = tj * Cfg::BND;
             const int bm = min(Cfg::BMD, a.M - r0), bn = min(Cfg::BND, a.N - c0);
-            const int doff = data_off<kTF32, FT>(tj);          // data col q <-> MMA col q + doff
-            const int xoff = doff ? 0 : BN - 4;                // row-reference split columns
+            constexpr int doff = 0;                            // data col q <-> MMA col q
+            constexpr int xoff = BN - 4;                       // row-reference split columns
             const int acc = lt & 1;
             const uint32_t accph = (lt >> 1) & 1;
             const uint32_t tb = tmem_base + acc * BN;
@@ -339,7 +283,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 
             int kind = 0, pstar = -1, qstar = -1;
             float corr = 0.0f;
-            if (FT && !(a.dbg & 2)) {
+            if (FT) {
                 // ---- pass 1: row sums, row refs, column partial sums ----
                 named_bar_sync(1, 128);          // previous tile's readers of sflag are done
                 if (et == 0) { sflag[0] = 0; sflag[1] = 0; sflag[2] = 1 << 30; sflag[3] = 1 << 30; }

@@ -1,6 +1,5 @@
-mkdir -p gpurun_out/debug6
-D=gpurun_out/debug6
-timeout 120 python tools/gpu_debug.py full_bf16 > $D/bf16.log 2>&1
-timeout 300 compute-sanitizer --tool memcheck --show-backtrace device python tools/gpu_debug.py bf16 > $D/san.log 2>&1
-timeout 300 python tools/gpu_debug.py big > $D/big.log 2>&1
+mkdir -p gpurun_out/r6
+D=gpurun_out/r6
+timeout 200 python tools/gpu_debug.py full_bf16 full_tf32 big > $D/dbg.log 2>&1
+for a in "bf16 8192 8192 8192 2" "bf16 8192 8192 8192 0" "tf32 8192 8192 8192 2" "tf32 8192 8192 8192 0" "bf16 8192 8192 1024 2" "bf16 8192 8192 1024 0"; do timeout 60 python tools/perf_probe.py $a >> $D/perf.log 2>&1; done
 echo done
