@@ -1,0 +1,128 @@
+"""CPU-side checks of the C ABI: the library builds for sm_100a, loads, exports
+every symbol include/ftgemm.h declares, the host plan table is consistent, and
+argument errors are reported synchronously (no device needed).  There is no
+CPU fallback: on a machine without an sm_100 GPU a well-formed call fails with
+FTGEMM_ERR_UNSUPPORTED."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "ftgemm.h")
+
+
+@pytest.fixture(scope="module")
+def F():
+    from paper_2305_01024_b200 import build
+    build.build()
+    from paper_2305_01024_b200 import ftgemm
+    ftgemm.lib()
+    return ftgemm
+
+
+def declared_symbols():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"FTGEMM_API\s+[\w\s\*]+?\b(ftgemm_\w+)\s*\(", txt)))
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    for s in ("ftgemm_plan", "ftgemm_encode", "ftgemm_run", "ftgemm_report", "ftgemm_report_reset",
+              "ftgemm_last_error"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(F):
+    lib = F.lib()
+    for s in declared_symbols():
+        assert hasattr(lib, s), s
+    assert lib.ftgemm_version() == 1
+    assert lib.ftgemm_device_arch() == 1000
+
+
+def test_built_for_sm100a(F):
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", F.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", F.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass or "UTCQMMA" in sass      # tcgen05.mma
+    assert "UTMALDG" in sass                           # TMA loads
+    assert "LDTM" in sass                              # tcgen05.ld
+
+
+def test_struct_layouts(F, tmp_path):
+    """The ctypes mirrors in the binding have the header's sizes and offsets (compiled with gcc)."""
+    import subprocess
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "ftgemm.h"\n'
+                   'int main(){printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(ftgemm_inject_t), sizeof(ftgemm_event_t),'
+                   ' sizeof(ftgemm_counts_t), sizeof(ftgemm_plan_t), offsetof(ftgemm_plan_t, tiles_m),'
+                   ' offsetof(ftgemm_plan_t, u_acc));return 0;}')
+    exe = tmp_path / "sz"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)], check=True)
+    got = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()))
+    assert got == [C.sizeof(F.Inject), C.sizeof(F.Event), C.sizeof(F.Counts), C.sizeof(F.PlanStruct),
+                   F.PlanStruct.tiles_m.offset, F.PlanStruct.u_acc.offset]
+    assert got[:3] == [40, 56, 64]
+
+
+@pytest.mark.parametrize("dtype", ["f32_simt", "tf32", "bf16"])
+def test_plan_table(F, dtype):
+    p = F.plan(dtype, 8192, 8192, 8192)
+    if dtype == "f32_simt":
+        assert (p.bm, p.bn, p.bk, p.check_tile_m, p.check_tile_n) == (128, 128, 8, 128, 128)
+        assert p.u_acc == 2.0 ** -24
+    else:
+        assert (p.bm, p.bn) == (128, 256) and p.check_tile_m == 125 and p.check_tile_n == 252
+        assert p.bk == (32 if dtype == "tf32" else 64)
+        assert p.u_acc == 2.0 ** -23
+    assert p.tiles_m == -(-8192 // p.check_tile_m) and p.tiles_n == -(-8192 // p.check_tile_n)
+    assert 0 < p.enc_b_offset < p.enc_bytes and p.enc_b_offset + p.enc_b_bytes == p.enc_bytes
+    assert p.report_bytes > 0 and p.max_events == 4096
+    small = F.plan(dtype, 128, 16384, 16384)
+    if dtype != "f32_simt":
+        assert small.bn == 128 and small.shape_class == 1
+
+
+def test_plan_errors(F):
+    for dims in [(0, 8, 8), (8, -1, 8), (8, 8, 0)]:
+        with pytest.raises(F.FtgemmError) as e:
+            F.plan("bf16", *dims)
+        assert e.value.code == 1
+    with pytest.raises(F.FtgemmError) as e:
+        F.plan(7, 8, 8, 8)
+    assert e.value.code == 1
+
+
+def test_synchronous_argument_errors(F):
+    lib = F.lib()
+    buf = (C.c_uint8 * 4096)()
+    base = (C.addressof(buf) + 255) & ~255
+    # null operands
+    assert lib.ftgemm_run(2, 64, 64, 64, 1.0, None, 64, base, 64, 0.0, base, 64, None, 0, None, 0, None, None) == 1
+    # leading dimension too small
+    assert lib.ftgemm_run(2, 64, 64, 64, 1.0, base, 32, base, 64, 0.0, base, 64, None, 0, None, 0, None, None) == 1
+    # FT without workspaces
+    assert lib.ftgemm_run(2, 64, 64, 64, 1.0, base, 64, base, 64, 0.0, base, 64, None, 2, None, 0, None, None) == 1
+    # misaligned base (TMA needs 16-byte bases)
+    assert lib.ftgemm_run(2, 64, 64, 64, 1.0, base + 2, 64, base, 64, 0.0, base, 64, None, 0, None, 0, None, None) == 2
+    # row pitch not a multiple of 16 bytes
+    assert lib.ftgemm_run(2, 64, 64, 60, 1.0, base, 60, base, 64, 0.0, base, 64, None, 0, None, 0, None, None) == 2
+    # bad encode selector
+    assert lib.ftgemm_encode(2, 64, 64, 64, base, 64, base, 64, base, 4, None) == 1
+    assert "which" in lib.ftgemm_last_error().decode()
+
+
+def test_no_cpu_fallback(F):
+    """A well-formed call on a host without an sm_100 device fails loudly."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    lib = F.lib()
+    buf = (C.c_uint8 * (64 * 64 * 2 + 512))()
+    base = (C.addressof(buf) + 255) & ~255
+    rc = lib.ftgemm_run(2, 64, 64, 64, 1.0, base, 64, base, 64, 0.0, base, 64, None, 0, None, 0, None, None)
+    assert rc == 2
+    assert "sm_100" in lib.ftgemm_last_error().decode()

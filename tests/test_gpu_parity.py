@@ -1,0 +1,272 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Bars (north_star): detected / corrected positions and
+counts bit-exact; C within a relative Frobenius tolerance of 1e-6 (FP32 SIMT),
+5e-3 (TF32), 2e-2 (BF16); bit-exact where the arithmetic is exact (integer
+inputs; the SIMT kernel against the oracle's sequential-fmaf mode)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_util import TOL, Case, detectable_sites, odt
+
+pytestmark = pytest.mark.gpu
+
+DTYPES = ["f32_simt", "tf32", "bf16"]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2305_01024_b200 import ftgemm as F
+    F.lib()
+    oracle.build()
+
+
+def ftmod():
+    from paper_2305_01024_b200 import ftgemm as F
+    return F
+
+
+# ------------------------------------------------------- operand semantics ---
+
+def test_tf32_operand_semantics():
+    """kind::tf32 ignores the low 13 mantissa bits of FP32 operands (truncation);
+    the encode relies on it (reading R8)."""
+    import torch
+    F = ftmod()
+    A = np.zeros((128, 32), np.float32)
+    B = np.zeros((32, 128), np.float32)
+    A[0, 0] = 1 + 2 ** -11 + 2 ** -12
+    B[0, 0] = 1.0
+    Cd = torch.zeros(128, 128, device="cuda")
+    F.run("tf32", torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), Cd, ft_level=F.FT_OFF)
+    torch.cuda.synchronize()
+    assert Cd[0, 0].item() == 1.0
+
+
+# ------------------------------------------------------------ clean parity ---
+
+SHAPES = [
+    (256, 256, 256, None, None, None),        # cfg1 shape
+    (300, 520, 200, None, None, None),        # ragged M, N
+    (1000, 1112, 704, None, None, None),      # several tiles + ragged tail
+    (257, 301, 333, 336, 304, 304),           # ragged everything, padded leading dims
+    (4096, 4096, 256, None, None, None),      # 128 x 256 tensor-core instantiation
+]
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "x".join(map(str, s[:3])))
+def test_clean_parity(dtype, shape):
+    M, N, K, lda, ldb, ldc = shape
+    c = Case(dtype, M, N, K, lda=lda, ldb=ldb, ldc=ldc, alpha=1.5, beta=-0.5)
+    tol = TOL[dtype] if dtype != "f32_simt" else max(1e-6, 2 * 2 ** -24 * math.sqrt(K))
+    assert c.fro() < tol, c.fro()
+    assert c.counts["tiles_checked"] == c.plan.tiles_m * c.plan.tiles_n
+    assert c.counts["tiles_detected"] == 0 and c.counts_match() and c.events_match()
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_integer_inputs_bit_exact(dtype):
+    """|values| <= 4, K <= 1024: every product, sum and checksum is exact in all
+    three precisions, so C equals the oracle bit for bit."""
+    c = Case(dtype, 384, 520, 512, dist="int", alpha=2.0, beta=-1.0)
+    assert np.array_equal(c.C, c.ref.C)
+    assert c.counts["tiles_detected"] == 0
+
+
+def test_simt_bit_exact_vs_sequential_fma():
+    """FP32 SIMT = the paper's SGEMM numerics: clean C bit-identical to the
+    oracle's FP32SEQ mode (one fmaf per k, ascending k; fmaf(alpha, acc, beta c))."""
+    for dist in ("signed", "unit"):
+        c = Case("f32_simt", 300, 260, 1000, dist=dist, alpha=1.5, beta=-0.5, acc="fp32seq")
+        assert np.array_equal(c.C, c.ref.C)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_ft_off_matches_ft_on_clean(dtype):
+    """No-fault transparency: FT on (no faults) leaves C as FT off computes it."""
+    F = ftmod()
+    on = Case(dtype, 640, 760, 512, run_oracle=False)
+    off = Case(dtype, 640, 760, 512, ft=F.FT_OFF, run_oracle=False)
+    if dtype == "f32_simt":
+        assert np.array_equal(on.C, off.C)
+    else:
+        assert np.abs(on.C - off.C).max() <= 1e-6 * np.abs(off.C).max()
+
+
+def test_determinism():
+    a = Case("bf16", 700, 904, 1024, injections=[(10, 20, 300, 30, 0, 0, 0.0)], run_oracle=False)
+    b = Case("bf16", 700, 904, 1024, injections=[(10, 20, 300, 30, 0, 0, 0.0)], run_oracle=False)
+    assert np.array_equal(a.C, b.C) and a.events == b.events
+
+
+# ------------------------------------------------------------ fault parity ---
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("dist", ["signed", "unit"])
+def test_injected_single_faults_parity(dtype, dist):
+    """One detectable flip in several tiles: every fault is located at the same
+    position, classified the same and corrected, as in the oracle."""
+    M, N, K = 640, 760, 768
+    A, B, _ = synth.problem(M, N, K, dist=dist, dtype=odt(dtype))
+    F = ftmod()
+    plan = F.plan(dtype, M, N, K)
+    inj = detectable_sites(dtype, 6, M, N, K, plan, A, B, seed=11)
+    assert len(inj) >= 4
+    c = Case(dtype, M, N, K, dist=dist, injections=inj, alpha=1.0, beta=0.0)
+    assert c.counts["corrected"] == len(inj), (c.counts, c.ref.counts)
+    assert c.events_match() and c.counts_match()
+    assert c.fro() < TOL[dtype] if dtype != "f32_simt" else c.fro() < 5e-6
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_cfg1_one_flip(dtype):
+    """BASELINE cfg1 shape: 256^3, one bit flip at a seeded site (bit chosen per
+    site by the oracle's generator), alpha 1.5, beta -0.5."""
+    M = N = K = 256
+    for dist in ("signed", "unit"):
+        A, B, _ = synth.problem(M, N, K, dist=dist, dtype=odt(dtype))
+        plan = ftmod().plan(dtype, M, N, K)
+        inj = detectable_sites(dtype, 1, M, N, K, plan, A, B, seed=230501024 + 3)
+        c = Case(dtype, M, N, K, dist=dist, injections=inj, alpha=1.5, beta=-0.5)
+        assert c.counts["corrected"] == 1 and c.events_match()
+        assert c.fro() < (TOL[dtype] if dtype != "f32_simt" else 1e-6)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_benign_flips_not_detected(dtype):
+    M, N, K = 512, 512, 512
+    A, B, _ = synth.problem(M, N, K, dtype=odt(dtype))
+    plan = ftmod().plan(dtype, M, N, K)
+    inj = detectable_sites(dtype, 4, M, N, K, plan, A, B, seed=5, benign=True)
+    assert inj
+    c = Case(dtype, M, N, K, injections=inj)
+    assert c.counts["tiles_detected"] == 0 and c.ref.counts["tiles_detected"] == 0
+    assert c.fro() < (TOL[dtype] if dtype != "f32_simt" else 1e-6)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_add_mode_and_nonfinite(dtype):
+    """ADD faults of +-1e3 and a flip to Inf/NaN (bit 30 of a partial >= 2 makes
+    it infinite) are located and reconstructed from the row checksum."""
+    M, N, K = 400, 400, 256
+    inj = [(5, 7, 40, 0, oracle.INJ_ADD, 0, 1000.0), (260, 300, 200, 0, oracle.INJ_ADD, 0, -1000.0),
+           (130, 3, 255, 0, oracle.INJ_ADD, 0, float("inf"))]
+    c = Case(dtype, M, N, K, dist="unit", injections=inj)
+    assert c.counts["corrected"] == 3 and c.events_match()
+    assert np.all(np.isfinite(c.C))
+    assert c.fro() < (TOL[dtype] if dtype != "f32_simt" else 5e-6)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_seu_violation_and_checksum_faults(dtype):
+    """Two faults in one tile -> uncorrectable (C left as computed); a fault in a
+    carried reference -> checksum_only (C untouched); both as in the oracle."""
+    F = ftmod()
+    M, N, K = 400, 400, 256
+    plan = F.plan(dtype, M, N, K)
+    tm, tn = plan.check_tile_m, plan.check_tile_n
+    inj = [(1, 2, 30, 0, oracle.INJ_ADD, 0, 500.0), (7, 9, 100, 0, oracle.INJ_ADD, 0, -700.0),    # tile (0,0)
+           (tm + 3, 5, 64, 0, oracle.INJ_ADD, oracle.TGT_ROW_REF, 800.0),                            # tile (1,0)
+           (7, tn + 4, 64, 0, oracle.INJ_ADD, oracle.TGT_COL_REF, 800.0)]                            # tile (0,1)
+    c = Case(dtype, M, N, K, dist="unit", injections=inj)
+    assert c.counts["uncorrectable"] == 1 and c.counts["checksum_only"] == 2
+    assert c.events_match() and c.counts_match()
+    bad = np.zeros((M, N), bool)
+    bad[[1, 7], :] = True
+    bad[:, [2, 9]] = True
+    assert c.fro(~bad) < (TOL[dtype] if dtype != "f32_simt" else 5e-6)
+    assert abs(c.C[1, 2] - c.ref.C[1, 2]) <= 1e-2 * abs(c.ref.C[1, 2]) + 1.0
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_detect_level(dtype):
+    F = ftmod()
+    inj = [(33, 44, 100, 0, oracle.INJ_ADD, 0, 250.0)]
+    c = Case(dtype, 300, 304, 256, dist="unit", ft=F.FT_DETECT, injections=inj)
+    assert c.counts["located"] == 1 and c.counts["corrected"] == 0 and c.events_match()
+    assert abs(c.C[33, 44] - c.ref.C[33, 44]) <= 2e-2 * abs(c.ref.C[33, 44])
+
+
+def test_stress_one_fault_per_tile():
+    """One detectable flip in EVERY tile (BF16): all corrected at the oracle's positions."""
+    M = N = 1024
+    K = 512
+    A, B, _ = synth.problem(M, N, K, dtype="bf16")
+    plan = ftmod().plan("bf16", M, N, K)
+    inj = detectable_sites("bf16", plan.tiles_m * plan.tiles_n, M, N, K, plan, A, B, seed=99)
+    c = Case("bf16", M, N, K, injections=inj)
+    assert c.counts["corrected"] == len(inj) and c.events_match() and c.fro() < TOL["bf16"]
+
+
+@pytest.mark.parametrize("dtype", ["tf32", "bf16"])
+def test_false_positive_sweep(dtype):
+    """Fault-free tiles never trip the threshold (SPEC.md:283 analogue)."""
+    F = ftmod()
+    for dist in ("signed", "unit"):
+        c = Case(dtype, 2048, 2048, 2048, dist=dist, run_oracle=False)
+        assert c.counts["tiles_detected"] == 0
+        assert c.counts["tiles_checked"] == c.plan.tiles_m * c.plan.tiles_n
+
+
+# ------------------------------------------------- full size, sampled oracle --
+
+def test_cfg3_full_size_sampled():
+    """BF16 8192^3 in the bench's launch configuration (same plan, same kernel),
+    with faults in 4 tiles; the oracle checks whole sampled tiles (tile-local
+    sub-problems, see tests/test_oracle.py::test_tile_local_subproblem)."""
+    import torch
+    F = ftmod()
+    M = N = K = 8192
+    plan = F.plan("bf16", M, N, K)
+    tm, tn = plan.check_tile_m, plan.check_tile_n
+    seedA, seedB = synth.BASE_SEED + synth.SEED_A, synth.BASE_SEED + synth.SEED_B
+    A = synth.to_torch(synth.matrix(seedA, M, K, dtype="bf16"), "bf16").cuda()
+    B = synth.to_torch(synth.matrix(seedB, K, N, dtype="bf16"), "bf16").cuda()
+    C = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    tiles = [(0, 0), (17, 5), (40, 32), (plan.tiles_m - 1, plan.tiles_n - 1), (33, 20), (64, 1)]
+    inj = [(ti * tm + 7, tj * tn + 11, 4000, 30, oracle.INJ_FLIP, 0, 0.0) for ti, tj in tiles[:4]]
+    g = F.FTGemm("bf16", M, N, K)
+    g.encode(A, B)
+    g.run(A, B, C, injections=inj)
+    counts, events = g.report()
+    assert counts["corrected"] == 4 and counts["tiles_detected"] == 4
+    assert counts["tiles_checked"] == plan.tiles_m * plan.tiles_n
+    Ch = C.float().cpu().numpy()
+    for (ti, tj) in tiles:
+        r0, c0 = ti * tm, tj * tn
+        r1, c1 = min(M, r0 + tm), min(N, c0 + tn)
+        Ab = synth.matrix(seedA, M, K, dtype="bf16", r0=r0, r1=r1)
+        Bb = synth.matrix(seedB, K, N, dtype="bf16", c0=c0, c1=c1)
+        loc = [(r - r0, c - c0, k, b, m, t, a) for (r, c, k, b, m, t, a) in inj if r0 <= r < r1 and c0 <= c < c1]
+        ref = oracle.ftgemm(Ab, Bb, out="bf16", tile_m=tm, tile_n=tn, bk=plan.bk, u_acc=plan.u_acc,
+                            lambda1=plan.lambda1, lambda2=plan.lambda2, injections=loc)
+        assert ref.counts["corrected"] == len(loc)
+        blk = Ch[r0:r1, c0:c1].astype(np.float64)
+        rel = np.linalg.norm(blk - ref.C) / np.linalg.norm(ref.C)
+        assert rel < TOL["bf16"], (ti, tj, rel)
+        mine = sorted((e["row"] - r0, e["col"] - c0) for e in events if e["tile_m"] == ti and e["tile_n"] == tj)
+        assert mine == sorted((e["row"], e["col"]) for e in ref.events)
+
+
+# --------------------------------------------------------------- API errors --
+
+def test_device_argument_errors():
+    import torch
+    F = ftmod()
+    A = torch.zeros(64, 64, dtype=torch.bfloat16, device="cuda")
+    C = torch.zeros(64, 64, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(F.FtgemmError) as e:
+        F.run("bf16", A[:, 1:], A[1:, :], C[:, 1:], ft_level=F.FT_OFF)     # misaligned base
+    assert e.value.code == 2
+    g = F.FTGemm("bf16", 64, 64, 64)
+    with pytest.raises(F.FtgemmError) as e:
+        F.run("bf16", A, A, C, ft_level=F.FT_OFF, injections=[(0, 0, 0, 3, 0, 0, 0.0)], enc_ws=g.enc_ws,
+              report_ws=g.report_ws)
+    assert e.value.code == 1
