@@ -95,7 +95,7 @@ Geometry geometry(const ftgemm_plan_t& p, int64_t K) {
     g.elt = p.dtype == FTGEMM_BF16 ? 2 : 4;
     g.tc = p.dtype != FTGEMM_F32_SIMT;
     g.nkc_a = (g.kp + 255) / 256;
-    g.nkc_b = g.tc ? g.nkb : (g.kp + 255) / 256;
+    g.nkc_b = (g.kp + 255) / 256;
     return g;
 }
 
@@ -295,9 +295,10 @@ int ftgemm_run(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const vo
         CUtensorMap mA, mB;
         if ((e = make_map(&mA, dt, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * elt, (uint32_t)p.bk, (uint32_t)bmd))) return e;
         if (ft) {
-            // the encoded operand B^r (K-major, tiles_n * bn rows of kp) from the encode workspace
-            if ((e = make_map(&mB, dt, enc + L.bt, (uint64_t)g.kp, (uint64_t)g.tiles_n * p.bn, (uint64_t)g.kp * elt,
-                              (uint32_t)p.bk, (uint32_t)p.bn))) return e;
+            // the encoded operand B^r (N-major, kp rows of tiles_n * bn) from the encode workspace
+            const uint64_t ldt = (uint64_t)g.tiles_n * p.bn;
+            if ((e = make_map(&mB, dt, enc + L.bt, ldt, (uint64_t)g.kp, ldt * elt, boxn, (uint32_t)p.bk,
+                              tf32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B))) return e;
         } else {
             if ((e = make_map(&mB, dt, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb * elt, boxn, (uint32_t)p.bk,
                               tf32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B))) return e;

@@ -79,13 +79,13 @@ struct Geometry {
 //           of e^T A per (tile, k-block), 3 x 128 bytes, already in the smem
 //           SWIZZLE_128B order of MMA rows 125..127), row norms, tile norms.
 //   B part: Br (FP32 B e per tile), Bt (tensor-core paths: the encoded operand
-//           B^r = [B_j, B_j e] of PAPER.md Eq. (2) per check tile j, stored
-//           K-major as bn rows x kp: rows 0..bnd-1 = columns of B_j, rows
-//           bnd..bnd+2 = split(B_j e), row bn-1 = 0), column norms, tile norms.
+//           B^r = [B_j, B_j e] of PAPER.md Eq. (2), N-major, kp rows of
+//           tiles_n * bn: tile j's slot holds columns 0..bnd-1 of B_j, then
+//           split(B_j e) (3 columns) and a zero column), column norms, tile norms.
 struct EncLayout {
-    size_t ac, y, rownorm, acnorm, rn2;       // A part
-    size_t b_off;                             // start of the B part
-    size_t br, bt, colnorm, brnorm, cn2;      // absolute offsets
+    size_t ac, y, rownorm, acnorm, rn2, acn2, cnt_a;     // A part
+    size_t b_off;                                        // start of the B part
+    size_t br, bt, colnorm, brnorm, cn2, brn2, cnt_b;    // absolute offsets
     size_t a_bytes, b_bytes, total;
 };
 
@@ -99,6 +99,8 @@ inline EncLayout enc_layout(const Geometry& g, int64_t M, int64_t N) {
     L.rownorm = o; o = align256(o + sizeof(float) * (size_t)M);
     L.acnorm = o;  o = align256(o + sizeof(float) * (size_t)g.tiles_m);
     L.rn2 = o;     o = align256(o + sizeof(float) * (size_t)g.nkc_a * M);
+    L.acn2 = o;    o = align256(o + sizeof(float) * (size_t)g.nkc_a * g.tiles_m);
+    L.cnt_a = o;   o = align256(o + sizeof(int) * (size_t)g.tiles_m);
     L.a_bytes = o;
     L.b_off = o;
     L.br = o;      o = align256(o + sizeof(float) * (size_t)g.tiles_n * g.kp);
@@ -106,6 +108,8 @@ inline EncLayout enc_layout(const Geometry& g, int64_t M, int64_t N) {
     L.colnorm = o; o = align256(o + sizeof(float) * (size_t)N);
     L.brnorm = o;  o = align256(o + sizeof(float) * (size_t)g.tiles_n);
     L.cn2 = o;     o = align256(o + sizeof(float) * (size_t)g.nkc_b * N);
+    L.brn2 = o;    o = align256(o + sizeof(float) * (size_t)g.nkc_b * g.tiles_n);
+    L.cnt_b = o;   o = align256(o + sizeof(int) * (size_t)g.tiles_n);
     L.b_bytes = o - L.b_off;
     L.total = o;
     return L;

@@ -3,18 +3,22 @@
 //
 //   encode A (Eq. (1), A^c = [A; e^T A]):  per check tile i
 //       Ac_i[k] = sum_{p in tile rows} A[p,k]            (FP32)
-//       Y_i     = exact 3-way split of Ac_i into operand-format values
-//                 (hi + mid + lo == Ac_i), appended to the MMA's A tile as
-//                 rows 125..127 by the fused kernel
+//       Ypack_i = exact 3-way split of Ac_i into operand-format values
+//                 (hi + mid + lo == Ac_i), pre-swizzled as MMA rows 125..127
 //       ||A[p,:]||_2 per row, ||Ac_i||_2 per tile         (threshold, R1)
 //   encode B (Eq. (2), B^r = [B, B e]):   per check tile j
-//       Br_j[k] = sum_{q in tile cols} B[k,q], split X_j (appended as columns
-//       BN-4..BN-2 of the MMA's B tile), ||B[:,q]||_2, ||Br_j||_2.
+//       Br_j[k] = sum_{q in tile cols} B[k,q]            (FP32)
+//       Bt_j    = B^r_j = [B_j, split(B_j e), 0], K-major (tensor-core paths)
+//       ||B[:,q]||_2 per column, ||Br_j||_2 per tile.
 //
-// Both are single streaming passes over the operand (HBM bound); the only
-// other traffic is the small outputs.  TF32 mode sums the values exactly as the
-// tensor core will see them (low 13 mantissa bits dropped), so that the
-// carried references and the main product are built from the same operands.
+// Single streaming passes over each operand (HBM bound): loads are 8- or
+// 16-byte vectors, issued in unrolled batches before use (memory-level
+// parallelism), reductions go through warp shuffles and shared memory.  The
+// per-row / per-column norms are reduced across K-chunk blocks by the LAST
+// block of each tile (atomic ticket, self-resetting), so no extra launch is
+// needed.  TF32 mode sums the values exactly as the tensor core will see them
+// (low 13 mantissa bits dropped), so the carried references and the main
+// product are built from the same operands.
 #include <cstdint>
 #include <type_traits>
 
@@ -22,54 +26,22 @@
 
 namespace ftg {
 
-__device__ __forceinline__ void load8_bf16(const uint16_t* p, int valid, float (&v)[8]) {
-    if (valid >= 8) {
-        uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
-        uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            v[2 * i] = __uint_as_float(w[i] << 16);
-            v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = (i < valid) ? bf16_to_f32(__ldg(p + i)) : 0.0f;
-    }
-}
-__device__ __forceinline__ void load8_f32(const float* p, int valid, float (&v)[8]) {
-    if (valid >= 8) {
-        float4 a = __ldg(reinterpret_cast<const float4*>(p));
-        float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
-        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-    } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = (i < valid) ? __ldg(p + i) : 0.0f;
-    }
-}
-__device__ __forceinline__ void load4_bf16(const uint16_t* p, int valid, float (&v)[4]) {
-    if (valid >= 4) {
-        uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
-        v[0] = __uint_as_float(u.x << 16); v[1] = __uint_as_float(u.x & 0xFFFF0000u);
-        v[2] = __uint_as_float(u.y << 16); v[3] = __uint_as_float(u.y & 0xFFFF0000u);
-    } else {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) v[i] = (i < valid) ? bf16_to_f32(__ldg(p + i)) : 0.0f;
-    }
-}
-__device__ __forceinline__ void load4_f32(const float* p, int valid, float (&v)[4]) {
-    if (valid >= 4) {
-        float4 a = __ldg(reinterpret_cast<const float4*>(p));
-        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-    } else {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) v[i] = (i < valid) ? __ldg(p + i) : 0.0f;
-    }
-}
-
 __device__ __forceinline__ float warp_sum(float x) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
     return x;
+}
+
+// sum over the 256 threads of a block (result valid in every thread)
+__device__ __forceinline__ float block_sum256(float x, float* red8) {
+    x = warp_sum(x);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red8[threadIdx.x >> 5] = x;
+    __syncthreads();
+    float t = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += red8[i];
+    return t;
 }
 
 // Exact three-term split of an FP32 value into operand-format values.
@@ -89,47 +61,168 @@ __device__ __forceinline__ void split3(float s, float& hi, float& mid, float& lo
     }
 }
 
-// MODE: 0 = BF16 operands, 1 = TF32 (FP32 storage, truncated), 2 = FP32 SIMT (no split)
+// 8 consecutive operand values of a row starting at p (valid = elements inside K)
 template <int MODE>
-__global__ void __launch_bounds__(256) encode_a_kernel(const void* __restrict__ A_, int64_t lda, int M, int K,
-                                                       int bmd, int kp, int bk, float* __restrict__ Ac,
-                                                       void* __restrict__ Y_, float* __restrict__ rn2) {
+__device__ __forceinline__ void load8(const void* base, int64_t off, int valid, float (&v)[8]) {
+    if constexpr (MODE == 0) {
+        const uint16_t* p = reinterpret_cast<const uint16_t*>(base) + off;
+        if (valid >= 8) {
+            const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                v[2 * i] = __uint_as_float(w[i] << 16);
+                v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = (i < valid) ? bf16_to_f32(__ldg(p + i)) : 0.0f;
+        }
+    } else {
+        const float* p = reinterpret_cast<const float*>(base) + off;
+        if (valid >= 8) {
+            const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+            const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+            v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = (i < valid) ? __ldg(p + i) : 0.0f;
+        }
+        if constexpr (MODE == 1) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = tf32_trunc(v[i]);
+        }
+    }
+}
+
+// sum_{c < n} p[c * stride]: independent loads in flight (the partial-norm
+// reductions of the last block sit on the kernel's critical tail)
+__device__ __forceinline__ float strided_sum(const float* p, int n, int64_t stride) {
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    int c = 0;
+    for (; c + 4 <= n; c += 4) {
+        a0 += p[(int64_t)c * stride];
+        a1 += p[(int64_t)(c + 1) * stride];
+        a2 += p[(int64_t)(c + 2) * stride];
+        a3 += p[(int64_t)(c + 3) * stride];
+    }
+    for (; c < n; ++c) a0 += p[(int64_t)c * stride];
+    return (a0 + a1) + (a2 + a3);
+}
+
+// Returns true in every thread of the block that arrives last for ticket[idx];
+// that block then sees all partial results of the others.  Resets the ticket.
+__device__ __forceinline__ bool last_block(int* ticket, int idx, int nblocks, int* s_flag) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int prev = atomicAdd(&ticket[idx], 1);
+        *s_flag = (prev == nblocks - 1);
+        if (*s_flag) ticket[idx] = 0;
+    }
+    __syncthreads();
+    const bool last = *s_flag != 0;
+    if (last) __threadfence();
+    return last;
+}
+
+// ---------------------------------------------------------------- encode A --
+// grid (nkc = ceil(kp/256), tiles_m); block 256 = 8 warps.  Lane l owns k in
+// [kc*256 + 8l, +8); warp w sums rows w, w+8, ... of the tile (4 rows per batch).
+// MODE: 0 = BF16, 1 = TF32 (FP32 storage, truncated), 2 = FP32 SIMT (no split).
+template <int MODE>
+__global__ void __launch_bounds__(256) encode_a_kernel(const void* __restrict__ A, int64_t lda, int M, int K,
+                                                       int bmd, int kp, int bk, int nkc, float* __restrict__ Ac,
+                                                       uint8_t* __restrict__ Y, float* rn2, float* acn2, int* ticket,
+                                                       float* __restrict__ rownorm, float* __restrict__ acnorm) {
     __shared__ float red[8][257];
+    __shared__ float red8[8];
+    __shared__ int s_flag;
     const int kc = blockIdx.x, ti = blockIdx.y;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int k0 = kc * 256 + lane * 8;
-    const int valid = K - k0;             // elements of this lane's 8 inside K
+    const int valid = K - k0;
     float ac[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) ac[i] = 0.0f;
     const int rbeg = ti * bmd;
     const int rend = min(M, rbeg + bmd);
-    for (int row = rbeg + w; row < rend; row += 8) {
-        float v[8];
-        if (valid > 0) {
-            if constexpr (MODE == 0) load8_bf16(reinterpret_cast<const uint16_t*>(A_) + (int64_t)row * lda + k0, valid, v);
-            else load8_f32(reinterpret_cast<const float*>(A_) + (int64_t)row * lda + k0, valid, v);
+    // rows w, w+8, ... of the tile; RB rows per batch so that RB independent
+    // 16-byte loads per lane are in flight (BF16 keeps them packed until use)
+    constexpr int RB = MODE == 0 ? 8 : 4;
+    for (int row = rbeg + w; row < rend; row += 8 * RB) {
+        float sq[RB];
+        if constexpr (MODE == 0) {
+            uint4 raw[RB];
+#pragma unroll
+            for (int u = 0; u < RB; ++u) {
+                const int r = row + 8 * u;
+                raw[u] = make_uint4(0u, 0u, 0u, 0u);
+                if (r < rend && valid >= 8) {
+                    raw[u] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(A) + (int64_t)r * lda + k0));
+                } else if (r < rend && valid > 0) {
+                    float v[8];
+                    load8<0>(A, (int64_t)r * lda + k0, valid, v);
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        pk[i] = (__float_as_uint(v[2 * i]) >> 16) | (__float_as_uint(v[2 * i + 1]) & 0xFFFF0000u);
+                    raw[u] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < RB; ++u) {
+                const uint32_t wd[4] = {raw[u].x, raw[u].y, raw[u].z, raw[u].w};
+                float q = 0.0f;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float lo = __uint_as_float(wd[i] << 16), hi = __uint_as_float(wd[i] & 0xFFFF0000u);
+                    ac[2 * i] += lo;
+                    ac[2 * i + 1] += hi;
+                    q = fmaf(lo, lo, q);
+                    q = fmaf(hi, hi, q);
+                }
+                sq[u] = q;
+            }
         } else {
+            float v[RB][8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) v[i] = 0.0f;
-        }
-        float sq = 0.0f;
+            for (int u = 0; u < RB; ++u) {
+                const int r = row + 8 * u;
+                if (r < rend && valid > 0) load8<MODE>(A, (int64_t)r * lda + k0, valid, v[u]);
+                else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            float x = (MODE == 1) ? tf32_trunc(v[i]) : v[i];
-            ac[i] += x;
-            sq = fmaf(x, x, sq);
+                    for (int i = 0; i < 8; ++i) v[u][i] = 0.0f;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < RB; ++u) {
+                float q = 0.0f;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    ac[i] += v[u][i];
+                    q = fmaf(v[u][i], v[u][i], q);
+                }
+                sq[u] = q;
+            }
         }
-        sq = warp_sum(sq);
-        if (lane == 0) rn2[(int64_t)kc * M + row] = sq;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int u = 0; u < RB; ++u) sq[u] += __shfl_xor_sync(0xffffffffu, sq[u], o);
+        if (lane == 0) {
+#pragma unroll
+            for (int u = 0; u < RB; ++u)
+                if (row + 8 * u < rend) rn2[(int64_t)kc * M + row + 8 * u] = sq[u];
+        }
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) red[w][lane * 8 + i] = ac[i];
     __syncthreads();
     const int t = threadIdx.x;
     const int k = kc * 256 + t;
+    float s = 0.0f;
     if (k < kp) {
-        float s = 0.0f;
 #pragma unroll
         for (int ww = 0; ww < 8; ++ww) s += red[ww][t];
         if (k >= K) s = 0.0f;
@@ -140,11 +233,11 @@ __global__ void __launch_bounds__(256) encode_a_kernel(const void* __restrict__ 
             // Ypack[tile][k-block][r][128 bytes]: split row r lands in MMA row
             // 125 + r of the A tile, whose 16-byte chunks are stored in the
             // SWIZZLE_128B order (chunk c at c ^ (row & 7)) so the fused kernel
-            // can bulk-copy the 384 bytes straight into shared memory.
+            // bulk-copies the 384 bytes straight into shared memory.
             constexpr int ELT = MODE == 0 ? 2 : 4;
             const int kb = k / bk, kk = k % bk;
             const int chunk = (kk * ELT) >> 4, within = (kk * ELT) & 15;
-            uint8_t* yb = reinterpret_cast<uint8_t*>(Y_) + ((int64_t)ti * (kp / bk) + kb) * 384;
+            uint8_t* yb = Y + ((int64_t)ti * (kp / bk) + kb) * 384;
             const float parts[3] = {hi, mid, lo};
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
@@ -155,15 +248,23 @@ __global__ void __launch_bounds__(256) encode_a_kernel(const void* __restrict__ 
             }
         }
     }
+    const float s2 = block_sum256(s * s, red8);
+    if (t == 0) acn2[(int64_t)ti * nkc + kc] = s2;
+    if (last_block(ticket, ti, nkc, &s_flag)) {
+        for (int p = rbeg + t; p < rend; p += 256) rownorm[p] = sqrtf(strided_sum(rn2 + p, nkc, M));
+        if (t == 0) acnorm[ti] = sqrtf(strided_sum(acn2 + (int64_t)ti * nkc, nkc, 1));
+    }
 }
 
-// FP32 SIMT path: B e per tile, column sums of squares (no operand copy).
-// Each warp reduces whole k-rows of one check tile j along its bnd columns
-// (4-element chunks, lane l owns chunks l and l+32).
+// ----------------------------------------------------- encode B (FP32 SIMT) --
+// grid (nkc = ceil(kp/256), tiles_n): Br_j (warp per k-row) and column squares.
 __global__ void __launch_bounds__(256) encode_b_simt_kernel(const float* __restrict__ B, int64_t ldb, int N, int K,
-                                                            int bnd, int kp, float* __restrict__ Br,
-                                                            float* __restrict__ cn2) {
+                                                            int bnd, int kp, int nkc, float* __restrict__ Br,
+                                                            float* cn2, float* brn2, int* ticket,
+                                                            float* __restrict__ colnorm, float* __restrict__ brnorm) {
     __shared__ float red[8][257];
+    __shared__ float red8[8];
+    __shared__ int s_flag;
     const int kc = blockIdx.x, tj = blockIdx.y;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nch = bnd / 4;
@@ -171,6 +272,7 @@ __global__ void __launch_bounds__(256) encode_b_simt_kernel(const float* __restr
     float csq[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) csq[i] = 0.0f;
+    float bq = 0.0f;
     for (int r = w; r < 256; r += 8) {
         const int k = kc * 256 + r;
         if (k >= kp) break;
@@ -179,10 +281,17 @@ __global__ void __launch_bounds__(256) encode_b_simt_kernel(const float* __restr
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int ch = lane + 32 * h;
-                if (ch < nch) {
-                    const int col = c0 + ch * 4;
-                    float v[4] = {0.f, 0.f, 0.f, 0.f};
-                    if (N - col > 0) load4_f32(B + (int64_t)k * ldb + col, N - col, v);
+                const int col = c0 + ch * 4;
+                if (ch < nch && col < N) {
+                    const float* p = B + (int64_t)k * ldb + col;
+                    float v[4];
+                    if (N - col >= 4) {
+                        const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+                        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) v[i] = (col + i < N) ? __ldg(p + i) : 0.0f;
+                    }
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         s += v[i];
@@ -193,6 +302,7 @@ __global__ void __launch_bounds__(256) encode_b_simt_kernel(const float* __restr
         }
         s = warp_sum(s);
         if (lane == 0) Br[(int64_t)tj * kp + k] = s;
+        bq = fmaf(s, s, bq);                       // identical in every lane
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h)
@@ -201,6 +311,7 @@ __global__ void __launch_bounds__(256) encode_b_simt_kernel(const float* __restr
             const int ch = lane + 32 * h;
             if (ch < nch) red[w][ch * 4 + i] = csq[h * 4 + i];
         }
+    if (lane == 0) red8[w] = bq;
     __syncthreads();
     for (int t = threadIdx.x; t < bnd; t += 256) {
         const int col = c0 + t;
@@ -211,129 +322,154 @@ __global__ void __launch_bounds__(256) encode_b_simt_kernel(const float* __restr
             cn2[(int64_t)kc * N + col] = s;
         }
     }
+    if (threadIdx.x == 0) {
+        float s = 0.0f;
+        for (int i = 0; i < 8; ++i) s += red8[i];
+        brn2[(int64_t)tj * nkc + kc] = s;
+    }
+    if (last_block(ticket, tj, nkc, &s_flag)) {
+        for (int t = threadIdx.x; t < bnd; t += 256) {
+            const int col = c0 + t;
+            if (col < N) colnorm[col] = sqrtf(strided_sum(cn2 + col, nkc, N));
+        }
+        if (threadIdx.x == 0) brnorm[tj] = sqrtf(strided_sum(brn2 + (int64_t)tj * nkc, nkc, 1));
+    }
 }
 
-// Tensor-core paths: one block per (k-block of KC = one 128-byte row of K,
-// check tile j).  Stages B[k0:k0+KC, c0:c0+bnd] in shared memory (row stride
-// 257 elements: conflict-free transpose), reduces B_j e per k-row (warp
-// shuffles), the column sums of squares, and writes the encoded operand
-// B^r_j = [B_j, split(B_j e), 0] transposed (K-major, bn rows of KC) with
-// coalesced 128-byte row stores.
+// -------------------------------------------- encode B (tensor-core paths) --
+// grid (nkc = ceil(kp/256), tiles_n); warp w handles k-rows kc*256 + w + 8i.
+// Per k-row of check tile j the warp streams the bnd data columns (4-element
+// chunks: lane l owns chunks l and l+32), reduces B_j e with warp shuffles,
+// accumulates column squares in registers, and writes the encoded operand row
+//     Bt[k][j*bn : (j+1)*bn] = [B[k, j*bnd : j*bnd+bnd], split(B_j e)[k], 0]
+// (B^r of Eq. (2), N-major, every tile slot 16-byte / 128-byte aligned so the
+// fused kernel's TMA boxes start on cache-line boundaries).
 template <int MODE>
 __global__ void __launch_bounds__(256) encode_b_tc_kernel(const void* __restrict__ B_, int64_t ldb, int N, int K,
-                                                          int bnd, int bn, int kp, float* __restrict__ Br,
-                                                          void* __restrict__ Bt_, float* __restrict__ cn2) {
+                                                          int bnd, int bn, int kp, int ldt, int nkc,
+                                                          float* __restrict__ Br, uint8_t* __restrict__ Bt,
+                                                          float* cn2, float* brn2, int* ticket,
+                                                          float* __restrict__ colnorm, float* __restrict__ brnorm) {
     constexpr int ELT = MODE == 0 ? 2 : 4;
-    constexpr int KC = 128 / ELT;
-    constexpr int S = 257;
     using T = typename std::conditional<MODE == 0, uint16_t, float>::type;
-    __shared__ T sb[KC * S];
-    __shared__ float br_s[KC];
+    using V = typename std::conditional<MODE == 0, uint2, uint4>::type;     // 4 elements
+    constexpr int RB = 4;                                                   // rows per batch
+    __shared__ float red[8][257];
+    __shared__ float red8[8];
+    __shared__ int s_flag;
     const int kc = blockIdx.x, tj = blockIdx.y;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int k0 = kc * KC, c0 = tj * bnd;
-    const int nch = bnd / 4;
-    // ---- load (coalesced 4-element chunks) ----
-    for (int idx = threadIdx.x; idx < KC * nch; idx += 256) {
-        const int kk = idx / nch, ch = idx - kk * nch;
-        const int k = k0 + kk, col = c0 + ch * 4;
-        float v[4] = {0.f, 0.f, 0.f, 0.f};
-        if (k < K && col < N) {
-            if constexpr (MODE == 0) load4_bf16(reinterpret_cast<const uint16_t*>(B_) + (int64_t)k * ldb + col, N - col, v);
-            else load4_f32(reinterpret_cast<const float*>(B_) + (int64_t)k * ldb + col, N - col, v);
+    const int c0 = tj * bnd;
+    const int nch = bnd / 4;                  // data chunks; chunk index nch is the split slot
+    float colq[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) colq[i] = 0.0f;
+    float bq = 0.0f;
+    auto to_f = [](T x) -> float {
+        if constexpr (MODE == 0) return bf16_to_f32(x);
+        else return tf32_trunc(x);
+    };
+    for (int r = w; r < 256; r += 8 * RB) {
+        V raw[RB][2];
+        float s[RB];
+#pragma unroll
+        for (int u = 0; u < RB; ++u) {
+            const int k = kc * 256 + r + 8 * u;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int ch = lane + 32 * h;
+                const int col = c0 + ch * 4;
+                V x;
+                if constexpr (MODE == 0) x = make_uint2(0u, 0u); else x = make_uint4(0u, 0u, 0u, 0u);
+                if (k < K && ch < nch && col < N) {
+                    const T* p = reinterpret_cast<const T*>(B_) + (int64_t)k * ldb + col;
+                    if (N - col >= 4) {
+                        x = __ldg(reinterpret_cast<const V*>(p));
+                    } else {
+                        alignas(16) T e4[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) e4[q] = (col + q < N) ? __ldg(p + q) : T(0);
+                        x = *reinterpret_cast<V*>(e4);
+                    }
+                }
+                raw[u][h] = x;
+            }
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            if constexpr (MODE == 0) sb[kk * S + ch * 4 + i] = f32_to_bf16_rn(v[i]);   // exact (bf16 values)
-            else sb[kk * S + ch * 4 + i] = tf32_trunc(v[i]);
-        }
-    }
-    __syncthreads();
-    auto val = [&](int kk, int n) -> float {
-        if constexpr (MODE == 0) return bf16_to_f32(sb[kk * S + n]);
-        else return sb[kk * S + n];
-    };
-    // ---- B_j e per k-row ----
-    for (int kk = w; kk < KC; kk += 8) {
-        float s = 0.0f;
-        for (int n = lane; n < bnd; n += 32) s += val(kk, n);
-        s = warp_sum(s);
-        if (lane == 0) {
-            br_s[kk] = s;
-            Br[(int64_t)tj * kp + k0 + kk] = s;
-        }
-    }
-    // ---- column sums of squares (partial over this k-block) ----
-    for (int n = threadIdx.x; n < bnd; n += 256) {
-        float q = 0.0f;
-        for (int kk = 0; kk < KC; ++kk) { const float x = val(kk, n); q = fmaf(x, x, q); }
-        if (c0 + n < N) cn2[(int64_t)kc * N + c0 + n] = q;
-    }
-    __syncthreads();
-    // ---- write B^r rows (K-major) ----
-    for (int n = w; n < bn; n += 8) {
-        uint8_t* dst = reinterpret_cast<uint8_t*>(Bt_) + (((int64_t)tj * bn + n) * kp + k0) * ELT;
-        if constexpr (MODE == 0) {
-            uint32_t pk;
-            const int kk = 2 * lane;
-            if (n < bnd) {
-                pk = (uint32_t)sb[kk * S + n] | ((uint32_t)sb[(kk + 1) * S + n] << 16);
-            } else if (n < bnd + 3) {
-                float p0[3], p1[3];
-                split3<0>(br_s[kk], p0[0], p0[1], p0[2]);
-                split3<0>(br_s[kk + 1], p1[0], p1[1], p1[2]);
-                const int r = n - bnd;
-                pk = (uint32_t)f32_to_bf16_rn(p0[r]) | ((uint32_t)f32_to_bf16_rn(p1[r]) << 16);
-            } else {
-                pk = 0u;
+        for (int u = 0; u < RB; ++u) {
+            float acc = 0.0f;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const T* e4 = reinterpret_cast<const T*>(&raw[u][h]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float x = to_f(e4[q]);
+                    acc += x;
+                    colq[h * 4 + q] = fmaf(x, x, colq[h * 4 + q]);
+                }
             }
-            reinterpret_cast<uint32_t*>(dst)[lane] = pk;
-        } else {
-            const int kk = lane;
-            float v;
-            if (n < bnd) {
-                v = sb[kk * S + n];
-            } else if (n < bnd + 3) {
-                float p[3];
-                split3<1>(br_s[kk], p[0], p[1], p[2]);
-                v = p[n - bnd];
-            } else {
-                v = 0.0f;
+            s[u] = acc;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int u = 0; u < RB; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
+#pragma unroll
+        for (int u = 0; u < RB; ++u) {
+            const int k = kc * 256 + r + 8 * u;
+            if (k >= kp) continue;
+            uint8_t* row = Bt + ((int64_t)k * ldt + (int64_t)tj * bn) * ELT;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int ch = lane + 32 * h;
+                if (ch < nch) {
+                    *reinterpret_cast<V*>(row + ch * 4 * ELT) = raw[u][h];
+                } else if (ch == nch) {               // the split of B_j e, then a zero column
+                    float hi, mid, lo;
+                    split3<MODE>(s[u], hi, mid, lo);
+                    if constexpr (MODE == 0) {
+                        uint2 pk;
+                        pk.x = (uint32_t)f32_to_bf16_rn(hi) | ((uint32_t)f32_to_bf16_rn(mid) << 16);
+                        pk.y = (uint32_t)f32_to_bf16_rn(lo);
+                        *reinterpret_cast<uint2*>(row + ch * 4 * ELT) = pk;
+                    } else {
+                        *reinterpret_cast<float4*>(row + ch * 4 * ELT) = make_float4(hi, mid, lo, 0.0f);
+                    }
+                }
             }
-            reinterpret_cast<float*>(dst)[lane] = v;
+            if (lane == 0) Br[(int64_t)tj * kp + k] = s[u];
+            bq = fmaf(s[u], s[u], bq);
         }
     }
-}
-
-// norms: rownorm[p] = sqrt(sum_c rn2[c][p]); acnorm[i] = ||Ac_i||_2.
-__global__ void __launch_bounds__(256) finalize_kernel(int n_vec, int nkc, const float* __restrict__ part,
-                                                       float* __restrict__ vecnorm, int ntiles, int kp,
-                                                       const float* __restrict__ sums, float* __restrict__ tilenorm) {
-    const int nvb = (n_vec + 255) / 256;
-    if ((int)blockIdx.x < nvb) {
-        const int i = blockIdx.x * 256 + threadIdx.x;
-        if (i < n_vec) {
-            float s = 0.0f;
-            for (int c = 0; c < nkc; ++c) s += part[(int64_t)c * n_vec + i];
-            vecnorm[i] = sqrtf(s);
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int ch = lane + 32 * h;
+            if (ch < nch) red[w][ch * 4 + q] = colq[h * 4 + q];
         }
-        return;
-    }
-    const int t = blockIdx.x - nvb;
-    if (t >= ntiles) return;
-    __shared__ float red[8];
-    float s = 0.0f;
-    for (int k = threadIdx.x; k < kp; k += 256) {
-        float x = sums[(int64_t)t * kp + k];
-        s = fmaf(x, x, s);
-    }
-    s = warp_sum(s);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    if (lane == 0) red8[w] = bq;
     __syncthreads();
+    for (int t = threadIdx.x; t < bnd; t += 256) {
+        const int col = c0 + t;
+        if (col < N) {
+            float q = 0.0f;
+#pragma unroll
+            for (int ww = 0; ww < 8; ++ww) q += red[ww][t];
+            cn2[(int64_t)kc * N + col] = q;
+        }
+    }
     if (threadIdx.x == 0) {
-        float tot = 0.0f;
-        for (int i = 0; i < 8; ++i) tot += red[i];
-        tilenorm[t] = sqrtf(tot);
+        float q = 0.0f;
+        for (int i = 0; i < 8; ++i) q += red8[i];
+        brn2[(int64_t)tj * nkc + kc] = q;
+    }
+    if (last_block(ticket, tj, nkc, &s_flag)) {
+        for (int t = threadIdx.x; t < bnd; t += 256) {
+            const int col = c0 + t;
+            if (col < N) colnorm[col] = sqrtf(strided_sum(cn2 + col, nkc, N));
+        }
+        if (threadIdx.x == 0) brnorm[tj] = sqrtf(strided_sum(brn2 + (int64_t)tj * nkc, nkc, 1));
     }
 }
 
@@ -343,34 +479,34 @@ cudaError_t launch_encode(const Geometry& g, const EncLayout& L, int64_t M, int6
                           cudaStream_t st) {
     char* base = reinterpret_cast<char*>(enc);
     const int mode = g.dtype == FTGEMM_BF16 ? 0 : (g.dtype == FTGEMM_TF32 ? 1 : 2);
+    auto F = [&](size_t off) { return reinterpret_cast<float*>(base + off); };
     if (which & 1) {
+        cudaError_t e = cudaMemsetAsync(base + L.cnt_a, 0, sizeof(int) * (size_t)g.tiles_m, st);
+        if (e != cudaSuccess) return e;
         dim3 grid(g.nkc_a, g.tiles_m);
-        float* Ac = reinterpret_cast<float*>(base + L.ac);
-        void* Y = base + L.y;
-        float* rn2 = reinterpret_cast<float*>(base + L.rn2);
-        if (mode == 0) encode_a_kernel<0><<<grid, 256, 0, st>>>(A, lda, (int)M, (int)K, g.bmd, g.kp, g.bk, Ac, Y, rn2);
-        else if (mode == 1) encode_a_kernel<1><<<grid, 256, 0, st>>>(A, lda, (int)M, (int)K, g.bmd, g.kp, g.bk, Ac, Y, rn2);
-        else encode_a_kernel<2><<<grid, 256, 0, st>>>(A, lda, (int)M, (int)K, g.bmd, g.kp, g.bk, Ac, Y, rn2);
-        const int nb = (int)((M + 255) / 256) + g.tiles_m;
-        finalize_kernel<<<nb, 256, 0, st>>>((int)M, g.nkc_a, rn2, reinterpret_cast<float*>(base + L.rownorm),
-                                            g.tiles_m, g.kp, Ac, reinterpret_cast<float*>(base + L.acnorm));
+        uint8_t* Y = reinterpret_cast<uint8_t*>(base + L.y);
+        int* tk = reinterpret_cast<int*>(base + L.cnt_a);
+#define ENC_A(MD) encode_a_kernel<MD><<<grid, 256, 0, st>>>(A, lda, (int)M, (int)K, g.bmd, g.kp, g.bk, g.nkc_a, \
+            F(L.ac), Y, F(L.rn2), F(L.acn2), tk, F(L.rownorm), F(L.acnorm))
+        if (mode == 0) ENC_A(0); else if (mode == 1) ENC_A(1); else ENC_A(2);
+#undef ENC_A
     }
     if (which & 2) {
-        float* Br = reinterpret_cast<float*>(base + L.br);
-        float* cn2 = reinterpret_cast<float*>(base + L.cn2);
+        cudaError_t e = cudaMemsetAsync(base + L.cnt_b, 0, sizeof(int) * (size_t)g.tiles_n, st);
+        if (e != cudaSuccess) return e;
+        int* tk = reinterpret_cast<int*>(base + L.cnt_b);
+        dim3 grid(g.nkc_b, g.tiles_n);
         if (mode == 2) {
-            dim3 grid(g.nkc_b, g.tiles_n);
             encode_b_simt_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(B), ldb, (int)N, (int)K, g.bnd,
-                                                       g.kp, Br, cn2);
+                                                       g.kp, g.nkc_b, F(L.br), F(L.cn2), F(L.brn2), tk,
+                                                       F(L.colnorm), F(L.brnorm));
         } else {
-            dim3 grid(g.nkc_b, g.tiles_n);
-            void* Bt = base + L.bt;
-            if (mode == 0) encode_b_tc_kernel<0><<<grid, 256, 0, st>>>(B, ldb, (int)N, (int)K, g.bnd, g.bn, g.kp, Br, Bt, cn2);
-            else encode_b_tc_kernel<1><<<grid, 256, 0, st>>>(B, ldb, (int)N, (int)K, g.bnd, g.bn, g.kp, Br, Bt, cn2);
+            uint8_t* Bt = reinterpret_cast<uint8_t*>(base + L.bt);
+#define ENC_B(MD) encode_b_tc_kernel<MD><<<grid, 256, 0, st>>>(B, ldb, (int)N, (int)K, g.bnd, g.bn, g.kp, \
+            g.tiles_n * g.bn, g.nkc_b, F(L.br), Bt, F(L.cn2), F(L.brn2), tk, F(L.colnorm), F(L.brnorm))
+            if (mode == 0) ENC_B(0); else ENC_B(1);
+#undef ENC_B
         }
-        const int nb = (int)((N + 255) / 256) + g.tiles_n;
-        finalize_kernel<<<nb, 256, 0, st>>>((int)N, g.nkc_b, cn2, reinterpret_cast<float*>(base + L.colnorm),
-                                            g.tiles_n, g.kp, Br, reinterpret_cast<float*>(base + L.brnorm));
     }
     return cudaGetLastError();
 }

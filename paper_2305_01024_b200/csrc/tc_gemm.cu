@@ -11,9 +11,10 @@
 //     A tile (128 x BK, K-major)   rows 0..124  = A_i           (TMA, 125-row box)
 //                                  rows 125..127 = split(e^T A_i) (bulk copy of the
 //                                                 pre-swizzled encode output)
-//     B tile (BN x BK, K-major)    = B^r_j = [B_j, split(B_j e), 0] materialised by
-//                                    the encode kernel (rows 0..BN-5 = B_j^T)
-//     D = A_tile B_tile^T in TMEM = [[ C_ij , C^r_ij (3 partial cols) ],
+//     B tile (BK x BN, N-major)    = B^r_j = [B_j, split(B_j e), 0] materialised by
+//                                    the encode kernel in BN-wide, 128-byte
+//                                    aligned slots (cols 0..BN-5 = B_j)
+//     D = A_tile B_tile in TMEM   = [[ C_ij , C^r_ij (3 partial cols) ],
 //                                    [ C^c_ij (3 partial rows), unused ]]
 //
 // so the check tile is 125 x (BN-4) and verification needs no extra MMA.
@@ -169,15 +170,13 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     uint8_t* sa = stage_base + s * Cfg::STAGE_BYTES;
                     uint8_t* sb = sa + Cfg::A_BYTES;
                     tma_load_2d(sa, &tmA, &full[s], kb * Cfg::BK, row0);
-                    if constexpr (FT) {
+                    if constexpr (FT)
                         bulk_load(sa + Cfg::BMD * 128, reinterpret_cast<const uint8_t*>(a.Y) +
                                   ((int64_t)ti * a.num_kb + kb) * Cfg::Y_BYTES, Cfg::Y_BYTES, &full[s]);
-                        tma_load_2d(sb, &tmB, &full[s], kb * Cfg::BK, tj * BN);
-                    } else {
+                    // B (FT off) or B^r (FT on): N-major, BN-wide tile slots on 128-byte boundaries
 #pragma unroll
-                        for (int b = 0; b < Cfg::NBOX; ++b)
-                            tma_load_2d(sb + b * Cfg::B_BOX_BYTES, &tmB, &full[s], tj * BN + b * Cfg::BOXN, kb * Cfg::BK);
-                    }
+                    for (int b = 0; b < Cfg::NBOX; ++b)
+                        tma_load_2d(sb + b * Cfg::B_BOX_BYTES, &tmB, &full[s], tj * BN + b * Cfg::BOXN, kb * Cfg::BK);
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
             }
@@ -185,7 +184,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     } else if (warp == 1) {
         // ------------------------------------------------- MMA issuer -----
         if (lane == 0) {
-            constexpr uint32_t idesc = instr_desc(kTF32, Cfg::BM, BN, false, !FT);
+            constexpr uint32_t idesc = instr_desc(kTF32, Cfg::BM, BN, false, true);
             int s = 0; uint32_t ph = 0; uint32_t injph = 0;
             int lt = 0;
             for (int t = blockIdx.x; t < a.num_tiles; t += gridDim.x, ++lt) {
@@ -207,10 +206,8 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
                     for (int kk = 0; kk < Cfg::BK / Cfg::UK; ++kk) {
                         const uint64_t ad = smem_desc_sw128(sa + kk * 32, 16, 1024);
-                        // FT: B^r is K-major like A.  FT off: B is N-major, bf16 -> SW128
-                        // (8-row atoms), tf32 -> SW128_BASE32B (4-row atoms).
-                        const uint64_t bd = FT ? smem_desc_sw128<2>(sb + kk * 32, 16, 1024)
-                                          : kTF32 ? smem_desc_sw128<1>(sb + kk * Cfg::UK * 128, Cfg::B_BOX_BYTES, 512)
+                        // B is N-major: bf16 -> SW128 (8-row atoms), tf32 -> SW128_BASE32B (4-row atoms)
+                        const uint64_t bd = kTF32 ? smem_desc_sw128<1>(sb + kk * Cfg::UK * 128, Cfg::B_BOX_BYTES, 512)
                                                   : smem_desc_sw128<2>(sb + kk * Cfg::UK * 128, Cfg::B_BOX_BYTES, 1024);
                         umma<kTF32>(d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
                     }

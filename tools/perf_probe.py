@@ -19,5 +19,10 @@ def t(fn, n=20):
     e1.record(); e1.synchronize()
     return e0.elapsed_time(e1) / n
 ms = t(lambda: g.run(A, B, C, ft_level=ft))
-print(json.dumps({"dt": dt, "M": M, "N": N, "K": K, "ft": ft, "dbg": os.environ.get("FTGEMM_DBG", "0"), "ms": ms,
-                  "tflops": 2 * M * N * K / ms / 1e9}))
+out = {"dt": dt, "M": M, "N": N, "K": K, "ft": ft, "ms": ms, "tflops": 2 * M * N * K / ms / 1e9}
+if ft:
+    ea = t(lambda: g.encode(A, None, which=1)); eb = t(lambda: g.encode(None, B, which=2))
+    el = A.element_size()
+    out.update(enc_a_ms=ea, enc_a_gbs=M * K * el / ea / 1e6, enc_b_ms=eb,
+               enc_b_gbs=(K * N * el + g.plan.tiles_n * g.plan.bn * K * el) / eb / 1e6)
+print(json.dumps(out))
