@@ -27,7 +27,7 @@ cudaError_t launch_encode(const Geometry& g, const EncLayout& L, int64_t M, int6
 
 namespace ftg {
 cudaError_t launch_tc(bool tf32, int bn, bool ft, const CUtensorMap& mA, const CUtensorMap& mB,
-                      const TcArgs& a, cudaStream_t st);
+                      const CUtensorMap& mC, const CUtensorMap& mC29, const TcArgs& a, cudaStream_t st);
 cudaError_t launch_simt(bool ft, const SimtArgs& a, cudaStream_t st);
 }  // namespace ftg
 
@@ -303,6 +303,12 @@ int ftgemm_run(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const vo
             if ((e = make_map(&mB, dt, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb * elt, boxn, (uint32_t)p.bk,
                               tf32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B))) return e;
         }
+        // C: 128-byte rows of output per thread, 32-row boxes (29 rows for the
+        // last epilogue warp of a 125-row check tile)
+        CUtensorMap mC, mC29;
+        const CUtensorMapDataType dc = tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+        if ((e = make_map(&mC, dc, C, (uint64_t)N, (uint64_t)M, (uint64_t)ldc * elt, boxn, 32))) return e;
+        if ((e = make_map(&mC29, dc, C, (uint64_t)N, (uint64_t)M, (uint64_t)ldc * elt, boxn, ft ? 29 : 32))) return e;
         TcArgs a{};
         a.M = (int)M; a.N = (int)N; a.K = (int)K; a.num_kb = num_kb;
         a.tiles_m = (int)((M + bmd - 1) / bmd); a.tiles_n = (int)((N + bnd - 1) / bnd);
@@ -315,7 +321,7 @@ int ftgemm_run(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const vo
         }
         a.tau_u = tau_u; a.tau_l1 = l1; a.tau_l2 = l2; a.sqrtK = sqk;
         a.rep = (ReportDev*)report_ws; a.inj = dinj; a.n_inj = n_inj;
-        ce = launch_tc(tf32, p.bn, ft, mA, mB, a, st);
+        ce = launch_tc(tf32, p.bn, ft, mA, mB, mC, mC29, a, st);
     }
     if (ce != cudaSuccess) return fail_cuda(ce, "kernel launch");
     g_err.clear();

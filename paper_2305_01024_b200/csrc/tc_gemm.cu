@@ -30,6 +30,7 @@
 // The accumulator is double-buffered in TMEM (2 x BN columns), so the epilogue
 // of tile t (verification included) overlaps the mainloop of tile t+1.
 #include <cstdint>
+#include <type_traits>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -55,9 +56,13 @@ struct TcCfg {
     static constexpr int BND = FT ? BN - 4 : BN;   // data cols of a check tile
     static constexpr int TMEM_COLS = 2 * BN;
     static constexpr int NCHUNK = BN / 32;
-    // epilogue shared memory
-    static constexpr int STG_FLOATS = 4 * 32 * 33;
-    static constexpr int EPI_BYTES = (STG_FLOATS + 4 * BN + BN + 2 * BN + 2 * BM) * 4 + 64;
+    // epilogue shared memory: per-warp 32 x 128-byte SWIZZLE_128B staging for the
+    // TMA stores, column partial sums, reference sums, residuals
+    static constexpr int STG_BYTES = 4 * 4096;
+    static constexpr int EPI_BYTES = STG_BYTES + (4 * BN + BN + 2 * BN + 2 * BM) * 4 + 64;
+    static constexpr int GW = kTF32 ? 32 : 64;     // output columns per 128-byte store box
+    static constexpr int NG = (BND + GW - 1) / GW; // store groups per tile
+    static constexpr int LAST = BND - GW;          // start of the last group (overlaps the previous one by BND % GW)
     static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 256;
 };
 
@@ -103,7 +108,8 @@ __device__ __forceinline__ uint32_t apply_fault(uint32_t bits, const DevInject& 
 
 template <bool kTF32, int BN, bool FT>
 __global__ void __launch_bounds__(256, 1)
-tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcArgs a) {
+tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC29, const TcArgs a) {
     using Cfg = TcCfg<kTF32, BN, FT>;
     constexpr int S = Cfg::STAGES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -111,8 +117,8 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     // __shared__ array keeps the shared address space visible to the compiler
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* stage_base = smem;
-    float* stg = reinterpret_cast<float*>(smem + S * Cfg::STAGE_BYTES);       // [4][32][33]
-    float* colsum = stg + Cfg::STG_FLOATS;                                    // [4][BN]
+    uint8_t* stg = smem + S * Cfg::STAGE_BYTES;                               // [4][4096] (1024-aligned)
+    float* colsum = reinterpret_cast<float*>(stg + Cfg::STG_BYTES);          // [4][BN]
     float* refsum = colsum + 4 * BN;                                          // [BN]
     float* cres = refsum + BN;                                                // [BN]
     float* ctau = cres + BN;                                                  // [BN]
@@ -126,7 +132,8 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     uint64_t* tm_empty = tm_full + 2;   // [2]
     uint64_t* inj_req = tm_empty + 2;
     uint64_t* inj_done = inj_req + 1;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(inj_done + 1);
+    uint64_t* cbar = inj_done + 1;      // [4]  C_in tile loads (beta != 0), one per epilogue warp
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(cbar + 4);
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
@@ -134,6 +141,8 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
+        tma_prefetch_desc(&tmC);
+        tma_prefetch_desc(&tmC29);
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -144,6 +153,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         }
         mbar_init(inj_req, 1);
         mbar_init(inj_done, 1);
+        for (int w = 0; w < 4; ++w) mbar_init(&cbar[w], 1);
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc<Cfg::TMEM_COLS>(tmem_holder);
@@ -232,8 +242,8 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const int rloc = ew * 32 + (int)lane;    // row of the 128-row tile
         const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
         const int et = threadIdx.x - 128;        // 0..127
-        float* mystg = stg + ew * 32 * 33;
-        uint32_t injph = 0;
+        uint8_t* sbuf = stg + ew * 4096;
+        uint32_t injph = 0, cph = 0;
         unsigned long long n_checked = 0;
         int lt = 0;
         for (int t = blockIdx.x; t < a.num_tiles; t += gridDim.x, ++lt) {
@@ -390,62 +400,158 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 }
             }
 
-            // ---- pass 2: alpha/beta epilogue and coalesced store ----
-            const bool do_corr = FT && kind == FTGEMM_EV_CORRECTED && rloc == pstar;
-#pragma unroll 1
-            for (int c = 0; c < Cfg::NCHUNK; ++c) {
+            // ---- pass 2: alpha/beta, SWIZZLE_128B staging, TMA stores ----
+            // Output in groups of GW columns (one 128-byte box row per thread).
+            // TMA box starts must be 16-byte aligned: BF16 check tiles (252
+            // columns) start at 0 or 4 mod 8, so the groups of odd tiles are
+            // shifted by 4 columns and the 4 columns left over (0..3 or
+            // 248..251) are written with one 8-byte store per row.  The last
+            // group ends at the tile's last data column and overlaps the
+            // previous one by OVL columns (identical values).  FT: warp 3 stores
+            // 29 rows (96..124).
+            const bool do_corr = FT && kind == FTGEMM_EV_CORRECTED && (pstar >> 5) == ew;   // warp-uniform
+            const int qs = (rloc == pstar) ? qstar : -1000;
+            const CUtensorMap* cmap = (FT && ew == 3) ? &tmC29 : &tmC;
+            const int par = (FT && !kTF32) ? (tj & 1) : 0;
+            constexpr int GW = Cfg::GW, NG = Cfg::NG;
+            constexpr int OVL = FT ? (kTF32 ? 4 : 8) : 0;
+            auto group_start = [&](int g) -> int {
+                if constexpr (!FT) return g * GW;
+                else if constexpr (kTF32) return (g == NG - 1) ? Cfg::BND - GW : g * GW;
+                else return (g == NG - 1) ? (Cfg::BND - GW - 4 * (1 - par)) : (g * GW + 4 * par);
+            };
+            const int trow = ew * 32 + (int)lane;            // row of this thread inside the tile
+            const bool row_ok = trow < bm;
+            if constexpr (FT && !kTF32) {
+                // leftover 4 columns (tile cols 0..3 for odd tiles, BND-4..BND-1 for even ones)
+                const int lo = par ? 0 : Cfg::BND - 4;
                 float v[32];
-                tmem_ld32(tb + lane_off + c * 32, v);
-                if (c == Cfg::NCHUNK - 1) {
+                tmem_ld32(tb + lane_off + (lo & ~31), v);
+                float x[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) x[i] = par ? v[i] : v[((Cfg::BND - 4) & 31) + i];
+                if (do_corr) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) x[i] = (qs == lo + i) ? corr : x[i];
+                }
+                if (row_ok && lo < bn) {
+                    uint16_t* Cp = reinterpret_cast<uint16_t*>(a.C) + (int64_t)(r0 + trow) * a.ldc + c0 + lo;
+                    float o4[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        o4[i] = a.beta != 0.0f && lo + i < bn ? fmaf(a.beta, bf16_to_f32(Cp[i]), a.alpha * x[i]) : a.alpha * x[i];
+                    if (lo + 4 <= bn) {
+                        uint2 pk;
+                        pk.x = (uint32_t)f32_to_bf16_rn(o4[0]) | ((uint32_t)f32_to_bf16_rn(o4[1]) << 16);
+                        pk.y = (uint32_t)f32_to_bf16_rn(o4[2]) | ((uint32_t)f32_to_bf16_rn(o4[3]) << 16);
+                        *reinterpret_cast<uint2*>(Cp) = pk;
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) if (lo + i < bn) Cp[i] = f32_to_bf16_rn(o4[i]);
+                    }
+                }
+            }
+            float carry[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) carry[i] = 0.0f;
+#pragma unroll 1
+            for (int g = 0; g < NG; ++g) {
+                const int cs = group_start(g);
+                float o[GW];
+                {
+                    // gather TMEM columns [cs, cs + GW) (cs mod 32 in {0, 4, 24, 28})
+                    const uint32_t base = tb + lane_off + (uint32_t)(cs & ~31);
+                    auto gather = [&](auto shc) {
+                        constexpr int SH = decltype(shc)::value;
+                        constexpr int NL = (SH + GW + 31) / 32;
+#pragma unroll
+                        for (int h = 0; h < NL; ++h) {
+                            float v[32];
+                            tmem_ld32(base + 32 * h, v);
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) {
+                                const int idx = 32 * h + i - SH;
+                                if (idx >= 0 && idx < GW) o[idx] = v[i];
+                            }
+                        }
+                    };
+                    const int sh = cs & 31;
+                    if (sh == 0) gather(std::integral_constant<int, 0>{});
+                    else if (sh == 4) gather(std::integral_constant<int, 4>{});
+                    else if (sh == 24) gather(std::integral_constant<int, 24>{});
+                    else gather(std::integral_constant<int, 28>{});
+                }
+                if (g == NG - 1) {                         // last TMEM read of this accumulator
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tm_empty[acc]);
                 }
-                if (do_corr && ((qstar + doff) >> 5) == c) {
+                if (do_corr) {
+                    const int qq = qs - cs;
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) if (i == ((qstar + doff) & 31)) v[i] = corr;
+                    for (int i = 0; i < GW; ++i) o[i] = (i == qq) ? corr : o[i];
                 }
-#pragma unroll
-                for (int i = 0; i < 32; ++i) mystg[lane * 33 + i] = v[i];
+                // the staging buffer is free once the previous store has read it
+                if (lane == 0) bulk_wait_read0();
                 __syncwarp();
-                const int cl = 2 * (lane & 15);                  // column pair inside the chunk
-                const int col = c * 32 + cl - doff;              // data column inside the tile
-                const int gcol = c0 + col;
-#pragma unroll 4
-                for (int rr = 0; rr < 32; rr += 2) {
-                    const int r = rr + (int)(lane >> 4);
-                    const int trow = ew * 32 + r;
-                    const int grow = r0 + trow;
-                    if (trow < bm && col >= 0 && col < bn) {
-                        float o0 = a.alpha * mystg[r * 33 + cl];
-                        float o1 = a.alpha * mystg[r * 33 + cl + 1];
-                        const bool pair = (col + 1 < bn);
+                const int gcol = c0 + cs, grow = r0 + ew * 32;
+                if (a.beta != 0.0f) {
+                    if (lane == 0) {
+                        mbar_arrive_expect_tx(&cbar[ew], (FT && ew == 3 ? 29 : 32) * 128);
+                        tma_load_2d(sbuf, cmap, &cbar[ew], gcol, grow);
+                    }
+                    mbar_wait(&cbar[ew], cph);
+                    cph ^= 1;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const uint4 u = ld_shared_v4(sbuf + lane * 128 + ((j ^ (lane & 7)) << 4));
+                        const uint32_t wd[4] = {u.x, u.y, u.z, u.w};
                         if constexpr (kTF32) {
-                            float* Cp = reinterpret_cast<float*>(a.C) + (int64_t)grow * a.ldc + gcol;
-                            if (a.beta != 0.0f) {
-                                o0 = fmaf(a.beta, Cp[0], o0);
-                                if (pair) o1 = fmaf(a.beta, Cp[1], o1);
-                            }
-                            if (pair) *reinterpret_cast<float2*>(Cp) = make_float2(o0, o1);
-                            else Cp[0] = o0;
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) o[4 * j + q] = fmaf(a.beta, __uint_as_float(wd[q]), a.alpha * o[4 * j + q]);
                         } else {
-                            uint16_t* Cp = reinterpret_cast<uint16_t*>(a.C) + (int64_t)grow * a.ldc + gcol;
-                            if (a.beta != 0.0f) {
-                                o0 = fmaf(a.beta, bf16_to_f32(Cp[0]), o0);
-                                if (pair) o1 = fmaf(a.beta, bf16_to_f32(Cp[1]), o1);
-                            }
-                            if (pair) {
-                                const uint32_t pk = (uint32_t)f32_to_bf16_rn(o0) | ((uint32_t)f32_to_bf16_rn(o1) << 16);
-                                *reinterpret_cast<uint32_t*>(Cp) = pk;
-                            } else {
-                                Cp[0] = f32_to_bf16_rn(o0);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                o[8 * j + 2 * q] = fmaf(a.beta, __uint_as_float(wd[q] << 16), a.alpha * o[8 * j + 2 * q]);
+                                o[8 * j + 2 * q + 1] = fmaf(a.beta, __uint_as_float(wd[q] & 0xFFFF0000u), a.alpha * o[8 * j + 2 * q + 1]);
                             }
                         }
                     }
+                    if constexpr (OVL > 0) {
+                        // overlap columns were already updated in memory: reuse the values computed then
+                        if (g == NG - 1) {
+#pragma unroll
+                            for (int i = 0; i < OVL; ++i) o[i] = carry[i];
+                        }
+#pragma unroll
+                        for (int i = 0; i < OVL; ++i) carry[i] = o[GW - OVL + i];
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < GW; ++i) o[i] *= a.alpha;
                 }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    uint32_t pk[4];
+                    if constexpr (kTF32) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) pk[q] = __float_as_uint(o[4 * j + q]);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            pk[q] = (uint32_t)f32_to_bf16_rn(o[8 * j + 2 * q]) | ((uint32_t)f32_to_bf16_rn(o[8 * j + 2 * q + 1]) << 16);
+                    }
+                    st_shared_v4(sbuf + lane * 128 + ((j ^ (lane & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
+                }
+                fence_proxy_async_smem();
                 __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(cmap, sbuf, gcol, grow);
+                    bulk_commit();
+                }
             }
         }
+        if (lane == 0) bulk_wait0();
         if (FT && et == 0 && n_checked) atomicAdd(&a.rep->counts[CNT_CHECKED], n_checked);
     }
 
@@ -459,7 +565,8 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 
 // ---------------------------------------------------------------- launch ---
 template <bool kTF32, int BN, bool FT>
-cudaError_t launch_tc_t(const CUtensorMap& mA, const CUtensorMap& mB, const TcArgs& a, cudaStream_t st) {
+cudaError_t launch_tc_t(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mC, const CUtensorMap& mC29,
+                        const TcArgs& a, cudaStream_t st) {
     using Cfg = TcCfg<kTF32, BN, FT>;
     auto kern = tc_ftgemm_kernel<kTF32, BN, FT>;
     static bool attr_set = false;
@@ -469,18 +576,20 @@ cudaError_t launch_tc_t(const CUtensorMap& mA, const CUtensorMap& mB, const TcAr
         attr_set = true;
     }
     const int grid = a.num_tiles < kNumSMsB200 ? a.num_tiles : kNumSMsB200;
-    kern<<<grid, 256, Cfg::SMEM_BYTES, st>>>(mA, mB, a);
+    kern<<<grid, 256, Cfg::SMEM_BYTES, st>>>(mA, mB, mC, mC29, a);
     return cudaGetLastError();
 }
 
 cudaError_t launch_tc(bool tf32, int bn, bool ft, const CUtensorMap& mA, const CUtensorMap& mB,
-                      const TcArgs& a, cudaStream_t st) {
+                      const CUtensorMap& mC, const CUtensorMap& mC29, const TcArgs& a, cudaStream_t st) {
+#define L_(T, B, F) launch_tc_t<T, B, F>(mA, mB, mC, mC29, a, st)
     if (tf32) {
-        if (bn == 256) return ft ? launch_tc_t<true, 256, true>(mA, mB, a, st) : launch_tc_t<true, 256, false>(mA, mB, a, st);
-        return ft ? launch_tc_t<true, 128, true>(mA, mB, a, st) : launch_tc_t<true, 128, false>(mA, mB, a, st);
+        if (bn == 256) return ft ? L_(true, 256, true) : L_(true, 256, false);
+        return ft ? L_(true, 128, true) : L_(true, 128, false);
     }
-    if (bn == 256) return ft ? launch_tc_t<false, 256, true>(mA, mB, a, st) : launch_tc_t<false, 256, false>(mA, mB, a, st);
-    return ft ? launch_tc_t<false, 128, true>(mA, mB, a, st) : launch_tc_t<false, 128, false>(mA, mB, a, st);
+    if (bn == 256) return ft ? L_(false, 256, true) : L_(false, 256, false);
+    return ft ? L_(false, 128, true) : L_(false, 128, false);
+#undef L_
 }
 
 }  // namespace ftg

@@ -1,5 +1,5 @@
-mkdir -p gpurun_out/r12
-D=gpurun_out/r12
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:tc_ftgemm -s 1 -c 1 -o $D/k128_off python tools/prof_shape.py bf16 16384 16384 128 0 > $D/a.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:tc_ftgemm -s 1 -c 1 -o $D/k128_ft python tools/prof_shape.py bf16 16384 16384 128 2 > $D/b.log 2>&1
+mkdir -p gpurun_out/r15
+D=gpurun_out/r15
+timeout 1200 python -m pytest tests -q -m gpu -x > $D/pytest_gpu.log 2>&1
+for a in "bf16 8192 8192 8192 2" "bf16 8192 8192 8192 0" "tf32 8192 8192 8192 2" "tf32 8192 8192 8192 0" "bf16 8192 8192 1024 2" "bf16 8192 8192 1024 0" "bf16 16384 16384 128 2" "bf16 16384 16384 128 0"; do timeout 120 python tools/perf_probe.py $a >> $D/perf.log 2>&1; done
 echo done
