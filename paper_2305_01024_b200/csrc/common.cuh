@@ -126,5 +126,11 @@ __device__ __forceinline__ float bf16_to_f32(uint16_t h) { return __uint_as_floa
 __device__ __forceinline__ uint16_t f32_to_bf16_rn(float x) {
     return __bfloat16_as_ushort(__float2bfloat16_rn(x));
 }
+// two floats -> packed bf16x2 (RNE), low half = a (one cvt.rn.bf16x2.f32)
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+    return r;
+}
 
 }  // namespace ftg

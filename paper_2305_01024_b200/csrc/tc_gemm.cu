@@ -56,10 +56,14 @@ struct TcCfg {
     static constexpr int BND = FT ? BN - 4 : BN;   // data cols of a check tile
     static constexpr int TMEM_COLS = 2 * BN;
     static constexpr int NCHUNK = BN / 32;
-    // epilogue shared memory: per-warp 32 x 128-byte SWIZZLE_128B staging for the
-    // TMA stores, column partial sums, reference sums, residuals
-    static constexpr int STG_BYTES = 4 * 4096;
-    static constexpr int EPI_BYTES = STG_BYTES + (4 * BN + BN + 2 * BN + 2 * BM) * 4 + 64;
+    // epilogue shared memory: per-warp double-buffered 32 x 128-byte SWIZZLE_128B
+    // staging for the TMA stores; the verification arrays (column partial sums,
+    // reference rows, residuals, thresholds) alias the staging area (pass 1 runs
+    // only after the previous tile's stores have read it)
+    static constexpr int STG_BYTES = 4 * 2 * 4096;
+    static constexpr int VER_BYTES = (4 * BN + 3 * BN + 2 * BN + 2 * BM) * 4 + 64;
+    static_assert(VER_BYTES <= STG_BYTES, "verification arrays must fit in the staging area");
+    static constexpr int EPI_BYTES = STG_BYTES;
     static constexpr int GW = kTF32 ? 32 : 64;     // output columns per 128-byte store box
     static constexpr int NG = (BND + GW - 1) / GW; // store groups per tile
     static constexpr int LAST = BND - GW;          // start of the last group (overlaps the previous one by BND % GW)
@@ -118,9 +122,9 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* stage_base = smem;
     uint8_t* stg = smem + S * Cfg::STAGE_BYTES;                               // [4][4096] (1024-aligned)
-    float* colsum = reinterpret_cast<float*>(stg + Cfg::STG_BYTES);          // [4][BN]
-    float* refsum = colsum + 4 * BN;                                          // [BN]
-    float* cres = refsum + BN;                                                // [BN]
+    float* colsum = reinterpret_cast<float*>(stg);                            // [4][BN] (aliases staging)
+    float* refrow = colsum + 4 * BN;                                          // [3][BN] split rows of C^c
+    float* cres = refrow + 3 * BN;                                            // [BN]
     float* ctau = cres + BN;                                                  // [BN]
     float* rres = ctau + BN;                                                  // [BM]
     float* rtau = rres + Cfg::BM;                                             // [BM]
@@ -242,8 +246,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const int rloc = ew * 32 + (int)lane;    // row of the 128-row tile
         const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
         const int et = threadIdx.x - 128;        // 0..127
-        uint8_t* sbuf = stg + ew * 4096;
-        uint32_t injph = 0, cph = 0;
+        uint32_t injph = 0, cph = 0, gcount = 0;   // gcount: store groups issued by this warp
         unsigned long long n_checked = 0;
         int lt = 0;
         for (int t = blockIdx.x; t < a.num_tiles; t += gridDim.x, ++lt) {
@@ -256,6 +259,16 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             const int acc = lt & 1;
             const uint32_t accph = (lt >> 1) & 1;
             const uint32_t tb = tmem_base + acc * BN;
+            // norms for this tile's thresholds, fetched before the accumulator is ready
+            float nrow = 0.f, nbr = 0.f, nac = 0.f, ncol[2] = {0.f, 0.f};
+            if constexpr (FT) {
+                if (rloc < bm) nrow = __ldg(a.rownorm + r0 + rloc);
+                nbr = __ldg(a.brnorm + tj);
+                nac = __ldg(a.acnorm + ti);
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                    if (et + 128 * h < bn) ncol[h] = __ldg(a.colnorm + c0 + et + 128 * h);
+            }
 
             // ---- mid-mainloop fault injection ----
             if (FT && a.n_inj > 0) {
@@ -292,50 +305,57 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             float corr = 0.0f;
             if (FT) {
                 // ---- pass 1: row sums, row refs, column partial sums ----
-                named_bar_sync(1, 128);          // previous tile's readers of sflag are done
+                // previous tile's stores have read the staging area (aliased below) and
+                // every reader of sflag / residual arrays is done
+                if (lane == 0) bulk_wait_read0();
+                named_bar_sync(1, 128);
                 if (et == 0) { sflag[0] = 0; sflag[1] = 0; sflag[2] = 1 << 30; sflag[3] = 1 << 30; }
                 const bool rvalid = rloc < bm;
+                const bool isref = rloc >= Cfg::BMD;      // lanes 29..31 of warp 3: split rows of e^T A B
+                const bool all_rows = ew < 3 && bm >= (ew + 1) * 32;   // warp-uniform: no row of this warp masked
                 float srow = 0.0f, rref = 0.0f;
-#pragma unroll 1
+#pragma unroll
                 for (int c = 0; c < Cfg::NCHUNK; ++c) {
                     float v[32];
                     tmem_ld32(tb + lane_off + c * 32, v);
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const int mcol = c * 32 + i;
-                        if (mcol >= doff && mcol < doff + Cfg::BND) srow += v[i];
+                    for (int i = 0; i < 32; ++i)
+                        if (c * 32 + i < Cfg::BND) srow += v[i];
+                    if (c == Cfg::NCHUNK - 1) rref = (v[28] + v[29]) + v[30];
+                    if (ew == 3 && isref) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) refrow[(rloc - Cfg::BMD) * BN + c * 32 + i] = v[i];
                     }
-                    if (xoff == 0 && c == 0) rref = (v[0] + v[1]) + v[2];
-                    if (xoff != 0 && c == Cfg::NCHUNK - 1) rref = (v[28] + v[29]) + v[30];
                     float w[32];
+                    if (all_rows) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) w[i] = rvalid ? v[i] : 0.0f;
-                    colsum[ew * BN + c * 32 + lane] = transpose_reduce32(w, lane);
-                    if (ew == 3) {
+                        for (int i = 0; i < 32; ++i) w[i] = v[i];
+                    } else {
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) w[i] = (rloc >= Cfg::BMD) ? v[i] : 0.0f;
-                        refsum[c * 32 + lane] = transpose_reduce32(w, lane);
+                        for (int i = 0; i < 32; ++i) w[i] = rvalid ? v[i] : 0.0f;
                     }
+                    colsum[ew * BN + c * 32 + lane] = transpose_reduce32(w, lane);
                 }
                 named_bar_sync(1, 128);
                 // ---- row residuals ----
                 if (rvalid) {
                     const float r = srow - rref;
-                    const float tr = a.tau_u * (a.tau_l1 * a.sqrtK * fabsf(rref) +
-                                                a.tau_l2 * __ldg(a.rownorm + r0 + rloc) * __ldg(a.brnorm + tj));
+                    const float tr = a.tau_u * (a.tau_l1 * a.sqrtK * fabsf(rref) + a.tau_l2 * nrow * nbr);
                     rres[rloc] = r; rtau[rloc] = tr;
                     if (!(fabsf(r) <= tr)) { atomicAdd(&sflag[0], 1); atomicMin(&sflag[2], rloc); }
                 }
                 // ---- column residuals ----
-                for (int col = et; col < bn; col += 128) {
-                    const int mc = col + doff;
-                    const float sc = (colsum[mc] + colsum[BN + mc]) + (colsum[2 * BN + mc] + colsum[3 * BN + mc]);
-                    const float rc = refsum[mc];
-                    const float c = sc - rc;
-                    const float tc = a.tau_u * (a.tau_l1 * a.sqrtK * fabsf(rc) +
-                                                a.tau_l2 * __ldg(a.acnorm + ti) * __ldg(a.colnorm + c0 + col));
-                    cres[col] = c; ctau[col] = tc;
-                    if (!(fabsf(c) <= tc)) { atomicAdd(&sflag[1], 1); atomicMin(&sflag[3], col); }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int col = et + 128 * h;
+                    if (col < bn && col < BN) {
+                        const float sc = (colsum[col] + colsum[BN + col]) + (colsum[2 * BN + col] + colsum[3 * BN + col]);
+                        const float rc = (refrow[col] + refrow[BN + col]) + refrow[2 * BN + col];
+                        const float c = sc - rc;
+                        const float tc = a.tau_u * (a.tau_l1 * a.sqrtK * fabsf(rc) + a.tau_l2 * nac * ncol[h]);
+                        cres[col] = c; ctau[col] = tc;
+                        if (!(fabsf(c) <= tc)) { atomicAdd(&sflag[1], 1); atomicMin(&sflag[3], col); }
+                    }
                 }
                 named_bar_sync(1, 128);
                 // ---- decide (R3-R5) ----
@@ -398,6 +418,8 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         }
                     }
                 }
+                // the verification arrays alias the staging buffers that pass 2 writes
+                named_bar_sync(1, 128);
             }
 
             // ---- pass 2: alpha/beta, SWIZZLE_128B staging, TMA stores ----
@@ -491,8 +513,11 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
                     for (int i = 0; i < GW; ++i) o[i] = (i == qq) ? corr : o[i];
                 }
-                // the staging buffer is free once the previous store has read it
-                if (lane == 0) bulk_wait_read0();
+                // double-buffered staging: the buffer is free once the store issued
+                // two groups ago has read it
+                uint8_t* sbuf = stg + ew * 8192 + (gcount & 1) * 4096;
+                ++gcount;
+                if (lane == 0) bulk_wait_read1();
                 __syncwarp();
                 const int gcol = c0 + cs, grow = r0 + ew * 32;
                 if (a.beta != 0.0f) {
@@ -526,7 +551,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
                         for (int i = 0; i < OVL; ++i) carry[i] = o[GW - OVL + i];
                     }
-                } else {
+                } else if (a.alpha != 1.0f) {
 #pragma unroll
                     for (int i = 0; i < GW; ++i) o[i] *= a.alpha;
                 }
@@ -538,8 +563,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         for (int q = 0; q < 4; ++q) pk[q] = __float_as_uint(o[4 * j + q]);
                     } else {
 #pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            pk[q] = (uint32_t)f32_to_bf16_rn(o[8 * j + 2 * q]) | ((uint32_t)f32_to_bf16_rn(o[8 * j + 2 * q + 1]) << 16);
+                        for (int q = 0; q < 4; ++q) pk[q] = pack_bf16x2(o[8 * j + 2 * q], o[8 * j + 2 * q + 1]);
                     }
                     st_shared_v4(sbuf + lane * 128 + ((j ^ (lane & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
                 }
