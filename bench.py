@@ -58,36 +58,28 @@ def load_peaks():
 # ----------------------------------------------------------- CPU oracle leg ---
 def cpu_oracle_sample(budget_s: float):
     """Time the oracle (as it stands) on a bounded tile sample of the workload:
-    whole check tiles (125 x 248 x 8192) of the 8192^3 problem, FP64, all host
+    whole check tiles (125 x 252 x 8192) of the 8192^3 problem, FP64, all host
     cores.  Returns (TFLOPS, cores, description)."""
-    import numpy as np
     import oracle
     import synth
     oracle.build()
-    tm, tn, K = 125, 248, K_DIM
-    rate_probe_tiles = 1
+    tm, tn, K = 125, 252, K_DIM                # the plan's BF16 check tile
     done_tiles, flops, t_spent = 0, 0.0, 0.0
-    tiles = []
     ti = tj = 0
     t0 = time.time()
     while True:
-        rows = (ti * tm, ti * tm + tm)
-        cols = (tj * tn, tj * tn + tn)
-        A = synth.matrix(synth.BASE_SEED + synth.SEED_A, M_PER_RANK, K, dtype="bf16", r0=rows[0], r1=rows[1])
-        B = synth.matrix(synth.BASE_SEED + synth.SEED_B, K, N_DIM, dtype="bf16", c0=cols[0], c1=cols[1])
+        A = synth.matrix(synth.BASE_SEED + synth.SEED_A, M_PER_RANK, K, dtype="bf16", r0=ti * tm, r1=ti * tm + tm)
+        B = synth.matrix(synth.BASE_SEED + synth.SEED_B, K, N_DIM, dtype="bf16", c0=tj * tn, c1=tj * tn + tn)
         t1 = time.time()
         oracle.ftgemm(A, B, out="bf16", tile_m=tm, tile_n=tn, bk=64, u_acc=2.0 ** -23, lambda1=8.0, lambda2=16.0)
         t_spent += time.time() - t1
         flops += 2.0 * tm * tn * K
         done_tiles += 1
-        tiles.append((ti, tj))
-        ti, tj = (ti + 7) % 65, (tj + 5) % 33
+        ti, tj = (ti + 7) % 65, (tj + 5) % 32
         if time.time() - t0 > budget_s or done_tiles >= 4096:
             break
-        del rate_probe_tiles
-        rate_probe_tiles = 0
     tflops = flops / t_spent / 1e12
-    return tflops, oracle.num_threads(), (f"{done_tiles} check tiles of 125x248x8192 (BF16 values, FP64 oracle incl. "
+    return tflops, oracle.num_threads(), (f"{done_tiles} check tiles of 125x252x8192 (BF16 values, FP64 oracle incl. "
                                            f"encode/verify), {flops / 1e9:.1f} GFLOP in {t_spent:.1f}s")
 
 
@@ -276,46 +268,66 @@ def run_ours(args):
 
     extra = {}
     if not args.no_sweep:
-        reps = max(10, args.steps)
-        t_off = timed([lambda: g.run(A, B, C, ft_level=F.FT_OFF)] * reps, 3)
-        t_run = timed([lambda: g.run(A, B, C, ft_level=F.FT_CORRECT)] * reps, 3)
-        t_enc = timed([lambda: g.encode(A, B)] * reps, 3)
-        t_enc_a = timed([lambda: g.encode(A, None, which=1)] * reps, 3)
-        t_cublas = timed([lambda: torch.matmul(A, B, out=C)] * reps, 3)
-        one = [site() for _ in range(1)]
-        t_one = timed([lambda: g.run(A, B, C, ft_level=F.FT_CORRECT, injections=one)] * reps, 3)
+        # comparators, measured in ROUNDS interleaved across configurations
+        # (median per configuration) so that clock / power drift hits all alike
+        reps, rounds = max(20, args.steps), 3
         stress = []
         for ti in range(pl.tiles_m):
             for tj in range(pl.tiles_n):
                 r = ti * pl.check_tile_m + (ti * 7 + tj) % min(pl.check_tile_m, Mr - ti * pl.check_tile_m)
                 c = tj * pl.check_tile_n + (tj * 5 + ti) % min(pl.check_tile_n, N - tj * pl.check_tile_n)
                 stress.append((r, c, (ti * 131 + tj * 17) % K, 30, F.INJ_FLIP, F.TGT_ACC, 0.0))
+        one = [site()]
+        configs = {
+            "ft_off": lambda: g.run(A, B, C, ft_level=F.FT_OFF),
+            "cublas": lambda: torch.matmul(A, B, out=C),
+            "ft_run": lambda: g.run(A, B, C, ft_level=F.FT_CORRECT),
+            "ft_step": lambda: step(),
+            "encode": lambda: g.encode(A, B),
+            "encode_a": lambda: g.encode(A, None, which=1),
+            "one_fault_run": lambda: g.run(A, B, C, ft_level=F.FT_CORRECT, injections=one),
+        }
+        samples = {k: [] for k in configs}
+        rate_samples = {str(int(r)): [] for r in SWEEP_RATES}
+        rate_inj = {str(int(r)): 0 for r in SWEEP_RATES}
+        for _ in range(rounds):
+            for k, fn in configs.items():
+                samples[k].append(timed([fn] * reps, 2))
+            for rate in SWEEP_RATES:
+                sc = schedule(rate, reps, est)
+                rate_inj[str(int(rate))] += sum(len(x) for x in sc)
+                rate_samples[str(int(rate))].append(timed([(lambda inj: (lambda: step(inj)))(x) for x in sc], 2))
+        med = {k: statistics.median(v) for k, v in samples.items()}
         g.reset()
         t_stress = timed([lambda: g.run(A, B, C, ft_level=F.FT_CORRECT, injections=stress)] * 3, 1)
         cs, _ = g.report(0)
         stress_ok = cs["corrected"] == 4 * len(stress) and cs["uncorrectable"] == 0
+        t_off, t_cub = med["ft_off"], med["cublas"]
         sweep = {}
         for rate in SWEEP_RATES:
-            nst = max(reps, int(math.ceil(2 * 60000.0 / max(rate, 1e-9) / est)) if rate >= 100 else reps)
-            nst = min(nst, 600)
-            sc = schedule(rate, nst, est)
-            fns = [(lambda inj: (lambda: step(inj)))(s) for s in sc]
-            t = timed(fns, 2)
-            sweep[str(int(rate))] = {"ms_per_step": t, "tflops": flops_rank * world / (t * 1e-3) / 1e12,
-                                     "steps": nst, "injected": sum(len(s) for s in sc),
-                                     "overhead_vs_ft_off_pct": 100.0 * (t - t_off) / t_off,
-                                     "overhead_vs_cublas_pct": 100.0 * (t - t_cublas) / t_cublas}
+            key = str(int(rate))
+            t = statistics.median(rate_samples[key])
+            p_inj = rate * t / 60000.0                       # faults per step at this rate
+            model = med["ft_step"] + p_inj * (med["one_fault_run"] - med["ft_run"])
+            sweep[key] = {"ms_per_step": t, "tflops": flops_rank * world / (t * 1e-3) / 1e12,
+                          "steps": reps * rounds, "injected": rate_inj[key],
+                          "overhead_vs_ft_off_pct": 100.0 * (t - t_off) / t_off,
+                          "overhead_vs_cublas_pct": 100.0 * (t - t_cub) / t_cub,
+                          "model_ms_per_step": model,
+                          "model_overhead_vs_ft_off_pct": 100.0 * (model - t_off) / t_off}
         extra = {
             "ft_off_ms": t_off, "ft_off_tflops": flops_rank * world / (t_off * 1e-3) / 1e12,
-            "cublas_ms": t_cublas, "cublas_tflops": flops_rank * world / (t_cublas * 1e-3) / 1e12,
-            "ft_run_only_ms": t_run, "encode_ms": t_enc, "encode_a_ms": t_enc_a,
-            "encode_gbs": (2 * Mr * K + 2 * K * N) / (t_enc * 1e-3) / 1e9,
-            "overhead_vs_ft_off_pct": 100.0 * (ms_step - t_off) / t_off,
-            "overhead_vs_cublas_pct": 100.0 * (ms_step - t_cublas) / t_cublas,
-            "overhead_run_only_vs_ft_off_pct": 100.0 * (t_run - t_off) / t_off,
-            "overhead_pre_encoded_B_vs_ft_off_pct": 100.0 * (t_run + t_enc_a - t_off) / t_off,
-            "one_fault_call_ms": t_one, "stress_one_fault_per_tile_ms": t_stress, "stress_faults": len(stress),
-            "stress_all_corrected": bool(stress_ok), "rate_sweep_errors_per_min": sweep,
+            "cublas_ms": t_cub, "cublas_tflops": flops_rank * world / (t_cub * 1e-3) / 1e12,
+            "ft_step_ms": med["ft_step"], "ft_run_only_ms": med["ft_run"],
+            "encode_ms": med["encode"], "encode_a_ms": med["encode_a"],
+            "encode_gbs": (2 * Mr * K + 2 * K * N + 2 * K * pl.tiles_n * pl.bn) / (med["encode"] * 1e-3) / 1e9,
+            "overhead_vs_ft_off_pct": 100.0 * (med["ft_step"] - t_off) / t_off,
+            "overhead_vs_cublas_pct": 100.0 * (med["ft_step"] - t_cub) / t_cub,
+            "overhead_run_only_vs_ft_off_pct": 100.0 * (med["ft_run"] - t_off) / t_off,
+            "overhead_pre_encoded_B_vs_ft_off_pct": 100.0 * (med["ft_run"] + med["encode_a"] - t_off) / t_off,
+            "one_fault_call_ms": med["one_fault_run"], "stress_one_fault_per_tile_ms": t_stress,
+            "stress_faults": len(stress), "stress_all_corrected": bool(stress_ok),
+            "rate_sweep_errors_per_min": sweep, "comparator_rounds": rounds, "comparator_reps": reps,
         }
 
     # ---- e2e: public API with host buffers, H2D inputs + D2H result per step ----

@@ -62,7 +62,8 @@ struct TcCfg {
     // only after the previous tile's stores have read it)
     static constexpr int STG_BYTES = 4 * 2 * 4096;
     static constexpr int VER_BYTES = (4 * BN + 3 * BN + 2 * BN + 2 * BM) * 4 + 64;
-    static_assert(VER_BYTES <= STG_BYTES, "verification arrays must fit in the staging area");
+    static_assert(VER_BYTES <= 12288, "verification arrays must fit below the transpose buffers");
+    static_assert(12288 + 4 * 32 * 36 * 4 <= STG_BYTES, "transpose buffers must fit in the staging area");
     static constexpr int EPI_BYTES = STG_BYTES;
     static constexpr int GW = kTF32 ? 32 : 64;     // output columns per 128-byte store box
     static constexpr int NG = (BND + GW - 1) / GW; // store groups per tile
@@ -313,6 +314,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 const bool rvalid = rloc < bm;
                 const bool isref = rloc >= Cfg::BMD;      // lanes 29..31 of warp 3: split rows of e^T A B
                 const bool all_rows = ew < 3 && bm >= (ew + 1) * 32;   // warp-uniform: no row of this warp masked
+                float* tbuf = reinterpret_cast<float*>(stg + 12288) + ew * (32 * 36);   // 32 x 36 transpose buffer
                 float srow = 0.0f, rref = 0.0f;
 #pragma unroll
                 for (int c = 0; c < Cfg::NCHUNK; ++c) {
@@ -326,15 +328,26 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
                         for (int i = 0; i < 32; ++i) refrow[(rloc - Cfg::BMD) * BN + c * 32 + i] = v[i];
                     }
-                    float w[32];
+                    // column partial sums over this warp's 32 rows: transpose through
+                    // shared memory (row-major writes, 16-byte column reads)
                     if (all_rows) {
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) w[i] = v[i];
+                        for (int i = 0; i < 32; ++i) tbuf[i * 36 + lane] = v[i];
                     } else {
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) w[i] = rvalid ? v[i] : 0.0f;
+                        for (int i = 0; i < 32; ++i) tbuf[i * 36 + lane] = rvalid ? v[i] : 0.0f;
                     }
-                    colsum[ew * BN + c * 32 + lane] = transpose_reduce32(w, lane);
+                    __syncwarp();
+                    {
+                        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+                        for (int r4 = 0; r4 < 8; ++r4) {
+                            const float4 x = *reinterpret_cast<const float4*>(tbuf + lane * 36 + 4 * r4);
+                            s0 += x.x; s1 += x.y; s2 += x.z; s3 += x.w;
+                        }
+                        colsum[ew * BN + c * 32 + lane] = (s0 + s1) + (s2 + s3);
+                    }
+                    __syncwarp();
                 }
                 named_bar_sync(1, 128);
                 // ---- row residuals ----
