@@ -30,7 +30,13 @@ def _deps_mtime() -> float:
     return max(os.path.getmtime(f) for f in files)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, defines=(), out: str | None = None) -> str:
+    """defines / out: development variants (e.g. -DFTGEMM_EXP_NO_Y) built to a separate library."""
+    global OBJ, LIB
+    if defines or out:
+        OBJ = os.path.join(HERE, "build_" + "_".join(d.lstrip("-D").lower() for d in defines))
+        LIB = out or os.path.join(HERE, "libftgemm_exp.so")
+        force = True
     os.makedirs(OBJ, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     dep = _deps_mtime()
@@ -39,7 +45,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         o = os.path.join(OBJ, os.path.basename(s) + ".o")
         objs.append(o)
         if force or not os.path.exists(o) or os.path.getmtime(o) < max(os.path.getmtime(s), dep):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", s, "-o", o]
+            cmd = [NVCC, *ARCH, *FLAGS, *defines, "-c", s, "-o", o]
             if verbose:
                 cmd += ["-Xptxas", "-v"]
                 print(" ".join(cmd), flush=True)
@@ -54,5 +60,5 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(verbose="--verbose" in sys.argv, force="--force" in sys.argv)
-    print(LIB)
+    defs = [a for a in sys.argv[1:] if a.startswith("-D")]
+    print(build(verbose="--verbose" in sys.argv, force="--force" in sys.argv, defines=defs))

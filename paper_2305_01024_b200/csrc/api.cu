@@ -26,8 +26,9 @@ cudaError_t launch_encode(const Geometry& g, const EncLayout& L, int64_t M, int6
 }  // namespace ftg
 
 namespace ftg {
-cudaError_t launch_tc(bool tf32, int bn, bool ft, const CUtensorMap& mA, const CUtensorMap& mB,
-                      const CUtensorMap& mC, const CUtensorMap& mC29, const TcArgs& a, cudaStream_t st);
+cudaError_t launch_tc(bool tf32, int bn, bool ft, int cg, const CUtensorMap& mA, const CUtensorMap& mB,
+                      const CUtensorMap& mC, const CUtensorMap& mC29, const CUtensorMap& mY, const TcArgs& a,
+                      cudaStream_t st);
 cudaError_t launch_simt(bool ft, const SimtArgs& a, cudaStream_t st);
 }  // namespace ftg
 
@@ -50,7 +51,6 @@ int fail_cuda(cudaError_t e, const char* where) {
     return fail(FTGEMM_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
 }
 
-constexpr int kTcGroup = 16;    // must match tile_coords() in tc_gemm.cu
 
 bool valid_dtype(int d) { return d == FTGEMM_F32_SIMT || d == FTGEMM_TF32 || d == FTGEMM_BF16; }
 
@@ -77,7 +77,13 @@ void fill_plan(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* p) {
         p->bm = 128; p->bn = bn; p->bk = bk;
         p->check_tile_m = 125; p->check_tile_n = bn - 4;
         p->off_tile_m = 128; p->off_tile_n = bn;
-        p->stages = bn == 256 ? 4 : 6; p->cta_group = 1;
+        // CTA pairs (cta_group::2, M = 256 per MMA) halve the B tile each SM loads
+        int cg = bn == 256 ? 1 : 1;
+        if (const char* e = getenv("FTGEMM_CG")) cg = atoi(e) == 2 ? 2 : 1;
+        p->cta_group = cg;
+        const int elt = dtype == FTGEMM_TF32 ? 4 : 2;
+        const int stage = 128 * 128 + (bn / cg) * bk * elt;
+        p->stages = std::min(8, (196 * 1024) / stage);
         p->u_acc = std::ldexp(1.0f, -23); p->lambda1 = 8.0f; p->lambda2 = 16.0f;
     }
     p->tiles_m = (M + p->check_tile_m - 1) / p->check_tile_m;
@@ -154,13 +160,16 @@ int check_dims(int dtype, int64_t M, int64_t N, int64_t K) {
     return FTGEMM_OK;
 }
 
-// schedule key of a check tile (the order the kernel walks tiles in)
+// schedule key of a check tile (the order the kernel walks work units in; a
+// unit is cta_group check tiles stacked in M, one per CTA of the pair)
 int tile_key(const ftgemm_plan_t& p, int ti, int tj) {
     if (p.dtype == FTGEMM_F32_SIMT) return ti * (int)p.tiles_n + tj;
-    const int G = kTcGroup;
-    const int grp = ti / G, first = grp * G;
-    const int gsz = std::min<int>(G, (int)p.tiles_m - first);
-    return grp * G * (int)p.tiles_n + tj * gsz + (ti - first);
+    const int cg = p.cta_group;
+    const int units_m = ((int)p.tiles_m + cg - 1) / cg, tu = ti / cg;
+    const int G = tc_group(units_m, cg);
+    const int grp = tu / G, first = grp * G;
+    const int gsz = std::min<int>(G, units_m - first);
+    return grp * G * (int)p.tiles_n + tj * gsz + (tu - first);
 }
 
 }  // namespace
@@ -250,7 +259,9 @@ int ftgemm_run(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const vo
             d.kb = (int)std::min<int64_t>(f.k_elem / p.bk, num_kb - 1);
             d.p = (int)(f.row - (int64_t)ti * p.check_tile_m);
             d.q = (int)(f.col - (int64_t)tj * p.check_tile_n);
-            d.bit = f.bit; d.mode = f.mode; d.target = f.target; d.addend = f.addend;
+            d.bit = f.bit; d.mode = f.mode; d.addend = f.addend;
+            // CTA of the pair that owns the tile in bits 8+ (the epilogue filters on it)
+            d.target = f.target | (dtype == FTGEMM_F32_SIMT ? 0 : (ti % p.cta_group) << 8);
             v[i] = d;
         }
         std::stable_sort(v.begin(), v.end(), [](const DevInject& x, const DevInject& y) {
@@ -293,7 +304,11 @@ int ftgemm_run(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const vo
         const int bnd = ft ? p.check_tile_n : p.off_tile_n;
         const uint32_t boxn = 128 / elt;
         CUtensorMap mA, mB;
+#if defined(FTGEMM_EXP_A128)
+        if ((e = make_map(&mA, dt, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * elt, (uint32_t)p.bk, 128u))) return e;
+#else
         if ((e = make_map(&mA, dt, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * elt, (uint32_t)p.bk, (uint32_t)bmd))) return e;
+#endif
         if (ft) {
             // the encoded operand B^r (N-major, kp rows of tiles_n * bn) from the encode workspace
             const uint64_t ldt = (uint64_t)g.tiles_n * p.bn;
@@ -313,6 +328,9 @@ int ftgemm_run(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const vo
         a.M = (int)M; a.N = (int)N; a.K = (int)K; a.num_kb = num_kb;
         a.tiles_m = (int)((M + bmd - 1) / bmd); a.tiles_n = (int)((N + bnd - 1) / bnd);
         a.num_tiles = a.tiles_m * a.tiles_n;
+        a.units_m = (a.tiles_m + p.cta_group - 1) / p.cta_group;
+        a.num_units = a.units_m * a.tiles_n;
+        a.group = tc_group(a.units_m, p.cta_group);
         a.ft_level = ft_level; a.alpha = alpha; a.beta = beta; a.C = C; a.ldc = ldc;
         if (ft) {
             a.Y = enc + L.y; a.kp = g.kp;
@@ -321,7 +339,11 @@ int ftgemm_run(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const vo
         }
         a.tau_u = tau_u; a.tau_l1 = l1; a.tau_l2 = l2; a.sqrtK = sqk;
         a.rep = (ReportDev*)report_ws; a.inj = dinj; a.n_inj = n_inj;
-        ce = launch_tc(tf32, p.bn, ft, mA, mB, mC, mC29, a, st);
+        // pre-swizzled split rows of A^c: one 384-byte row per (check tile, k-block)
+        CUtensorMap mY{};
+        if (ft && (e = make_map(&mY, CU_TENSOR_MAP_DATA_TYPE_UINT32, enc + L.y, 96, (uint64_t)g.tiles_m * g.nkb, 384,
+                                96, 1, CU_TENSOR_MAP_SWIZZLE_NONE))) return e;
+        ce = launch_tc(tf32, p.bn, ft, p.cta_group, mA, mB, mC, mC29, mY, a, st);
     }
     if (ce != cudaSuccess) return fail_cuda(ce, "kernel launch");
     g_err.clear();

@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <cstdlib>
 
 #include "../../include/ftgemm.h"
 
@@ -36,6 +37,8 @@ inline size_t report_inject_offset() { return sizeof(ReportDev); }
 struct TcArgs {
     int M, N, K, num_kb;
     int tiles_m, tiles_n, num_tiles;
+    int units_m, num_units;   // work units: CG check tiles stacked in M (CG = CTAs per MMA)
+    int group;            // M-units per schedule group (tile_coords)
     int ft_level;
     float alpha, beta;
     void* C; int64_t ldc;
@@ -59,6 +62,15 @@ struct SimtArgs {
     ReportDev* rep;
     const DevInject* inj; int n_inj;
 };
+
+// M-tiles per schedule group of the tensor-core kernel: about 16, split evenly
+// so that no group is ragged (FTGEMM_GROUP overrides, for tuning)
+inline int tc_group(int units_m, int cg) {
+    int g0 = 16 / cg;
+    if (const char* e = getenv("FTGEMM_GROUP")) g0 = atoi(e) > 0 ? atoi(e) : g0;
+    const int ng = units_m / g0 > 0 ? (units_m + g0 / 2) / g0 : 1;
+    return (units_m + ng - 1) / ng;
+}
 
 // ---- tile geometry of a plan ---------------------------------------------
 struct Geometry {

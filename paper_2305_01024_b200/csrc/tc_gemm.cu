@@ -37,8 +37,9 @@
 
 namespace ftg {
 
-template <bool kTF32, int BN_, bool FT>
+template <bool kTF32, int BN_, bool FT, int CG_ = 1>
 struct TcCfg {
+    static constexpr int CG = CG_;                 // 1: one CTA per MMA; 2: CTA pair (M = 256)
     static constexpr int BM = 128;
     static constexpr int BN = BN_;
     static constexpr int ELT = kTF32 ? 4 : 2;
@@ -48,10 +49,10 @@ struct TcCfg {
     static constexpr int NBOX = BN / BOXN;
     static constexpr int A_BYTES = BM * 128;
     static constexpr int B_BOX_BYTES = BK * 128;
-    static constexpr int B_BYTES = NBOX * B_BOX_BYTES;
+    static constexpr int B_BYTES = (NBOX / CG) * B_BOX_BYTES;   // this CTA's share of the B tile
     static constexpr int Y_BYTES = 384;            // 3 split rows x 128 bytes
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int STAGES = (BN == 256) ? 4 : 6;
+    static constexpr int STAGES = (196 * 1024) / (A_BYTES + B_BYTES) < 8 ? (196 * 1024) / (A_BYTES + B_BYTES) : 8;
     static constexpr int BMD = FT ? BM - 3 : BM;   // data rows of a check tile
     static constexpr int BND = FT ? BN - 4 : BN;   // data cols of a check tile
     static constexpr int TMEM_COLS = 2 * BN;
@@ -71,8 +72,10 @@ struct TcCfg {
     static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 256;
 };
 
-__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& ti, int& tj) {
-    constexpr int G = 16;   // group of M-tiles swept together (L2 reuse of B)
+// Tile schedule: groups of G consecutive M-tiles are swept across all N-tiles
+// (M-tile fastest), so concurrently running tiles share A rows and B^r slots in
+// L2.  G comes from the host (tc_group(), also used to key fault lists).
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int G, int& ti, int& tj) {
     const int per_group = G * tiles_n;
     const int grp = t / per_group;
     const int first = grp * G;
@@ -111,11 +114,12 @@ __device__ __forceinline__ uint32_t apply_fault(uint32_t bits, const DevInject& 
     return bits ^ (1u << (f.bit & 31));
 }
 
-template <bool kTF32, int BN, bool FT>
+template <bool kTF32, int BN, bool FT, int CG>
 __global__ void __launch_bounds__(256, 1)
 tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC29, const TcArgs a) {
-    using Cfg = TcCfg<kTF32, BN, FT>;
+                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC29,
+                 const __grid_constant__ CUtensorMap tmY, const TcArgs a) {
+    using Cfg = TcCfg<kTF32, BN, FT, CG>;
     constexpr int S = Cfg::STAGES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte aligned base (SWIZZLE_128B atoms); pointer arithmetic on the
@@ -142,28 +146,34 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
+    // CTA pair: rank 0 is the MMA leader; each CTA owns 128 of the 256 MMA rows
+    // (one check tile) and half of the B tile's columns
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+    const bool leader = rank == 0;
+    const int cluster_id = blockIdx.x / CG, num_clusters = gridDim.x / CG;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
         tma_prefetch_desc(&tmC);
         tma_prefetch_desc(&tmC29);
+        if constexpr (FT) tma_prefetch_desc(&tmY);
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tm_full[b], 1);
-            mbar_init(&tm_empty[b], 4);
+            mbar_init(&tm_empty[b], 4 * CG);     // every epilogue warp of the pair
         }
         mbar_init(inj_req, 1);
-        mbar_init(inj_done, 1);
+        mbar_init(inj_done, CG);
         for (int w = 0; w < 4; ++w) mbar_init(&cbar[w], 1);
         fence_barrier_init();
     }
-    if (warp == 2) tmem_alloc<Cfg::TMEM_COLS>(tmem_holder);
+    if (warp == 2) tmem_alloc<Cfg::TMEM_COLS, CG>(tmem_holder);
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
 
@@ -171,38 +181,52 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         // ------------------------------------------------ TMA producer ----
         if (lane == 0) {
             int s = 0; uint32_t ph = 0;
-            // FT: A box of 125 data rows + 384-byte bulk copy of the split rows into
-            // rows 125..127; B^r box of BN rows (K-major).  FT off: 128-row A box and
-            // the row-major B in NBOX N-major boxes.
-            constexpr uint32_t bytes = FT ? (Cfg::BMD * 128 + Cfg::Y_BYTES + Cfg::B_BYTES) : (Cfg::A_BYTES + Cfg::B_BYTES);
-            for (int t = blockIdx.x; t < a.num_tiles; t += gridDim.x) {
-                int ti, tj;
-                tile_coords(t, a.tiles_m, a.tiles_n, ti, tj);
+            // FT: A box of 125 data rows + the 384-byte pre-swizzled split rows into
+            // rows 125..127 (TMA, no swizzle); B^r.  FT off: 128-row A box and the
+            // row-major B.  B is N-major in BOXN-column boxes; with a CTA pair each
+            // CTA loads half of the tile's columns.  All bytes of a stage (both CTAs)
+            // are counted on the leader's full barrier.
+            constexpr uint32_t bytes_cta = FT ? (Cfg::BMD * 128 + Cfg::Y_BYTES + Cfg::B_BYTES) : (Cfg::A_BYTES + Cfg::B_BYTES);
+            for (int u = cluster_id; u < a.num_units; u += num_clusters) {
+                int tmu, tj;
+                tile_coords(u, a.units_m, a.tiles_n, a.group, tmu, tj);
+                const int ti = tmu * CG + (int)rank;
                 const int row0 = ti * Cfg::BMD;
+                const int colb = tj * BN + (int)rank * (BN / CG);
                 for (int kb = 0; kb < a.num_kb; ++kb) {
                     mbar_wait(&empty[s], ph ^ 1);
-                    mbar_arrive_expect_tx(&full[s], bytes);
+                    if (leader) mbar_arrive_expect_tx(&full[s], CG * bytes_cta);
                     uint8_t* sa = stage_base + s * Cfg::STAGE_BYTES;
                     uint8_t* sb = sa + Cfg::A_BYTES;
-                    tma_load_2d(sa, &tmA, &full[s], kb * Cfg::BK, row0);
-                    if constexpr (FT)
-                        bulk_load(sa + Cfg::BMD * 128, reinterpret_cast<const uint8_t*>(a.Y) +
-                                  ((int64_t)ti * a.num_kb + kb) * Cfg::Y_BYTES, Cfg::Y_BYTES, &full[s]);
-                    // B (FT off) or B^r (FT on): N-major, BN-wide tile slots on 128-byte boundaries
+                    if constexpr (CG == 1) {
+                        tma_load_2d(sa, &tmA, &full[s], kb * Cfg::BK, row0);
+                        if constexpr (FT) tma_load_2d(sa + Cfg::BMD * 128, &tmY, &full[s], 0, ti * a.num_kb + kb);
 #pragma unroll
-                    for (int b = 0; b < Cfg::NBOX; ++b)
-                        tma_load_2d(sb + b * Cfg::B_BOX_BYTES, &tmB, &full[s], tj * BN + b * Cfg::BOXN, kb * Cfg::BK);
+                        for (int b = 0; b < Cfg::NBOX; ++b)
+                            tma_load_2d(sb + b * Cfg::B_BOX_BYTES, &tmB, &full[s], colb + b * Cfg::BOXN, kb * Cfg::BK);
+                    } else {
+                        const uint32_t mb = smem_u32(&full[s]) & kPeerBitMask;
+                        tma_load_2d_pair(sa, &tmA, mb, kb * Cfg::BK, row0);
+                        if constexpr (FT) tma_load_2d_pair(sa + Cfg::BMD * 128, &tmY, mb, 0, ti * a.num_kb + kb);
+#pragma unroll
+                        for (int b = 0; b < Cfg::NBOX / CG; ++b)
+                            tma_load_2d_pair(sb + b * Cfg::B_BOX_BYTES, &tmB, mb, colb + b * Cfg::BOXN, kb * Cfg::BK);
+                    }
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------- MMA issuer -----
-        if (lane == 0) {
-            constexpr uint32_t idesc = instr_desc(kTF32, Cfg::BM, BN, false, true);
+        if (lane == 0 && leader) {
+            constexpr uint32_t idesc = instr_desc(kTF32, Cfg::BM * CG, BN, false, true);
+            constexpr uint16_t pair = (1u << CG) - 1;
+            auto commit = [&](uint64_t* bar) {
+                if constexpr (CG == 2) umma_commit_pair(bar, pair); else umma_commit(bar);
+            };
             int s = 0; uint32_t ph = 0; uint32_t injph = 0;
             int lt = 0;
-            for (int t = blockIdx.x; t < a.num_tiles; t += gridDim.x, ++lt) {
+            for (int t = cluster_id; t < a.num_units; t += num_clusters, ++lt) {
                 const int acc = lt & 1;
                 const uint32_t accph = (lt >> 1) & 1;
                 mbar_wait(&tm_empty[acc], accph ^ 1);
@@ -224,12 +248,12 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         // B is N-major: bf16 -> SW128 (8-row atoms), tf32 -> SW128_BASE32B (4-row atoms)
                         const uint64_t bd = kTF32 ? smem_desc_sw128<1>(sb + kk * Cfg::UK * 128, Cfg::B_BOX_BYTES, 512)
                                                   : smem_desc_sw128<2>(sb + kk * Cfg::UK * 128, Cfg::B_BOX_BYTES, 1024);
-                        umma<kTF32>(d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                        umma<kTF32, CG>(d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
                     }
-                    umma_commit(&empty[s]);
+                    commit(&empty[s]);
                     if (FT && ii < ie && a.inj[ii].kb == kb) {
-                        // hand the accumulator to the epilogue warps for the fault(s)
-                        umma_commit(inj_req);
+                        // hand the accumulator to the epilogue warps (of both CTAs) for the fault(s)
+                        commit(inj_req);
                         mbar_wait(inj_done, injph);
                         injph ^= 1;
                         tc_fence_after();
@@ -237,7 +261,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     }
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
-                umma_commit(&tm_full[acc]);
+                commit(&tm_full[acc]);
             }
         }
         __syncwarp();
@@ -250,10 +274,17 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         uint32_t injph = 0, cph = 0, gcount = 0;   // gcount: store groups issued by this warp
         unsigned long long n_checked = 0;
         int lt = 0;
-        for (int t = blockIdx.x; t < a.num_tiles; t += gridDim.x, ++lt) {
-            int ti, tj;
-            tile_coords(t, a.tiles_m, a.tiles_n, ti, tj);
+        // arrival on a barrier of the MMA leader (remote for the peer CTA)
+        auto arrive_leader = [&](uint64_t* bar) {
+            if (CG == 1 || leader) mbar_arrive(bar);
+            else mbar_arrive_cluster(mapa_shared(smem_u32(bar), 0));
+        };
+        for (int t = cluster_id; t < a.num_units; t += num_clusters, ++lt) {
+            int tmu, tj;
+            tile_coords(t, a.units_m, a.tiles_n, a.group, tmu, tj);
+            const int ti = tmu * CG + (int)rank;
             const int r0 = ti * Cfg::BMD, c0 = tj * Cfg::BND;
+            const bool has_rows = r0 < a.M;                    // the pair's second tile may lie beyond M
             const int bm = min(Cfg::BMD, a.M - r0), bn = min(Cfg::BND, a.N - c0);
             constexpr int doff = 0;                            // data col q <-> MMA col q
             constexpr int xoff = BN - 4;                       // row-reference split columns
@@ -262,7 +293,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             const uint32_t tb = tmem_base + acc * BN;
             // norms for this tile's thresholds, fetched before the accumulator is ready
             float nrow = 0.f, nbr = 0.f, nac = 0.f, ncol[2] = {0.f, 0.f};
-            if constexpr (FT) {
+            if (FT && has_rows) {
                 if (rloc < bm) nrow = __ldg(a.rownorm + r0 + rloc);
                 nbr = __ldg(a.brnorm + tj);
                 nac = __ldg(a.acnorm + ti);
@@ -282,9 +313,11 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     tc_fence_after();
                     for (; ii < ie && a.inj[ii].kb == kb; ++ii) {
                         const DevInject f = a.inj[ii];
+                        if ((f.target >> 8) != (int)rank) continue;   // fault in the other CTA's check tile
+                        const int tgt = f.target & 0xff;
                         int trow, tcol;
-                        if (f.target == FTGEMM_TGT_ROW_REF) { trow = f.p; tcol = xoff; }
-                        else if (f.target == FTGEMM_TGT_COL_REF) { trow = Cfg::BMD; tcol = f.q + doff; }
+                        if (tgt == FTGEMM_TGT_ROW_REF) { trow = f.p; tcol = xoff; }
+                        else if (tgt == FTGEMM_TGT_COL_REF) { trow = Cfg::BMD; tcol = f.q + doff; }
                         else { trow = f.p; tcol = f.q + doff; }
                         if ((trow >> 5) == ew) {
                             const uint32_t addr = tb + lane_off + (uint32_t)tcol;
@@ -295,16 +328,25 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     }
                     tc_fence_before();
                     named_bar_sync(1, 128);
-                    if (et == 0) mbar_arrive(inj_done);
+                    if (et == 0) arrive_leader(inj_done);
                 }
             }
 
             mbar_wait(&tm_full[acc], accph);
             tc_fence_after();
+            if (!has_rows) {                                   // padding half of the last pair row
+                __syncwarp();
+                if (lane == 0) arrive_leader(&tm_empty[acc]);
+                continue;
+            }
 
             int kind = 0, pstar = -1, qstar = -1;
             float corr = 0.0f;
+#ifdef FTGEMM_EXP_NO_VERIFY
+            if (false) {
+#else
             if (FT) {
+#endif
                 // ---- pass 1: row sums, row refs, column partial sums ----
                 // previous tile's stores have read the staging area (aliased below) and
                 // every reader of sflag / residual arrays is done
@@ -519,7 +561,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 if (g == NG - 1) {                         // last TMEM read of this accumulator
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&tm_empty[acc]);
+                    if (lane == 0) arrive_leader(&tm_empty[acc]);
                 }
                 if (do_corr) {
                     const int qq = qs - cs;
@@ -593,33 +635,48 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     }
 
     tc_fence_before();
-    __syncthreads();
+    // a CTA pair stays resident until both are done (remote arrivals, pair MMA into the peer's TMEM)
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+        tmem_dealloc<Cfg::TMEM_COLS, CG>(tmem_base);
     }
 }
 
 // ---------------------------------------------------------------- launch ---
-template <bool kTF32, int BN, bool FT>
+template <bool kTF32, int BN, bool FT, int CG>
 cudaError_t launch_tc_t(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mC, const CUtensorMap& mC29,
-                        const TcArgs& a, cudaStream_t st) {
-    using Cfg = TcCfg<kTF32, BN, FT>;
-    auto kern = tc_ftgemm_kernel<kTF32, BN, FT>;
+                        const CUtensorMap& mY, const TcArgs& a, cudaStream_t st) {
+    using Cfg = TcCfg<kTF32, BN, FT, CG>;
+    auto kern = tc_ftgemm_kernel<kTF32, BN, FT, CG>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    const int grid = a.num_tiles < kNumSMsB200 ? a.num_tiles : kNumSMsB200;
-    kern<<<grid, 256, Cfg::SMEM_BYTES, st>>>(mA, mB, mC, mC29, a);
-    return cudaGetLastError();
+    // persistent: one CTA (pair) per SM (pair of SMs)
+    const int clusters = a.num_units < kNumSMsB200 / CG ? a.num_units : kNumSMsB200 / CG;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(clusters * CG, 1, 1);
+    cfg.blockDim = dim3(256, 1, 1);
+    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, mA, mB, mC, mC29, mY, a);
 }
 
-cudaError_t launch_tc(bool tf32, int bn, bool ft, const CUtensorMap& mA, const CUtensorMap& mB,
-                      const CUtensorMap& mC, const CUtensorMap& mC29, const TcArgs& a, cudaStream_t st) {
-#define L_(T, B, F) launch_tc_t<T, B, F>(mA, mB, mC, mC29, a, st)
+cudaError_t launch_tc(bool tf32, int bn, bool ft, int cg, const CUtensorMap& mA, const CUtensorMap& mB,
+                      const CUtensorMap& mC, const CUtensorMap& mC29, const CUtensorMap& mY, const TcArgs& a,
+                      cudaStream_t st) {
+#define L_(T, B, F) (cg == 2 ? launch_tc_t<T, B, F, 2>(mA, mB, mC, mC29, mY, a, st) \
+                             : launch_tc_t<T, B, F, 1>(mA, mB, mC, mC29, mY, a, st))
     if (tf32) {
         if (bn == 256) return ft ? L_(true, 256, true) : L_(true, 256, false);
         return ft ? L_(true, 128, true) : L_(true, 128, false);

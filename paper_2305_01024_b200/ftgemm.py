@@ -17,7 +17,7 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libftgemm.so")
+LIB_PATH = os.environ.get("FTGEMM_LIB") or os.path.join(_HERE, "libftgemm.so")   # FTGEMM_LIB: development variants
 
 F32_SIMT, TF32, BF16 = 0, 1, 2
 DTYPES = {"f32_simt": F32_SIMT, "tf32": TF32, "bf16": BF16}
