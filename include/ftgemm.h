@@ -118,7 +118,10 @@ typedef struct ftgemm_plan {
     int32_t check_tile_m;        /* data rows per check tile (FT on)    */
     int32_t check_tile_n;        /* data columns per check tile (FT on) */
     int32_t off_tile_m, off_tile_n; /* data tile with FT_OFF */
-    int32_t stages, cta_group;
+    int32_t stages;              /* smem pipeline depth */
+    int32_t cta_group;           /* 1, or 2: a CTA pair issues one M = 256 tcgen05.mma (cta_group::2);
+                                    each CTA still owns one 128-row (125 + 3) check tile.  The
+                                    environment variable FTGEMM_CG=1|2 overrides (tuning/tests) */
     int32_t max_events, max_inject;
     int32_t pad0;
     int64_t tiles_m, tiles_n;    /* check-tile grid with FT on */

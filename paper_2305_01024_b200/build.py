@@ -35,7 +35,8 @@ def build(verbose: bool = False, force: bool = False, defines=(), out: str | Non
     global OBJ, LIB
     if defines or out:
         OBJ = os.path.join(HERE, "build_" + "_".join(d.lstrip("-D").lower() for d in defines))
-        LIB = out or os.path.join(HERE, "libftgemm_exp.so")
+        LIB = out or os.path.join(HERE, "libftgemm_" + "_".join(d[2:].lower().replace("ftgemm_exp_", "")
+                                                                 for d in defines) + ".so")
         force = True
     os.makedirs(OBJ, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))

@@ -77,8 +77,12 @@ void fill_plan(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* p) {
         p->bm = 128; p->bn = bn; p->bk = bk;
         p->check_tile_m = 125; p->check_tile_n = bn - 4;
         p->off_tile_m = 128; p->off_tile_n = bn;
-        // CTA pairs (cta_group::2, M = 256 per MMA) halve the B tile each SM loads
-        int cg = bn == 256 ? 1 : 1;
+        // CTA pairs (cta_group::2, M = 256 per MMA) halve the B tile each SM
+        // loads; measured on B200 (profiles/cg_sweep_r1.txt) they pay off for
+        // the large-tile class with enough K to amortise the pair handshake
+        // (BF16 K >= 2048, TF32 K >= 1024) and lose on K = 128 and M = 128
+        const int64_t tiles_m125 = (M + 124) / 125;
+        int cg = (bn == 256 && tiles_m125 >= 4 && (K >= 2048 || (dtype == FTGEMM_TF32 && K >= 1024))) ? 2 : 1;
         if (const char* e = getenv("FTGEMM_CG")) cg = atoi(e) == 2 ? 2 : 1;
         p->cta_group = cg;
         const int elt = dtype == FTGEMM_TF32 ? 4 : 2;

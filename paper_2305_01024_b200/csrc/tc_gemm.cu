@@ -358,38 +358,71 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 const bool all_rows = ew < 3 && bm >= (ew + 1) * 32;   // warp-uniform: no row of this warp masked
                 float* tbuf = reinterpret_cast<float*>(stg + 12288) + ew * (32 * 36);   // 32 x 36 transpose buffer
                 float srow = 0.0f, rref = 0.0f;
+#if defined(FTGEMM_EXP_PASS1_LDONLY)
+                if (true) {
+                    float acc8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                for (int c = 0; c < Cfg::NCHUNK; ++c) {
-                    float v[32];
-                    tmem_ld32(tb + lane_off + c * 32, v);
+                    for (int c = 0; c < Cfg::NCHUNK; ++c) {
+                        float v[32];
+                        tmem_ld32(tb + lane_off + c * 32, v);
 #pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        if (c * 32 + i < Cfg::BND) srow += v[i];
-                    if (c == Cfg::NCHUNK - 1) rref = (v[28] + v[29]) + v[30];
-                    if (ew == 3 && isref) {
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) refrow[(rloc - Cfg::BMD) * BN + c * 32 + i] = v[i];
+                        for (int i = 0; i < 32; ++i) acc8[i & 7] += v[i];
+                        colsum[ew * BN + c * 32 + lane] = 0.f;
+                        if (ew == 0 && lane < 3) refrow[lane * BN + c * 32] = 0.f;
                     }
-                    // column partial sums over this warp's 32 rows: transpose through
-                    // shared memory (row-major writes, 16-byte column reads)
-                    if (all_rows) {
+                    if (ew == 0) for (int i = lane; i < 3 * BN; i += 32) refrow[i] = 0.f;
+                    srow = ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
+                    rref = srow;
+                } else
+#endif
+                {
+                    // 64 columns per TMEM load; row sums in 4 independent chains
+                    float rs[4] = {0.f, 0.f, 0.f, 0.f};
+                    const bool w3 = ew == 3;
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) tbuf[i * 36 + lane] = v[i];
-                    } else {
+                    for (int c2 = 0; c2 < Cfg::NCHUNK; c2 += 2) {
+                        float v[64];
+                        tmem_ld64(tb + lane_off + c2 * 32, v);
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) tbuf[i * 36 + lane] = rvalid ? v[i] : 0.0f;
-                    }
-                    __syncwarp();
-                    {
-                        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+                        for (int i = 0; i < 64; ++i)
+                            if (c2 * 32 + i < Cfg::BND) rs[i & 3] += v[i];
+                        if (c2 + 2 == Cfg::NCHUNK) rref = (v[60] + v[61]) + v[62];
 #pragma unroll
-                        for (int r4 = 0; r4 < 8; ++r4) {
-                            const float4 x = *reinterpret_cast<const float4*>(tbuf + lane * 36 + 4 * r4);
-                            s0 += x.x; s1 += x.y; s2 += x.z; s3 += x.w;
+                        for (int h = 0; h < 2; ++h) {
+                            const int c = c2 + h;
+                            // column partial sums over this warp's 32 rows: transpose
+                            // through shared memory (row-major writes, 16-byte column
+                            // reads).  Warp 3's lanes 29..31 are the split rows of
+                            // e^T A B: they pass through the transpose unmasked and
+                            // come out as the column references.
+                            if (all_rows) {
+#pragma unroll
+                                for (int i = 0; i < 32; ++i) tbuf[i * 36 + lane] = v[32 * h + i];
+                            } else {
+#pragma unroll
+                                for (int i = 0; i < 32; ++i) tbuf[i * 36 + lane] = (rvalid || isref) ? v[32 * h + i] : 0.0f;
+                            }
+                            __syncwarp();
+                            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+                            for (int r4 = 0; r4 < 7; ++r4) {
+                                const float4 x = *reinterpret_cast<const float4*>(tbuf + lane * 36 + 4 * r4);
+                                s0 += x.x; s1 += x.y; s2 += x.z; s3 += x.w;
+                            }
+                            const float4 x = *reinterpret_cast<const float4*>(tbuf + lane * 36 + 28);
+                            s0 += x.x;
+                            if (w3) {
+                                refrow[0 * BN + c * 32 + lane] = x.y;
+                                refrow[1 * BN + c * 32 + lane] = x.z;
+                                refrow[2 * BN + c * 32 + lane] = x.w;
+                            } else {
+                                s1 += x.y; s2 += x.z; s3 += x.w;
+                            }
+                            colsum[ew * BN + c * 32 + lane] = (s0 + s1) + (s2 + s3);
+                            __syncwarp();
                         }
-                        colsum[ew * BN + c * 32 + lane] = (s0 + s1) + (s2 + s3);
                     }
-                    __syncwarp();
+                    srow = (rs[0] + rs[1]) + (rs[2] + rs[3]);
                 }
                 named_bar_sync(1, 128);
                 // ---- row residuals ----

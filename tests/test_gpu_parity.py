@@ -215,6 +215,42 @@ def test_false_positive_sweep(dtype):
         assert c.counts["tiles_checked"] == c.plan.tiles_m * c.plan.tiles_n
 
 
+# ----------------------------------------------------- CTA pairs (2-SM MMA) --
+
+@pytest.mark.parametrize("cg", [1, 2])
+@pytest.mark.parametrize("dtype", ["tf32", "bf16"])
+@pytest.mark.parametrize("shape", [(845, 600, 320), (845, 10896, 256)], ids=["bn128", "bn256"])
+def test_cta_pair_modes(dtype, cg, shape, monkeypatch):
+    """Both tensor-core launch modes (one CTA per MMA, or a cta_group::2 pair with
+    M = 256) give the oracle's C, events and counts.  7 check-tile rows: the last
+    pair's second tile lies beyond M.  Faults in both CTAs of a pair (even and
+    odd tile rows), in the carried references, and an SEU violation."""
+    monkeypatch.setenv("FTGEMM_CG", str(cg))
+    F = ftmod()
+    M, N, K = shape
+    A, B, _ = synth.problem(M, N, K, dtype=odt(dtype))
+    plan = F.plan(dtype, M, N, K)
+    assert plan.cta_group == cg and plan.tiles_m == 7
+    tm, tn = plan.check_tile_m, plan.check_tile_n
+    inj = detectable_sites(dtype, 8, M, N, K, plan, A, B, seed=21)
+    used = {(r // tm, c // tn) for r, c, *_ in inj}
+    extra = [(3 * tm + 5, 2, 64, 0, oracle.INJ_ADD, oracle.TGT_ROW_REF, 600.0),          # odd tile row
+             (5 * tm + 9, tn + 7, 100, 0, oracle.INJ_ADD, oracle.TGT_COL_REF, -600.0),    # odd tile row
+             (6 * tm + 1, 4, 10, 0, oracle.INJ_ADD, 0, 900.0),                            # last (unpaired) row
+             (6 * tm + 2, 8, 200, 0, oracle.INJ_ADD, 0, -900.0)]                          # ... twice: SEU violation
+    inj += [f for f in extra if (f[0] // tm, f[1] // tn) not in used]
+    c = Case(dtype, M, N, K, injections=inj, alpha=1.25, beta=0.5)
+    assert c.counts_match() and c.events_match(), (c.counts, c.ref.counts)
+    assert c.counts["tiles_checked"] == plan.tiles_m * plan.tiles_n
+    bad = np.zeros((M, N), bool)
+    for e in c.ref.events:
+        if e["kind"] == oracle.EV_UNCORRECTABLE:
+            bad[e["tile_m"] * tm:(e["tile_m"] + 1) * tm, e["tile_n"] * tn:(e["tile_n"] + 1) * tn] = True
+    assert c.fro(~bad) < TOL[dtype]
+    off = Case(dtype, M, N, K, ft=F.FT_OFF, alpha=1.25, beta=0.5)
+    assert off.fro() < TOL[dtype]
+
+
 # ------------------------------------------------- full size, sampled oracle --
 
 def test_cfg3_full_size_sampled():
