@@ -64,6 +64,9 @@ extern "C" {
 #define FTGEMM_FT_OFF     0  /* same tile shape family, checksums compiled out (the overhead baseline) */
 #define FTGEMM_FT_DETECT  1  /* verify + locate, report, leave C as computed (detect-only flavour) */
 #define FTGEMM_FT_CORRECT 2  /* verify + locate + correct (the paper's online ABFT) */
+#define FTGEMM_FT_DETECT_ROWS 3 /* offline (detect-only) ABFT: row checks only, no
+                                   column sums, no correction; a flagged tile is reported (EV_DETECTED)
+                                   and the caller re-computes (ftgemm_run_offline) */
 
 /* ---- fault injection (section 5.3) ---------------------------- */
 #define FTGEMM_INJ_FLIP 0    /* acc bits ^= (1 << bit)            (register bit flip) */
@@ -83,11 +86,52 @@ typedef struct ftgemm_inject {
     float   addend;     /* for FTGEMM_INJ_ADD */
 } ftgemm_inject_t;      /* 40 bytes */
 
+/* ---- offline (detect-only) ABFT with re-computation -------------------------
+ * PAPER.md:571-583 (section 5.5, "Online ABFT vs. Offline ABFT"): executions of
+ * ftgemm_run at FT_DETECT_ROWS (row checks only, nothing corrected); after
+ * each execution the host reads the detection counter (the call synchronises
+ * `stream`) and, if a tile was flagged, re-computes the whole product, up to
+ * max_runs executions in total.  Fault i strikes execution inj_run[i]
+ * (0-based; inj_run may be NULL: every fault strikes execution 0), so faults
+ * during re-computation can be modelled.  When beta != 0 the product reads C,
+ * which an execution overwrites: c_backup (device, M x N with leading
+ * dimension ldc, caller-owned -- the extra memory an offline scheme needs,
+ * PAPER.md:173) receives C_in before execution 0 and restores it before each
+ * re-execution; it may be NULL when beta == 0.
+ * out[0] = executions performed, out[1] = 1 if the last execution passed the
+ * row checks (0: max_runs exhausted, C not trusted; the report has the events).
+ * Errors: as ftgemm_run, INVALID_VALUE (max_runs < 1, inj_run out of range,
+ * beta != 0 without c_backup).                                                */
+FTGEMM_API int ftgemm_run_offline(int dtype, int64_t M, int64_t N, int64_t K, float alpha,
+               const void* A, int64_t lda, const void* B, int64_t ldb,
+               float beta, void* C, int64_t ldc, void* c_backup,
+               const void* enc_ws, const ftgemm_inject_t* inj, const int32_t* inj_run,
+               int32_t n_inj, int32_t max_runs, void* report_ws, int32_t* out, void* stream);
+
+/* ---- online vs offline cost model --------------------------
+ * Pure host function.  tiles = M/m_tb x N/n_tb threadblock (check) tiles,
+ * gamma0 = per-tile error probability of one execution.
+ *   gamma = 1 - (1 - gamma0)^tiles                     (whole-call error rate)
+ *   online_expected_runs  = 1                          (errors corrected on the fly)
+ *   offline_expected_runs = (1 - gamma) / (1 - 2 gamma) (the paper's restart series;
+ *                           +INFINITY when gamma >= 1/2: the series diverges)
+ * Errors: INVALID_VALUE (gamma0 outside [0, 1), tiles < 1, null out).          */
+typedef struct ftgemm_cost {
+    double gamma0;
+    int64_t tiles;
+    double gamma;
+    double online_expected_runs;
+    double offline_expected_runs;
+} ftgemm_cost_t;
+FTGEMM_API int ftgemm_cost_model(double gamma0, int64_t tiles, ftgemm_cost_t* out);
+
 /* ---- report ------------------------------------------------------------------ */
 #define FTGEMM_EV_CORRECTED      1  /* one row + one column flagged, consistent: element corrected */
 #define FTGEMM_EV_CHECKSUM_ONLY  2  /* one row only or one column only: the fault hit a reference; C untouched */
 #define FTGEMM_EV_UNCORRECTABLE  3  /* >= 2 rows or >= 2 columns, or inconsistent magnitudes; C untouched */
 #define FTGEMM_EV_LOCATED        4  /* FT_DETECT: single error located, not corrected */
+#define FTGEMM_EV_DETECTED       5  /* FT_DETECT_ROWS: >= 1 row flagged (row = first flagged row, col = -1);
+                                       counted in tiles_detected only */
 
 typedef struct ftgemm_event {
     int64_t row, col;            /* global position (p*, q*); -1 when that side had no flag */

@@ -27,10 +27,10 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 
 ACC_FP64, ACC_FP32SEQ = 0, 1
 OUT_F32, OUT_BF16 = 0, 1
-FT_OFF, FT_DETECT, FT_CORRECT = 0, 1, 2
+FT_OFF, FT_DETECT, FT_CORRECT, FT_DETECT_ROWS = 0, 1, 2, 3
 INJ_FLIP, INJ_ADD = 0, 1
 TGT_ACC, TGT_ROW_REF, TGT_COL_REF = 0, 1, 2
-EV_CORRECTED, EV_CHECKSUM_ONLY, EV_UNCORRECTABLE, EV_LOCATED = 1, 2, 3, 4
+EV_CORRECTED, EV_CHECKSUM_ONLY, EV_UNCORRECTABLE, EV_LOCATED, EV_DETECTED = 1, 2, 3, 4, 5
 
 
 class Inject(C.Structure):

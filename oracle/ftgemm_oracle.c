@@ -48,10 +48,10 @@
 
 enum { OR_ACC_FP64 = 0, OR_ACC_FP32SEQ = 1 };
 enum { OR_OUT_F32 = 0, OR_OUT_BF16 = 1 };
-enum { OR_FT_OFF = 0, OR_FT_DETECT = 1, OR_FT_CORRECT = 2 };
+enum { OR_FT_OFF = 0, OR_FT_DETECT = 1, OR_FT_CORRECT = 2, OR_FT_DETECT_ROWS = 3 };
 enum { OR_INJ_FLIP = 0, OR_INJ_ADD = 1 };
 enum { OR_TGT_ACC = 0, OR_TGT_ROW_REF = 1, OR_TGT_COL_REF = 2 };
-enum { OR_EV_CORRECTED = 1, OR_EV_CHECKSUM_ONLY = 2, OR_EV_UNCORRECTABLE = 3, OR_EV_LOCATED = 4 };
+enum { OR_EV_CORRECTED = 1, OR_EV_CHECKSUM_ONLY = 2, OR_EV_UNCORRECTABLE = 3, OR_EV_LOCATED = 4, OR_EV_DETECTED = 5 };
 
 typedef struct {
     int64_t row, col, k_elem;
@@ -370,8 +370,20 @@ static int run_tile(const oracle_problem_t *pr, int64_t ti, int64_t tj) {
         if (!(fabs(c) <= tc[q])) { if (nc == 0) { qstar = q; cstar = c; } ++nc; }
     }
 
+    /* Step 6 (offline, detect-only ABFT, R15): only
+     * the row checks count; any flagged row marks the tile for re-computation,
+     * C is left as computed. */
+    if (pr->ft_level == OR_FT_DETECT_ROWS) {
+#pragma omp atomic
+        pr->counts->tiles_checked++;
+        if (nr > 0) {
+#pragma omp atomic
+            pr->counts->tiles_detected++;
+            emit_event(pr, ti, tj, OR_EV_DETECTED, r0 + pstar, -1, nr, 0, rstar, 0.0, tr[pstar], 0.0);
+        }
+    }
     /* Step 6: decide (R3-R5) and correct. */
-    if (pr->ft_level != OR_FT_OFF) {
+    else if (pr->ft_level != OR_FT_OFF) {
 #pragma omp atomic
         pr->counts->tiles_checked++;
         if (nr > 0 || nc > 0) {

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cmath>
+#include <limits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -229,7 +230,7 @@ int ftgemm_run(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const vo
     if (e) return e;
     if (!A || !B || !C) return fail(FTGEMM_ERR_INVALID_VALUE, "null A, B or C");
     if (lda < K || ldb < N || ldc < N) return fail(FTGEMM_ERR_INVALID_VALUE, "leading dimension too small");
-    if (ft_level < FTGEMM_FT_OFF || ft_level > FTGEMM_FT_CORRECT) return fail(FTGEMM_ERR_INVALID_VALUE, "bad ft_level");
+    if (ft_level < FTGEMM_FT_OFF || ft_level > FTGEMM_FT_DETECT_ROWS) return fail(FTGEMM_ERR_INVALID_VALUE, "bad ft_level");
     if (n_inj < 0 || n_inj > kMaxInject || (n_inj > 0 && !inj)) return fail(FTGEMM_ERR_INVALID_VALUE, "bad injection list");
     if (ft_level == FTGEMM_FT_OFF && n_inj > 0) return fail(FTGEMM_ERR_INVALID_VALUE, "fault injection needs ft_level DETECT or CORRECT");
     if (ft_level != FTGEMM_FT_OFF && (!enc_ws || !report_ws)) return fail(FTGEMM_ERR_INVALID_VALUE, "FT needs enc_ws and report_ws");
@@ -350,6 +351,69 @@ int ftgemm_run(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const vo
         ce = launch_tc(tf32, p.bn, ft, p.cta_group, mA, mB, mC, mC29, mY, a, st);
     }
     if (ce != cudaSuccess) return fail_cuda(ce, "kernel launch");
+    g_err.clear();
+    return FTGEMM_OK;
+}
+
+int ftgemm_run_offline(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const void* A, int64_t lda,
+                       const void* B, int64_t ldb, float beta, void* C, int64_t ldc, void* c_backup,
+                       const void* enc_ws, const ftgemm_inject_t* inj, const int32_t* inj_run, int32_t n_inj,
+                       int32_t max_runs, void* report_ws, int32_t* out, void* stream) {
+    if (!out) return fail(FTGEMM_ERR_INVALID_VALUE, "null out");
+    if (max_runs < 1) return fail(FTGEMM_ERR_INVALID_VALUE, "max_runs must be >= 1");
+    if (n_inj < 0 || (n_inj > 0 && !inj)) return fail(FTGEMM_ERR_INVALID_VALUE, "bad injection list");
+    if (beta != 0.0f && !c_backup) return fail(FTGEMM_ERR_INVALID_VALUE, "beta != 0 needs c_backup");
+    if (!report_ws) return fail(FTGEMM_ERR_INVALID_VALUE, "null report_ws");
+    if (inj_run)
+        for (int i = 0; i < n_inj; ++i)
+            if (inj_run[i] < 0 || inj_run[i] >= max_runs) return fail(FTGEMM_ERR_INVALID_VALUE, "inj_run[%d] out of range", i);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int elt = dtype == FTGEMM_BF16 ? 2 : 4;
+    const size_t pitch = (size_t)ldc * elt, width = (size_t)N * elt;
+    cudaError_t ce;
+    if (beta != 0.0f && (ce = cudaMemcpy2DAsync(c_backup, pitch, C, pitch, width, (size_t)M, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+        return fail_cuda(ce, "C_in backup");
+    const unsigned long long* dcnt = reinterpret_cast<const ReportDev*>(report_ws)->counts;
+    unsigned long long det0 = 0, det = 0;
+    if ((ce = cudaMemcpyAsync(&det0, dcnt + CNT_DETECTED, sizeof(det0), cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (ce = cudaStreamSynchronize(st)) != cudaSuccess)
+        return fail_cuda(ce, "report read");
+    std::vector<ftgemm_inject_t> mine;
+    int runs = 0, clean = 0;
+    for (int r = 0; r < max_runs && !clean; ++r) {
+        if (r > 0 && beta != 0.0f &&
+            (ce = cudaMemcpy2DAsync(C, pitch, c_backup, pitch, width, (size_t)M, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+            return fail_cuda(ce, "C_in restore");
+        mine.clear();
+        for (int i = 0; i < n_inj; ++i)
+            if ((inj_run ? inj_run[i] : 0) == r) mine.push_back(inj[i]);
+        int e = ftgemm_run(dtype, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, enc_ws, FTGEMM_FT_DETECT_ROWS,
+                           mine.empty() ? nullptr : mine.data(), (int32_t)mine.size(), report_ws, stream);
+        if (e) return e;
+        ++runs;
+        // the restart decision needs this execution's verdict
+        if ((ce = cudaMemcpyAsync(&det, dcnt + CNT_DETECTED, sizeof(det), cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+            (ce = cudaStreamSynchronize(st)) != cudaSuccess)
+            return fail_cuda(ce, "report read");
+        clean = det == det0;
+        det0 = det;
+    }
+    out[0] = runs;
+    out[1] = clean;
+    g_err.clear();
+    return FTGEMM_OK;
+}
+
+int ftgemm_cost_model(double gamma0, int64_t tiles, ftgemm_cost_t* out) {
+    if (!out) return fail(FTGEMM_ERR_INVALID_VALUE, "null out");
+    if (!(gamma0 >= 0.0 && gamma0 < 1.0) || tiles < 1) return fail(FTGEMM_ERR_INVALID_VALUE, "need 0 <= gamma0 < 1, tiles >= 1");
+    out->gamma0 = gamma0;
+    out->tiles = tiles;
+    // gamma = 1 - (1 - gamma0)^tiles, via log1p/expm1 for small gamma0
+    out->gamma = -std::expm1((double)tiles * std::log1p(-gamma0));
+    out->online_expected_runs = 1.0;
+    out->offline_expected_runs = out->gamma < 0.5 ? (1.0 - out->gamma) / (1.0 - 2.0 * out->gamma)
+                                                  : std::numeric_limits<double>::infinity();
     g_err.clear();
     return FTGEMM_OK;
 }

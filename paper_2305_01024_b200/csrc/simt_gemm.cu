@@ -246,7 +246,10 @@ __global__ void __launch_bounds__(256, 2) simt_ftgemm_kernel(const SimtArgs a) {
         const int nr = sflag[0], nc = sflag[1];
         pstar = nr ? sflag[2] : -1;
         qstar = nc ? sflag[3] : -1;
-        if (nr == 1 && nc == 1) {
+        if (a.ft_level == FTGEMM_FT_DETECT_ROWS) {          // offline ABFT: rows only
+            kind = nr ? FTGEMM_EV_DETECTED : 0;
+            qstar = -1;
+        } else if (nr == 1 && nc == 1) {
             const float rr = rres[pstar], cc = cres[qstar];
             const float big = fmaxf(fabsf(rr), fabsf(cc));
             const float guard = rtau[pstar] + ctau[qstar] + 2.0f * a.tau_u * (float)(bm + bn) * big;
@@ -294,15 +297,16 @@ __global__ void __launch_bounds__(256, 2) simt_ftgemm_kernel(const SimtArgs a) {
                 atomicAdd(&cnt[CNT_DETECTED], 1ull);
                 const int ci = kind == FTGEMM_EV_CORRECTED ? CNT_CORRECTED
                              : kind == FTGEMM_EV_CHECKSUM_ONLY ? CNT_CHECKSUM_ONLY
-                             : kind == FTGEMM_EV_LOCATED ? CNT_LOCATED : CNT_UNCORRECTABLE;
-                atomicAdd(&cnt[ci], 1ull);
+                             : kind == FTGEMM_EV_LOCATED ? CNT_LOCATED
+                             : kind == FTGEMM_EV_DETECTED ? -1 : CNT_UNCORRECTABLE;
+                if (ci >= 0) atomicAdd(&cnt[ci], 1ull);
                 const unsigned long long slot = atomicAdd(&cnt[CNT_EVENTS], 1ull);
                 if (slot < (unsigned long long)kMaxEvents) {
                     ftgemm_event_t& e = a.rep->events[slot];
                     e.row = pstar >= 0 ? (int64_t)(r0 + pstar) : -1;
                     e.col = qstar >= 0 ? (int64_t)(c0 + qstar) : -1;
                     e.tile_m = ti; e.tile_n = tj; e.kind = kind;
-                    e.n_rows = nr; e.n_cols = nc; e.reserved = 0;
+                    e.n_rows = nr; e.n_cols = kind == FTGEMM_EV_DETECTED ? 0 : nc; e.reserved = 0;
                     e.resid_row = pstar >= 0 ? rres[pstar] : 0.0f;
                     e.resid_col = qstar >= 0 ? cres[qstar] : 0.0f;
                     e.tau_row = pstar >= 0 ? rtau[pstar] : 0.0f;

@@ -379,6 +379,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     // 64 columns per TMEM load; row sums in 4 independent chains
                     float rs[4] = {0.f, 0.f, 0.f, 0.f};
                     const bool w3 = ew == 3;
+                    const bool rows_only = a.ft_level == FTGEMM_FT_DETECT_ROWS;   // offline ABFT: no column sums
 #pragma unroll
                     for (int c2 = 0; c2 < Cfg::NCHUNK; c2 += 2) {
                         float v[64];
@@ -388,7 +389,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                             if (c2 * 32 + i < Cfg::BND) rs[i & 3] += v[i];
                         if (c2 + 2 == Cfg::NCHUNK) rref = (v[60] + v[61]) + v[62];
 #pragma unroll
-                        for (int h = 0; h < 2; ++h) {
+                        for (int h = 0; h < 2 && !rows_only; ++h) {
                             const int c = c2 + h;
                             // column partial sums over this warp's 32 rows: transpose
                             // through shared memory (row-major writes, 16-byte column
@@ -434,7 +435,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 }
                 // ---- column residuals ----
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < 2 && a.ft_level != FTGEMM_FT_DETECT_ROWS; ++h) {
                     const int col = et + 128 * h;
                     if (col < bn && col < BN) {
                         const float sc = (colsum[col] + colsum[BN + col]) + (colsum[2 * BN + col] + colsum[3 * BN + col]);
@@ -450,7 +451,10 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 const int nr = sflag[0], nc = sflag[1];
                 pstar = nr ? sflag[2] : -1;
                 qstar = nc ? sflag[3] : -1;
-                if (nr == 1 && nc == 1) {
+                if (a.ft_level == FTGEMM_FT_DETECT_ROWS) {       // offline ABFT: rows only
+                    kind = nr ? FTGEMM_EV_DETECTED : 0;
+                    qstar = -1;
+                } else if (nr == 1 && nc == 1) {
                     const float rr = rres[pstar], cc = cres[qstar];
                     const float big = fmaxf(fabsf(rr), fabsf(cc));
                     const float guard = rtau[pstar] + ctau[qstar] + 2.0f * a.tau_u * (float)(bm + bn) * big;
@@ -488,15 +492,16 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         atomicAdd(&cnt[CNT_DETECTED], 1ull);
                         const int ci = kind == FTGEMM_EV_CORRECTED ? CNT_CORRECTED
                                      : kind == FTGEMM_EV_CHECKSUM_ONLY ? CNT_CHECKSUM_ONLY
-                                     : kind == FTGEMM_EV_LOCATED ? CNT_LOCATED : CNT_UNCORRECTABLE;
-                        atomicAdd(&cnt[ci], 1ull);
+                                     : kind == FTGEMM_EV_LOCATED ? CNT_LOCATED
+                                     : kind == FTGEMM_EV_DETECTED ? -1 : CNT_UNCORRECTABLE;
+                        if (ci >= 0) atomicAdd(&cnt[ci], 1ull);
                         const unsigned long long slot = atomicAdd(&cnt[CNT_EVENTS], 1ull);
                         if (slot < (unsigned long long)kMaxEvents) {
                             ftgemm_event_t& e = a.rep->events[slot];
                             e.row = pstar >= 0 ? (int64_t)(r0 + pstar) : -1;
                             e.col = qstar >= 0 ? (int64_t)(c0 + qstar) : -1;
                             e.tile_m = ti; e.tile_n = tj; e.kind = kind;
-                            e.n_rows = nr; e.n_cols = nc; e.reserved = 0;
+                            e.n_rows = nr; e.n_cols = kind == FTGEMM_EV_DETECTED ? 0 : nc; e.reserved = 0;
                             e.resid_row = pstar >= 0 ? rres[pstar] : 0.0f;
                             e.resid_col = qstar >= 0 ? cres[qstar] : 0.0f;
                             e.tau_row = pstar >= 0 ? rtau[pstar] : 0.0f;

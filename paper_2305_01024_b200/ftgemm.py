@@ -21,10 +21,10 @@ LIB_PATH = os.environ.get("FTGEMM_LIB") or os.path.join(_HERE, "libftgemm.so")  
 
 F32_SIMT, TF32, BF16 = 0, 1, 2
 DTYPES = {"f32_simt": F32_SIMT, "tf32": TF32, "bf16": BF16}
-FT_OFF, FT_DETECT, FT_CORRECT = 0, 1, 2
+FT_OFF, FT_DETECT, FT_CORRECT, FT_DETECT_ROWS = 0, 1, 2, 3
 INJ_FLIP, INJ_ADD = 0, 1
 TGT_ACC, TGT_ROW_REF, TGT_COL_REF = 0, 1, 2
-EV_CORRECTED, EV_CHECKSUM_ONLY, EV_UNCORRECTABLE, EV_LOCATED = 1, 2, 3, 4
+EV_CORRECTED, EV_CHECKSUM_ONLY, EV_UNCORRECTABLE, EV_LOCATED, EV_DETECTED = 1, 2, 3, 4, 5
 ERR = {0: "OK", 1: "INVALID_VALUE", 2: "UNSUPPORTED", 3: "CUDA"}
 
 
@@ -54,8 +54,13 @@ class PlanStruct(C.Structure):
                 ("u_acc", C.c_float), ("lambda1", C.c_float), ("lambda2", C.c_float), ("pad1", C.c_int32)]
 
 
-SYMBOLS = ("ftgemm_plan", "ftgemm_encode", "ftgemm_run", "ftgemm_report", "ftgemm_report_reset",
-           "ftgemm_last_error", "ftgemm_version", "ftgemm_device_arch")
+class Cost(C.Structure):
+    _fields_ = [("gamma0", C.c_double), ("tiles", C.c_int64), ("gamma", C.c_double),
+                ("online_expected_runs", C.c_double), ("offline_expected_runs", C.c_double)]
+
+
+SYMBOLS = ("ftgemm_plan", "ftgemm_encode", "ftgemm_run", "ftgemm_run_offline", "ftgemm_cost_model",
+           "ftgemm_report", "ftgemm_report_reset", "ftgemm_last_error", "ftgemm_version", "ftgemm_device_arch")
 
 _lib = None
 
@@ -73,6 +78,9 @@ def lib():
         L.ftgemm_encode.argtypes = [C.c_int, i64, i64, i64, vp, i64, vp, i64, vp, C.c_int, vp]
         L.ftgemm_run.argtypes = [C.c_int, i64, i64, i64, C.c_float, vp, i64, vp, i64, C.c_float, vp, i64,
                                  vp, C.c_int, vp, i32, vp, vp]
+        L.ftgemm_run_offline.argtypes = [C.c_int, i64, i64, i64, C.c_float, vp, i64, vp, i64, C.c_float, vp, i64,
+                                         vp, vp, vp, vp, i32, i32, vp, vp, vp]
+        L.ftgemm_cost_model.argtypes = [C.c_double, i64, C.POINTER(Cost)]
         L.ftgemm_report.argtypes = [vp, C.POINTER(Counts), vp, i32, vp]
         L.ftgemm_report_reset.argtypes = [vp, i64, vp]
         L.ftgemm_last_error.restype = C.c_char_p
@@ -179,6 +187,37 @@ def run(dtype, A: torch.Tensor, B: torch.Tensor, C_: torch.Tensor, *, alpha: flo
            "ftgemm_run")
 
 
+def run_offline(dtype, A: torch.Tensor, B: torch.Tensor, C_: torch.Tensor, *, alpha: float = 1.0,
+                beta: float = 0.0, enc_ws: torch.Tensor, report_ws: torch.Tensor, injections=(), inj_run=None,
+                max_runs: int = 4, c_backup: torch.Tensor | None = None, stream=None):
+    """Offline (detect-only) ABFT with re-computation (PAPER.md:571-583).
+    Returns (executions, clean).  inj_run[i]: the execution fault i strikes."""
+    M, K = A.shape
+    N = B.shape[1]
+    arr, n = _inj_array(injections)
+    runs = None
+    if inj_run is not None:
+        runs = (C.c_int32 * max(1, n))(*inj_run)
+    if beta != 0.0 and c_backup is None:
+        c_backup = torch.empty_like(C_)
+    out = (C.c_int32 * 2)()
+    _check(lib().ftgemm_run_offline(_dt(dtype), M, N, K, alpha, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0),
+                                    beta, C_.data_ptr(), C_.stride(0),
+                                    c_backup.data_ptr() if c_backup is not None else None, enc_ws.data_ptr(),
+                                    C.cast(arr, C.c_void_p) if arr is not None else None,
+                                    C.cast(runs, C.c_void_p) if runs is not None else None, n, max_runs,
+                                    report_ws.data_ptr(), C.cast(out, C.c_void_p), _stream(stream)),
+           "ftgemm_run_offline")
+    return int(out[0]), bool(out[1])
+
+
+def cost_model(gamma0: float, tiles: int) -> dict:
+    """Online vs offline expected executions (host-only)."""
+    c = Cost()
+    _check(lib().ftgemm_cost_model(gamma0, tiles, C.byref(c)), "ftgemm_cost_model")
+    return {f: getattr(c, f) for f, _ in Cost._fields_}
+
+
 def report(report_ws: torch.Tensor, max_events: int = 4096, stream=None):
     cnt = Counts()
     evs = (Event * max(1, max_events))()
@@ -217,6 +256,12 @@ class FTGemm:
     def run(self, A, B, C_, *, alpha=1.0, beta=0.0, ft_level=FT_CORRECT, injections=(), stream=None):
         run(self.dtype, A, B, C_, alpha=alpha, beta=beta, enc_ws=self.enc_ws, ft_level=ft_level,
             injections=injections, report_ws=self.report_ws, stream=stream)
+
+    def run_offline(self, A, B, C_, *, alpha=1.0, beta=0.0, injections=(), inj_run=None, max_runs=4,
+                    c_backup=None, stream=None):
+        return run_offline(self.dtype, A, B, C_, alpha=alpha, beta=beta, enc_ws=self.enc_ws,
+                           report_ws=self.report_ws, injections=injections, inj_run=inj_run, max_runs=max_runs,
+                           c_backup=c_backup, stream=stream)
 
     def __call__(self, A, B, C_=None, **kw):
         if C_ is None:

@@ -126,3 +126,40 @@ def test_no_cpu_fallback(F):
     rc = lib.ftgemm_run(2, 64, 64, 64, 1.0, base, 64, base, 64, 0.0, base, 64, None, 0, None, 0, None, None)
     assert rc == 2
     assert "sm_100" in lib.ftgemm_last_error().decode()
+
+
+def test_cost_model_host(F):
+    """ftgemm_cost_model (host-only) against the oracle's closed form and its
+    pins (tests/test_oracle.py::test_cost_model_online_vs_offline)."""
+    import math
+    from oracle import cost_model as cm
+    assert C.sizeof(F.Cost) == 40
+    for g0, tiles in ((1 / 256, 64), (1e-6, 2048), (0.0, 5), (0.01, 10), (1e-3, 108900)):
+        c = F.cost_model(g0, tiles)
+        g = cm.gamma(g0, tiles)
+        assert abs(c["gamma"] - g) <= 1e-12 * max(1.0, g) and c["online_expected_runs"] == 1.0
+        if g < 0.5:
+            assert abs(c["offline_expected_runs"] - cm.offline_expected_runs(g)) <= 1e-12 * cm.offline_expected_runs(g)
+        else:
+            assert math.isinf(c["offline_expected_runs"])
+    c = F.cost_model(1 / 256, 64)
+    assert abs(c["gamma"] - 0.221580) < 5e-7 and abs(c["offline_expected_runs"] - 1.397925) < 5e-7
+    for bad in ((-0.1, 4), (1.0, 4), (0.1, 0)):
+        with pytest.raises(F.FtgemmError) as e:
+            F.cost_model(*bad)
+        assert e.value.code == 1
+
+
+def test_run_offline_argument_errors(F):
+    lib = F.lib()
+    out = (C.c_int32 * 2)()
+    vp = C.c_void_p(16)
+    # max_runs < 1, beta != 0 without a backup, inj_run outside [0, max_runs)
+    assert lib.ftgemm_run_offline(2, 64, 64, 64, 1.0, vp, 64, vp, 64, 0.0, vp, 64, None, vp, None, None, 0, 0,
+                                  vp, C.cast(out, C.c_void_p), None) == 1
+    assert lib.ftgemm_run_offline(2, 64, 64, 64, 1.0, vp, 64, vp, 64, 0.5, vp, 64, None, vp, None, None, 0, 2,
+                                  vp, C.cast(out, C.c_void_p), None) == 1
+    inj = (F.Inject * 1)(F.Inject(0, 0, 0, 3, 0, 0, 0.0))
+    run = (C.c_int32 * 1)(5)
+    assert lib.ftgemm_run_offline(2, 64, 64, 64, 1.0, vp, 64, vp, 64, 0.0, vp, 64, None, vp, C.cast(inj, C.c_void_p),
+                                  C.cast(run, C.c_void_p), 1, 2, vp, C.cast(out, C.c_void_p), None) == 1

@@ -215,6 +215,77 @@ def test_false_positive_sweep(dtype):
         assert c.counts["tiles_checked"] == c.plan.tiles_m * c.plan.tiles_n
 
 
+# ------------------------------------------- offline (detect-only) ABFT ----
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_detect_rows_parity(dtype):
+    """FT_DETECT_ROWS: the same tiles flagged at the same
+    first row with the same row counts as the oracle; column-reference faults
+    are invisible, row-reference faults flag their row; C is left as computed."""
+    F = ftmod()
+    M, N, K = 640, 760, 512
+    A, B, _ = synth.problem(M, N, K, dtype=odt(dtype))
+    plan = F.plan(dtype, M, N, K)
+    tm, tn = plan.check_tile_m, plan.check_tile_n
+    inj = detectable_sites(dtype, 5, M, N, K, plan, A, B, seed=31)
+    used = {(r // tm, c // tn) for r, c, *_ in inj}
+    extra = [(4 * tm + 3, 2 * tn + 1, 100, 0, oracle.INJ_ADD, oracle.TGT_COL_REF, 700.0),
+             (4 * tm + 5, 1, 100, 0, oracle.INJ_ADD, oracle.TGT_ROW_REF, 700.0),
+             (2 * tm + 1, tn + 2, 10, 0, oracle.INJ_ADD, 0, 900.0), (2 * tm + 9, tn + 7, 300, 0, oracle.INJ_ADD, 0, -900.0)]
+    inj += [f for f in extra if (f[0] // tm, f[1] // tn) not in used]
+    c = Case(dtype, M, N, K, injections=inj, ft=F.FT_DETECT_ROWS)
+    assert c.counts_match() and c.events_match(), (c.counts, c.ref.counts)
+    assert all(e["kind"] == F.EV_DETECTED and e["col"] == -1 for e in c.events)
+    assert c.counts["tiles_checked"] == plan.tiles_m * plan.tiles_n
+    bad = np.zeros((M, N), bool)
+    for r, col, _, _, _, tgt, _ in inj:
+        if tgt == 0:
+            bad[r, col] = True
+    assert c.fro(~bad) < (TOL[dtype] if dtype != "f32_simt" else 5e-6)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_run_offline_recompute(dtype):
+    """Offline ABFT: detect, then re-compute the product; the
+    final C equals the fault-free product; beta != 0 restores C_in from the
+    backup; faults striking the re-computation trigger further executions."""
+    import torch
+    F = ftmod()
+    M, N, K = 512, 520, 384
+    A, B, Cin = synth.problem(M, N, K, dtype=odt(dtype))
+    plan = F.plan(dtype, M, N, K)
+    tm, tn = plan.check_tile_m, plan.check_tile_n
+    ref = oracle.ftgemm(A, B, Cin, alpha=1.5, beta=-0.5, out=odt(dtype), tile_m=tm, tile_n=tn, bk=plan.bk,
+                        u_acc=plan.u_acc, lambda1=plan.lambda1, lambda2=plan.lambda2, ft_level=oracle.FT_OFF)
+    g = F.FTGemm(dtype, M, N, K)
+    Ad, Bd = synth.to_torch(A, odt(dtype)).cuda(), synth.to_torch(B, odt(dtype)).cuda()
+    g.encode(Ad, Bd)
+    faults = [(5, 7, 40, 0, oracle.INJ_ADD, 0, 1000.0), (tm + 3, tn + 4, 200, 0, oracle.INJ_ADD, 0, -1000.0),
+              (3 * tm + 1, 2 * tn + 9, 300, 0, oracle.INJ_ADD, 0, 5000.0)]
+    tol = TOL[dtype] if dtype != "f32_simt" else 5e-6
+
+    def go(inj_run, max_runs, beta=-0.5):
+        Cd = synth.to_torch(Cin, odt(dtype)).cuda()
+        g.reset()
+        runs, clean = g.run_offline(Ad, Bd, Cd, alpha=1.5, beta=beta, injections=faults, inj_run=inj_run,
+                                    max_runs=max_runs)
+        torch.cuda.synchronize()
+        counts, events = g.report()
+        return runs, clean, counts, events, Cd.float().cpu().numpy()
+
+    runs, clean, counts, events, Cg = go([0, 0, 0], 4)
+    assert (runs, clean) == (2, True) and counts["tiles_detected"] == 3
+    assert sorted((e["tile_m"], e["tile_n"]) for e in events) == [(0, 0), (1, 1), (3, 2)]
+    assert np.linalg.norm(Cg - ref.C) / np.linalg.norm(ref.C) < tol
+    runs, clean, counts, _, Cg = go([0, 1, 1], 4)
+    assert (runs, clean) == (3, True) and counts["tiles_detected"] == 3
+    assert np.linalg.norm(Cg - ref.C) / np.linalg.norm(ref.C) < tol
+    runs, clean, counts, _, _ = go([0, 1, 1], 2)
+    assert (runs, clean) == (2, False)
+    runs, clean, counts, _, _ = go([0, 0, 0], 4, beta=0.0)
+    assert (runs, clean) == (2, True) and counts["tiles_checked"] == 2 * plan.tiles_m * plan.tiles_n
+
+
 # ----------------------------------------------------- CTA pairs (2-SM MMA) --
 
 @pytest.mark.parametrize("cg", [1, 2])

@@ -245,6 +245,59 @@ def test_detect_level_locates_without_correcting(oracle_lib):
     assert np.array_equal(r.C.astype(np.float64), exact)
 
 
+def test_detect_rows_level_offline(oracle_lib):
+    """Offline detect-only ABFT (R15): row checks
+    only.  Integer inputs make every residual exact: an accumulator fault flags
+    exactly its row (event DETECTED, C left as computed, i.e. exact + delta); a
+    row-reference fault flags its row too (a false alarm costs a recompute);
+    a column-reference fault is invisible; clean tiles are only counted."""
+    A, B = ints(55, 32, 40), ints(56, 40, 32)
+    exact = (A.astype(np.int64) @ B.astype(np.int64)).astype(np.float64)
+    lvl = oracle.FT_DETECT_ROWS
+    r = oracle.ftgemm(A, B, tile_m=16, tile_n=16, ft_level=lvl,
+                      injections=[(18, 5, 7, 0, oracle.INJ_ADD, 0, 6.0)])
+    assert r.counts["tiles_checked"] == 4 and r.counts["tiles_detected"] == 1
+    assert r.counts["corrected"] == r.counts["located"] == r.counts["uncorrectable"] == 0
+    e = r.events[0]
+    assert (e["kind"], e["row"], e["col"], e["n_rows"], e["n_cols"], e["tile_m"], e["tile_n"]) == \
+        (oracle.EV_DETECTED, 18, -1, 1, 0, 1, 0)
+    assert e["resid_row"] == 6.0
+    want = exact.copy(); want[18, 5] += 6.0
+    assert np.array_equal(r.C.astype(np.float64), want)
+    r = oracle.ftgemm(A, B, tile_m=16, tile_n=16, ft_level=lvl,
+                      injections=[(3, 4, 10, 0, oracle.INJ_ADD, oracle.TGT_ROW_REF, 50.0)])
+    assert r.counts["tiles_detected"] == 1 and r.events[0]["row"] == 3
+    assert np.array_equal(r.C.astype(np.float64), exact)
+    r = oracle.ftgemm(A, B, tile_m=16, tile_n=16, ft_level=lvl,
+                      injections=[(3, 4, 10, 0, oracle.INJ_ADD, oracle.TGT_COL_REF, 50.0)])
+    assert r.counts["tiles_detected"] == 0 and r.counts["tiles_checked"] == 4
+    # two faults in one tile: still one detection (the tile is recomputed anyway)
+    r = oracle.ftgemm(A, B, tile_m=16, tile_n=16, ft_level=lvl,
+                      injections=[(1, 2, 0, 0, oracle.INJ_ADD, 0, 3.0), (7, 9, 0, 0, oracle.INJ_ADD, 0, -4.0)])
+    assert r.counts["tiles_detected"] == 1 and r.events[0]["n_rows"] == 2 and r.events[0]["row"] == 1
+
+
+def test_cost_model_online_vs_offline():
+    """gamma = 1-(1-gamma0)^tiles, offline expected executions
+    (1-gamma)/(1-2gamma).  Pinned by (a) the survey's evaluation for gamma0 = 1/256
+    and 64 tiles (1024^2 in 128x128 tiles, SURVEY 8c / SPEC:491), (b) the
+    independent Monte-Carlo branching process of reading R16, (c) the domain."""
+    from oracle import cost_model as cm
+    assert cm.tiles_of(1024, 1024, 128, 128) == 64
+    g = cm.gamma(1 / 256, 64)
+    assert abs(g - 0.221580) < 5e-7 and abs(cm.offline_expected_runs(g) - 1.397925) < 5e-7
+    assert cm.gamma(0.0, 1000) == 0.0 and cm.offline_expected_runs(0.0) == 1.0
+    assert cm.online_expected_runs(g) == 1.0
+    assert cm.simulate_offline(0.0, 1000) == 1.0
+    for gg, trials, tol in ((0.2, 20000, 0.05), (0.4, 20000, 0.05), (g, 20000, 0.05)):
+        mc = cm.simulate_offline(gg, trials, seed=7)
+        assert abs(mc - cm.offline_expected_runs(gg)) <= tol * cm.offline_expected_runs(gg), (gg, mc)
+    with pytest.raises(ValueError):
+        cm.offline_expected_runs(0.5)
+    with pytest.raises(ValueError):
+        cm.gamma(1.0, 4)
+
+
 def test_ft_off_no_checking(oracle_lib):
     A, B = ints(53, 16, 40), ints(54, 40, 16)
     r = oracle.ftgemm(A, B, tile_m=16, tile_n=16, ft_level=oracle.FT_OFF,
