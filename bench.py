@@ -34,6 +34,7 @@ METRIC = "FT-GEMM TFLOPS & % overhead vs non-FT/cuBLAS at 0..N errors/min, 1-8 B
 M_PER_RANK, N_DIM, K_DIM = 8192, 8192, 8192
 ERRORS_PER_MIN = 500.0           # "hundreds of errors per minute" (north_star)
 SWEEP_RATES = (0.0, 1.0, 10.0, 100.0, 500.0)
+OFFLINE_GAMMA0 = (1e-5, 1e-4, 2e-4)   # per-tile error probability per execution (online vs offline)
 
 
 def parse():
@@ -264,7 +265,7 @@ def run_ours(args):
     counts, events = g.report()
     ok_faults = counts["corrected"] == n_injected and counts["uncorrectable"] == 0 and counts["checksum_only"] == 0
     value = flops_rank * world / (ms_step * 1e-3) / 1e12
-    launches_per_step = 5   # encode_a, finalize(A), encode_b, finalize(B), fused GEMM
+    launches_per_step = 3   # encode_a, encode_b, fused GEMM (tickets reset by cudaMemsetAsync, not kernels)
 
     extra = {}
     if not args.no_sweep:
@@ -315,7 +316,53 @@ def run_ours(args):
                           "overhead_vs_cublas_pct": 100.0 * (t - t_cub) / t_cub,
                           "model_ms_per_step": model,
                           "model_overhead_vs_ft_off_pct": 100.0 * (model - t_off) / t_off}
+        # ---- online vs offline ABFT: per-tile error rate gamma0 ----
+        offline = {}
+        t_rows = timed([lambda: g.run(A, B, C, ft_level=F.FT_DETECT_ROWS)] * reps, 2)
+
+        def draw(g0):
+            hit = np.nonzero(rng.random(tiles_total) < g0)[0]
+            out = []
+            for t in hit:
+                ti, tj = divmod(int(t), pl.tiles_n)
+                out.append((ti * pl.check_tile_m + int(rng.integers(min(pl.check_tile_m, Mr - ti * pl.check_tile_m))),
+                            tj * pl.check_tile_n + int(rng.integers(min(pl.check_tile_n, N - tj * pl.check_tile_n))),
+                            int(rng.integers(K)), 30, F.INJ_FLIP, F.TGT_ACC, 0.0))
+            return out
+        calls, max_runs = 20, 8
+        for g0 in OFFLINE_GAMMA0:
+            cm = F.cost_model(g0, tiles_total)
+            on_inj = [draw(g0) for _ in range(calls)]
+            t_on = timed([(lambda inj: (lambda: step(inj)))(x) for x in on_inj], 2)
+            execs = []
+            e0o, e1o = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0o.record(stream)
+            for _ in range(calls):
+                inj, run_of = [], []
+                for r in range(max_runs):
+                    d = draw(g0)
+                    inj += d
+                    run_of += [r] * len(d)
+                g.encode(A, B)
+                n_exec, clean = g.run_offline(A, B, C, injections=inj, inj_run=run_of, max_runs=max_runs)
+                execs.append(n_exec)
+            e1o.record(stream)
+            e1o.synchronize()
+            t_off_call = e0o.elapsed_time(e1o) / calls
+            offline[f"{g0:g}"] = {
+                "gamma": cm["gamma"], "tiles": tiles_total, "calls": calls,
+                "online_ms_per_call": t_on, "online_faults": sum(len(x) for x in on_inj),
+                "offline_ms_per_call": t_off_call, "offline_mean_executions": float(np.mean(execs)),
+                "offline_restart_model_executions": 1.0 / (1.0 - cm["gamma"]),
+                "paper_model_offline_expected_runs": cm["offline_expected_runs"],
+                "paper_model_offline_ms": med["encode"] + cm["offline_expected_runs"] * t_rows,
+                "offline_vs_online_pct": 100.0 * (t_off_call - t_on) / t_on}
+        g.reset()
         extra = {
+            "detect_rows_run_ms": t_rows,
+            "detect_rows_overhead_vs_ft_off_pct": 100.0 * (t_rows - med["ft_off"]) / med["ft_off"],
+            "online_vs_offline": offline,
             "ft_off_ms": t_off, "ft_off_tflops": flops_rank * world / (t_off * 1e-3) / 1e12,
             "cublas_ms": t_cub, "cublas_tflops": flops_rank * world / (t_cub * 1e-3) / 1e12,
             "ft_step_ms": med["ft_step"], "ft_run_only_ms": med["ft_run"],
