@@ -287,6 +287,9 @@ def run_ours(args):
             "encode": lambda: g.encode(A, B),
             "encode_a": lambda: g.encode(A, None, which=1),
             "one_fault_run": lambda: g.run(A, B, C, ft_level=F.FT_CORRECT, injections=one),
+            # the paper's comparison scheme (Ding 2011): cuBLAS GEMMs + separate verification
+            "nonfused_step": lambda: (g.encode(A, B, which=3 | 4), g.run_nonfused(A, B, C, ft_level=F.FT_CORRECT)),
+            "nonfused_run": lambda: g.run_nonfused(A, B, C, ft_level=F.FT_CORRECT),
         }
         samples = {k: [] for k in configs}
         rate_samples = {str(int(r)): [] for r in SWEEP_RATES}
@@ -359,7 +362,10 @@ def run_ours(args):
                 "paper_model_offline_ms": med["encode"] + cm["offline_expected_runs"] * t_rows,
                 "offline_vs_online_pct": 100.0 * (t_off_call - t_on) / t_on}
         g.reset()
+        g.encode(A, B)                               # restore the fused path's encoded operand
         extra = {
+            "nonfused_step_ms": med["nonfused_step"], "nonfused_run_ms": med["nonfused_run"],
+            "fused_speedup_vs_nonfused_pct": 100.0 * (med["nonfused_step"] - med["ft_step"]) / med["ft_step"],
             "detect_rows_run_ms": t_rows,
             "detect_rows_overhead_vs_ft_off_pct": 100.0 * (t_rows - med["ft_off"]) / med["ft_off"],
             "online_vs_offline": offline,

@@ -86,6 +86,25 @@ typedef struct ftgemm_inject {
     float   addend;     /* for FTGEMM_INJ_ADD */
 } ftgemm_inject_t;      /* 40 bytes */
 
+/* ---- non-fused ABFT baseline (the paper's comparison scheme) -----------------
+ * Ding et al. 2011 as the paper benchmarks it:
+ * library GEMMs + separate kernels instead of one fused kernel.  C32 = A B by
+ * cuBLAS with an FP32 result; the references A (B e) and (e^T A) B by two more
+ * cuBLAS GEMMs (BF16: exact 3-term splits of B e and e^T A); faults (inj, same
+ * type as ftgemm_run; k_elem is ignored: a library GEMM cannot be entered
+ * mid-K, so a fault strikes the FP32 result); then one verification kernel per
+ * check tile with the fused path's threshold, decision and correction, and the
+ * alpha / beta store.  enc_ws: ftgemm_encode(which = 3 | 4) of A and B (4 =
+ * checksums only, no encoded operand).  nf_ws: device workspace of
+ * ftgemm_nonfused_workspace() bytes (C32, references, split operands).
+ * ft_level FT_OFF = the plain cuBLAS GEMM into C.  dtypes BF16 and F32_SIMT
+ * (FP32 SGEMM, no TF32); TF32 -> UNSUPPORTED.  Report as ftgemm_run.        */
+FTGEMM_API int ftgemm_nonfused_workspace(int dtype, int64_t M, int64_t N, int64_t K, int64_t* bytes);
+FTGEMM_API int ftgemm_run_nonfused(int dtype, int64_t M, int64_t N, int64_t K, float alpha,
+               const void* A, int64_t lda, const void* B, int64_t ldb,
+               float beta, void* C, int64_t ldc, const void* enc_ws, void* nf_ws, int ft_level,
+               const ftgemm_inject_t* inj, int32_t n_inj, void* report_ws, void* stream);
+
 /* ---- offline (detect-only) ABFT with re-computation -------------------------
  * PAPER.md:571-583 (section 5.5, "Online ABFT vs. Offline ABFT"): executions of
  * ftgemm_run at FT_DETECT_ROWS (row checks only, nothing corrected); after
@@ -190,7 +209,8 @@ FTGEMM_API int ftgemm_plan(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_pl
  *                         ||A[p,:]||_2 per row and ||Ac_i||_2.
  * which = 2: encode B  ->  per check-tile j: Br_j[k] = sum_{q in tile cols} B[k,q],
  *                         its split, ||B[:,q]||_2 per column and ||Br_j||_2.
- * which = 3: both.  Writes only enc_ws (plan.enc_bytes, caller-allocated,
+ * which = 3: both.  which | 4: checksums and norms only, without the encoded
+ * operand B^r (the non-fused baseline's encode).  Writes only enc_ws (plan.enc_bytes, caller-allocated,
  * 256-byte aligned); A and B are read-only.  The A part and the B part are
  * disjoint ([0, enc_b_offset) and [enc_b_offset, +enc_b_bytes)), so a B
  * encoded on one GPU can be broadcast with B and reused (weights).

@@ -31,6 +31,16 @@ cudaError_t launch_tc(bool tf32, int bn, bool ft, int cg, const CUtensorMap& mA,
                       const CUtensorMap& mC, const CUtensorMap& mC29, const CUtensorMap& mY, const TcArgs& a,
                       cudaStream_t st);
 cudaError_t launch_simt(bool ft, const SimtArgs& a, cudaStream_t st);
+struct NfInject {
+    int64_t row, col;
+    int32_t bit, mode, target;
+    float addend;
+};
+size_t nonfused_ws_bytes(const Geometry& g, int64_t M, int64_t N);
+cudaError_t launch_nonfused(const Geometry& g, const EncLayout& E, int64_t M, int64_t N, int64_t K, float alpha,
+                            const void* A, int64_t lda, const void* B, int64_t ldb, float beta, void* C, int64_t ldc,
+                            const void* enc_ws, void* nf_ws, int ft_level, const NfInject* dinj, int n_inj,
+                            ReportDev* rep, float tau_u, float l1, float l2, cudaStream_t st, const char** why);
 }  // namespace ftg
 
 using namespace ftg;
@@ -204,7 +214,7 @@ int ftgemm_encode(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int
                   int64_t ldb, void* enc_ws, int which, void* stream) {
     int e = check_dims(dtype, M, N, K);
     if (e) return e;
-    if (which < 1 || which > 3) return fail(FTGEMM_ERR_INVALID_VALUE, "which must be 1, 2 or 3");
+    if ((which & 3) == 0 || which > 7) return fail(FTGEMM_ERR_INVALID_VALUE, "which must be 1, 2 or 3 (| 4)");
     if (!enc_ws) return fail(FTGEMM_ERR_INVALID_VALUE, "null enc_ws");
     if ((which & 1) && (!A || lda < K)) return fail(FTGEMM_ERR_INVALID_VALUE, "bad A / lda");
     if ((which & 2) && (!B || ldb < N)) return fail(FTGEMM_ERR_INVALID_VALUE, "bad B / ldb");
@@ -351,6 +361,66 @@ int ftgemm_run(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const vo
         ce = launch_tc(tf32, p.bn, ft, p.cta_group, mA, mB, mC, mC29, mY, a, st);
     }
     if (ce != cudaSuccess) return fail_cuda(ce, "kernel launch");
+    g_err.clear();
+    return FTGEMM_OK;
+}
+
+int ftgemm_nonfused_workspace(int dtype, int64_t M, int64_t N, int64_t K, int64_t* bytes) {
+    int e = check_dims(dtype, M, N, K);
+    if (e) return e;
+    if (!bytes) return fail(FTGEMM_ERR_INVALID_VALUE, "null bytes");
+    if (dtype == FTGEMM_TF32) return fail(FTGEMM_ERR_UNSUPPORTED, "non-fused baseline: BF16 and F32_SIMT only");
+    ftgemm_plan_t p;
+    fill_plan(dtype, M, N, K, &p);
+    *bytes = (int64_t)nonfused_ws_bytes(geometry(p, K), M, N);
+    g_err.clear();
+    return FTGEMM_OK;
+}
+
+int ftgemm_run_nonfused(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const void* A, int64_t lda,
+                        const void* B, int64_t ldb, float beta, void* C, int64_t ldc, const void* enc_ws,
+                        void* nf_ws, int ft_level, const ftgemm_inject_t* inj, int32_t n_inj, void* report_ws,
+                        void* stream) {
+    int e = check_dims(dtype, M, N, K);
+    if (e) return e;
+    if (dtype == FTGEMM_TF32) return fail(FTGEMM_ERR_UNSUPPORTED, "non-fused baseline: BF16 and F32_SIMT only");
+    if (!A || !B || !C) return fail(FTGEMM_ERR_INVALID_VALUE, "null A, B or C");
+    if (lda < K || ldb < N || ldc < N) return fail(FTGEMM_ERR_INVALID_VALUE, "leading dimension too small");
+    if (ft_level < FTGEMM_FT_OFF || ft_level > FTGEMM_FT_DETECT_ROWS) return fail(FTGEMM_ERR_INVALID_VALUE, "bad ft_level");
+    if (n_inj < 0 || n_inj > kMaxInject || (n_inj > 0 && !inj)) return fail(FTGEMM_ERR_INVALID_VALUE, "bad injection list");
+    if (ft_level == FTGEMM_FT_OFF && n_inj > 0) return fail(FTGEMM_ERR_INVALID_VALUE, "fault injection needs FT on");
+    if (ft_level != FTGEMM_FT_OFF && (!enc_ws || !nf_ws || !report_ws))
+        return fail(FTGEMM_ERR_INVALID_VALUE, "FT needs enc_ws, nf_ws and report_ws");
+    if (!std::isfinite(alpha) || !std::isfinite(beta)) return fail(FTGEMM_ERR_INVALID_VALUE, "alpha/beta must be finite");
+    const int elt = dtype == FTGEMM_BF16 ? 2 : 4;
+    if (!aligned16(A) || !aligned16(B) || !aligned16(C) || (lda * elt) % 16 || (ldb * elt) % 16 || (ldc * elt) % 16)
+        return fail(FTGEMM_ERR_UNSUPPORTED, "A, B, C must be 16-byte aligned with 16-byte row pitches");
+    if (!check_device()) return fail(FTGEMM_ERR_UNSUPPORTED, "no sm_100 (B200) device");
+    ftgemm_plan_t p;
+    fill_plan(dtype, M, N, K, &p);
+    const Geometry g = geometry(p, K);
+    const EncLayout L = enc_layout(g, M, N);
+    cudaStream_t st = (cudaStream_t)stream;
+    const NfInject* dinj = nullptr;
+    if (n_inj > 0) {
+        std::vector<NfInject> v((size_t)n_inj);
+        for (int i = 0; i < n_inj; ++i) {
+            const ftgemm_inject_t& f = inj[i];
+            if (f.row < 0 || f.row >= M || f.col < 0 || f.col >= N || f.bit < 0 || f.bit > 31 || f.mode < 0 ||
+                f.mode > 1 || f.target < 0 || f.target > 2)
+                return fail(FTGEMM_ERR_INVALID_VALUE, "injection %d out of range", i);
+            v[i] = NfInject{f.row, f.col, f.bit, f.mode, f.target, f.addend};
+        }
+        char* dst = reinterpret_cast<char*>(report_ws) + report_inject_offset();
+        cudaError_t ce = cudaMemcpyAsync(dst, v.data(), sizeof(NfInject) * v.size(), cudaMemcpyHostToDevice, st);
+        if (ce != cudaSuccess) return fail_cuda(ce, "fault-list upload");
+        dinj = reinterpret_cast<const NfInject*>(dst);
+    }
+    const char* why = "kernel launch";
+    cudaError_t ce = launch_nonfused(g, L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, enc_ws, nf_ws, ft_level, dinj,
+                                     n_inj, reinterpret_cast<ReportDev*>(report_ws), p.u_acc, p.lambda1, p.lambda2, st,
+                                     &why);
+    if (ce != cudaSuccess) return fail_cuda(ce, why);
     g_err.clear();
     return FTGEMM_OK;
 }

@@ -138,6 +138,24 @@ __device__ __forceinline__ float bf16_to_f32(uint16_t h) { return __uint_as_floa
 __device__ __forceinline__ uint16_t f32_to_bf16_rn(float x) {
     return __bfloat16_as_ushort(__float2bfloat16_rn(x));
 }
+
+// Exact three-term split of an FP32 value into operand-format values.
+// kind 0 = BF16 (round-to-nearest-even per term), 1 = TF32 (truncation).
+template <int KIND>
+__device__ __forceinline__ void split3(float s, float& hi, float& mid, float& lo) {
+    if constexpr (KIND == 0) {
+        hi = bf16_to_f32(f32_to_bf16_rn(s));
+        float r1 = s - hi;
+        mid = bf16_to_f32(f32_to_bf16_rn(r1));
+        lo = bf16_to_f32(f32_to_bf16_rn(r1 - mid));
+    } else {
+        hi = tf32_trunc(s);
+        float r1 = s - hi;
+        mid = tf32_trunc(r1);
+        lo = r1 - mid;
+    }
+}
+
 // two floats -> packed bf16x2 (RNE), low half = a (one cvt.rn.bf16x2.f32)
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
     uint32_t r;

@@ -44,23 +44,6 @@ __device__ __forceinline__ float block_sum256(float x, float* red8) {
     return t;
 }
 
-// Exact three-term split of an FP32 value into operand-format values.
-// kind 0 = BF16 (round-to-nearest-even per term), 1 = TF32 (truncation).
-template <int KIND>
-__device__ __forceinline__ void split3(float s, float& hi, float& mid, float& lo) {
-    if constexpr (KIND == 0) {
-        hi = bf16_to_f32(f32_to_bf16_rn(s));
-        float r1 = s - hi;
-        mid = bf16_to_f32(f32_to_bf16_rn(r1));
-        lo = bf16_to_f32(f32_to_bf16_rn(r1 - mid));
-    } else {
-        hi = tf32_trunc(s);
-        float r1 = s - hi;
-        mid = tf32_trunc(r1);
-        lo = r1 - mid;
-    }
-}
-
 // 8 consecutive operand values of a row starting at p (valid = elements inside K)
 template <int MODE>
 __device__ __forceinline__ void load8(const void* base, int64_t off, int valid, float (&v)[8]) {
@@ -420,7 +403,7 @@ __global__ void __launch_bounds__(256) encode_b_tc_kernel(const void* __restrict
             if (k >= kp) continue;
             uint8_t* row = Bt + ((int64_t)k * ldt + (int64_t)tj * bn) * ELT;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < 2 && Bt != nullptr; ++h) {     // Bt == nullptr: checksums only
                 const int ch = lane + 32 * h;
                 if (ch < nch) {
                     *reinterpret_cast<V*>(row + ch * 4 * ELT) = raw[u][h];
@@ -501,7 +484,7 @@ cudaError_t launch_encode(const Geometry& g, const EncLayout& L, int64_t M, int6
                                                        g.kp, g.nkc_b, F(L.br), F(L.cn2), F(L.brn2), tk,
                                                        F(L.colnorm), F(L.brnorm));
         } else {
-            uint8_t* Bt = reinterpret_cast<uint8_t*>(base + L.bt);
+            uint8_t* Bt = (which & 4) ? nullptr : reinterpret_cast<uint8_t*>(base + L.bt);   // 4: no encoded operand
 #define ENC_B(MD) encode_b_tc_kernel<MD><<<grid, 256, 0, st>>>(B, ldb, (int)N, (int)K, g.bnd, g.bn, g.kp, \
             g.tiles_n * g.bn, g.nkc_b, F(L.br), Bt, F(L.cn2), F(L.brn2), tk, F(L.colnorm), F(L.brnorm))
             if (mode == 0) ENC_B(0); else ENC_B(1);

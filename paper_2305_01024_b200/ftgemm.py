@@ -60,6 +60,7 @@ class Cost(C.Structure):
 
 
 SYMBOLS = ("ftgemm_plan", "ftgemm_encode", "ftgemm_run", "ftgemm_run_offline", "ftgemm_cost_model",
+           "ftgemm_nonfused_workspace", "ftgemm_run_nonfused",
            "ftgemm_report", "ftgemm_report_reset", "ftgemm_last_error", "ftgemm_version", "ftgemm_device_arch")
 
 _lib = None
@@ -81,6 +82,9 @@ def lib():
         L.ftgemm_run_offline.argtypes = [C.c_int, i64, i64, i64, C.c_float, vp, i64, vp, i64, C.c_float, vp, i64,
                                          vp, vp, vp, vp, i32, i32, vp, vp, vp]
         L.ftgemm_cost_model.argtypes = [C.c_double, i64, C.POINTER(Cost)]
+        L.ftgemm_nonfused_workspace.argtypes = [C.c_int, i64, i64, i64, C.POINTER(C.c_int64)]
+        L.ftgemm_run_nonfused.argtypes = [C.c_int, i64, i64, i64, C.c_float, vp, i64, vp, i64, C.c_float, vp, i64,
+                                          vp, vp, C.c_int, vp, i32, vp, vp]
         L.ftgemm_report.argtypes = [vp, C.POINTER(Counts), vp, i32, vp]
         L.ftgemm_report_reset.argtypes = [vp, i64, vp]
         L.ftgemm_last_error.restype = C.c_char_p
@@ -211,6 +215,28 @@ def run_offline(dtype, A: torch.Tensor, B: torch.Tensor, C_: torch.Tensor, *, al
     return int(out[0]), bool(out[1])
 
 
+def nonfused_workspace(dtype, M: int, N: int, K: int) -> int:
+    b = C.c_int64()
+    _check(lib().ftgemm_nonfused_workspace(_dt(dtype), M, N, K, C.byref(b)), "ftgemm_nonfused_workspace")
+    return int(b.value)
+
+
+def run_nonfused(dtype, A: torch.Tensor, B: torch.Tensor, C_: torch.Tensor, *, alpha: float = 1.0, beta: float = 0.0,
+                 enc_ws: torch.Tensor | None = None, nf_ws: torch.Tensor | None = None, ft_level: int = FT_CORRECT,
+                 injections=(), report_ws: torch.Tensor | None = None, stream=None):
+    """The non-fused ABFT baseline (cuBLAS GEMMs + separate verification kernel)."""
+    M, K = A.shape
+    N = B.shape[1]
+    arr, n = _inj_array(injections)
+    _check(lib().ftgemm_run_nonfused(_dt(dtype), M, N, K, alpha, A.data_ptr(), A.stride(0), B.data_ptr(),
+                                     B.stride(0), beta, C_.data_ptr(), C_.stride(0),
+                                     enc_ws.data_ptr() if enc_ws is not None else None,
+                                     nf_ws.data_ptr() if nf_ws is not None else None, ft_level,
+                                     C.cast(arr, C.c_void_p) if arr is not None else None, n,
+                                     report_ws.data_ptr() if report_ws is not None else None, _stream(stream)),
+           "ftgemm_run_nonfused")
+
+
 def cost_model(gamma0: float, tiles: int) -> dict:
     """Online vs offline expected executions (host-only)."""
     c = Cost()
@@ -262,6 +288,14 @@ class FTGemm:
         return run_offline(self.dtype, A, B, C_, alpha=alpha, beta=beta, enc_ws=self.enc_ws,
                            report_ws=self.report_ws, injections=injections, inj_run=inj_run, max_runs=max_runs,
                            c_backup=c_backup, stream=stream)
+
+    def run_nonfused(self, A, B, C_, *, alpha=1.0, beta=0.0, ft_level=FT_CORRECT, injections=(), stream=None):
+        """Non-fused baseline; encode first with encode(A, B, which=3 | 4)."""
+        if getattr(self, "nf_ws", None) is None:
+            self.nf_ws = torch.empty(max(256, nonfused_workspace(self.dtype, self.M, self.N, self.K)),
+                                     dtype=torch.uint8, device=self.enc_ws.device)
+        run_nonfused(self.dtype, A, B, C_, alpha=alpha, beta=beta, enc_ws=self.enc_ws, nf_ws=self.nf_ws,
+                     ft_level=ft_level, injections=injections, report_ws=self.report_ws, stream=stream)
 
     def __call__(self, A, B, C_=None, **kw):
         if C_ is None:

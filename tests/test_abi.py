@@ -163,3 +163,18 @@ def test_run_offline_argument_errors(F):
     run = (C.c_int32 * 1)(5)
     assert lib.ftgemm_run_offline(2, 64, 64, 64, 1.0, vp, 64, vp, 64, 0.0, vp, 64, None, vp, C.cast(inj, C.c_void_p),
                                   C.cast(run, C.c_void_p), 1, 2, vp, C.cast(out, C.c_void_p), None) == 1
+
+
+def test_nonfused_host_checks(F):
+    """Workspace query (host) and the synchronous argument checks of the
+    non-fused baseline: TF32 is unsupported (cuBLAS rounds TF32 operands to
+    nearest, the encode truncates as the tensor core does)."""
+    b = F.nonfused_workspace("bf16", 1000, 1112, 704)
+    assert b >= 1000 * 1112 * 4
+    with pytest.raises(F.FtgemmError) as e:
+        F.nonfused_workspace("tf32", 64, 64, 64)
+    assert e.value.code == 2
+    lib = F.lib()
+    vp = C.c_void_p(16)
+    assert lib.ftgemm_run_nonfused(1, 64, 64, 64, 1.0, vp, 64, vp, 64, 0.0, vp, 64, vp, vp, 2, None, 0, vp, None) == 2
+    assert lib.ftgemm_run_nonfused(2, 64, 64, 64, 1.0, vp, 64, vp, 64, 0.0, vp, 64, None, None, 2, None, 0, vp, None) == 1

@@ -10,7 +10,7 @@ import pytest
 
 import oracle
 import synth
-from gpu_util import TOL, Case, detectable_sites, odt
+from gpu_util import TOL, Case, detectable_sites, frob, odt
 
 pytestmark = pytest.mark.gpu
 
@@ -213,6 +213,52 @@ def test_false_positive_sweep(dtype):
         c = Case(dtype, 2048, 2048, 2048, dist=dist, run_oracle=False)
         assert c.counts["tiles_detected"] == 0
         assert c.counts["tiles_checked"] == c.plan.tiles_m * c.plan.tiles_n
+
+
+# ------------------------------------------------ non-fused baseline -------
+
+@pytest.mark.parametrize("dtype", ["f32_simt", "bf16"])
+def test_nonfused_parity(dtype):
+    """The non-fused baseline (cuBLAS GEMMs + verification kernel) computes the
+    same function: clean C within tolerance, faults striking the final
+    accumulator (k_elem = K-1 in the oracle) located / corrected / classified
+    exactly as the oracle does, FT_OFF = the plain library GEMM."""
+    import torch
+    F = ftmod()
+    M, N, K = 700, 904, 640
+    A, B, Cin = synth.problem(M, N, K, dtype=odt(dtype))
+    plan = F.plan(dtype, M, N, K)
+    tm, tn = plan.check_tile_m, plan.check_tile_n
+    inj = [(5, 7, K - 1, 0, oracle.INJ_ADD, 0, 1000.0), (tm + 3, tn + 4, K - 1, 0, oracle.INJ_ADD, 0, -700.0),
+           (2 * tm + 10, 2 * tn + 3, K - 1, 30, oracle.INJ_FLIP, 0, 0.0),
+           (3 * tm + 1, 5, K - 1, 0, oracle.INJ_ADD, oracle.TGT_ROW_REF, 800.0),
+           (4 * tm + 2, tn + 9, K - 1, 0, oracle.INJ_ADD, oracle.TGT_COL_REF, -800.0),
+           (5 * tm + 1, 3, K - 1, 0, oracle.INJ_ADD, 0, 900.0), (5 * tm + 6, 20, K - 1, 0, oracle.INJ_ADD, 0, 900.0)]
+    kw = dict(out=odt(dtype), tile_m=tm, tile_n=tn, bk=plan.bk, u_acc=plan.u_acc, lambda1=plan.lambda1,
+              lambda2=plan.lambda2)
+    g = F.FTGemm(dtype, M, N, K)
+    Ad, Bd = synth.to_torch(A, odt(dtype)).cuda(), synth.to_torch(B, odt(dtype)).cuda()
+    g.encode(Ad, Bd, which=3 | 4)
+    tol = TOL[dtype] if dtype != "f32_simt" else max(1e-6, 2 * 2 ** -24 * math.sqrt(K))
+    for level, faults in ((F.FT_CORRECT, []), (F.FT_CORRECT, inj), (F.FT_DETECT_ROWS, inj), (F.FT_OFF, [])):
+        Cd = synth.to_torch(Cin, odt(dtype)).cuda()
+        g.reset()
+        g.run_nonfused(Ad, Bd, Cd, alpha=1.5, beta=-0.5, ft_level=level, injections=faults)
+        torch.cuda.synchronize()
+        Cg = Cd.float().cpu().numpy()
+        ref = oracle.ftgemm(A, B, Cin, alpha=1.5, beta=-0.5, ft_level=level, injections=faults, **kw)
+        bad = np.zeros((M, N), bool)
+        if level != F.FT_OFF:
+            counts, events = g.report()
+            keys = ("tiles_checked", "tiles_detected", "corrected", "checksum_only", "uncorrectable", "located")
+            assert all(int(counts[k]) == int(ref.counts[k]) for k in keys), (level, counts, ref.counts)
+            ek = lambda evs: sorted((e["tile_m"], e["tile_n"], e["kind"], e["row"], e["col"], e["n_rows"], e["n_cols"])
+                                    for e in evs)
+            assert ek(events) == ek(ref.events), level
+            for e in ref.events:
+                if e["kind"] in (oracle.EV_UNCORRECTABLE, oracle.EV_DETECTED):
+                    bad[e["tile_m"] * tm:(e["tile_m"] + 1) * tm, e["tile_n"] * tn:(e["tile_n"] + 1) * tn] = True
+        assert frob(Cg, ref.C, ~bad) < tol, level
 
 
 # ------------------------------------------- offline (detect-only) ABFT ----

@@ -52,9 +52,18 @@ def measure(dt, M, N, K, batch=1):
         g.encode(A, B)
         g.run(A, B, C)
     cfg = {"ft_step": step, "ft_run": lambda: g.run(A, B, C), "ft_off": lambda: g.run(A, B, C, ft_level=F.FT_OFF),
-           "encode": lambda: g.encode(A, B), "cublas": lambda: torch.matmul(A, B, out=C)}
+           "encode": lambda: g.encode(A, B), "cublas": lambda: torch.matmul(A, B, out=C),
+           "detect_rows_run": lambda: g.run(A, B, C, ft_level=F.FT_DETECT_ROWS)}
+    if dt != "tf32":                     # the non-fused baseline (paper's comparison scheme)
+        def nf_step():
+            g.encode(A, B, which=3 | 4)
+            g.run_nonfused(A, B, C)
+        cfg["nonfused_step"] = nf_step
     g.encode(A, B)
     samp = {k: [] for k in cfg}
+    if "nonfused_step" in cfg:
+        nf_step()
+        g.encode(A, B)
     for _ in range(3):
         for k, fn in cfg.items():
             samp[k].append(timeit(fn, reps))
@@ -76,6 +85,8 @@ def measure(dt, M, N, K, batch=1):
     out["overhead_step_vs_ft_off_pct"] = 100 * (med["ft_step"] - med["ft_off"]) / med["ft_off"]
     out["overhead_run_vs_ft_off_pct"] = 100 * (med["ft_run"] - med["ft_off"]) / med["ft_off"]
     out["overhead_step_vs_cublas_pct"] = 100 * (med["ft_step"] - med["cublas"]) / med["cublas"]
+    if "nonfused_step" in med:
+        out["fused_speedup_vs_nonfused_pct"] = 100 * (med["nonfused_step"] - med["ft_step"]) / med["ft_step"]
     out["ft_run_io_gbs"] = batch * io_bytes / (med["ft_run"] * 1e-3) / 1e9
     out["peak_tflops"] = peak
     return out
