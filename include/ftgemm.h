@@ -86,6 +86,22 @@ typedef struct ftgemm_inject {
     float   addend;     /* for FTGEMM_INJ_ADD */
 } ftgemm_inject_t;      /* 40 bytes */
 
+/* ---- online verification every K_s (outer-product online ABFT) ----------------
+ * PAPER.md:170-173 (Chen's online scheme: the checksum relation holds after
+ * every outer-product step, so "the online version, which corrects a single
+ * error for each step ..., can handle multiple errors") with the paper's
+ * step K_s.  As ftgemm_run, plus: after every ks of K (ks a
+ * positive multiple of plan.bk) the fused kernel verifies the partial
+ * accumulator against the partial carried references and corrects in place
+ * (TMEM), so up to ceil(K / ks) faults per check tile are corrected.  Each
+ * step's check counts in tiles_checked; events carry k_checked.  The step
+ * threshold uses sqrt(k_checked) and the full-K norms (R17).
+ * ft_level DETECT or CORRECT; tensor-core dtypes (F32_SIMT -> UNSUPPORTED).  */
+FTGEMM_API int ftgemm_run_online(int dtype, int64_t M, int64_t N, int64_t K, float alpha,
+               const void* A, int64_t lda, const void* B, int64_t ldb,
+               float beta, void* C, int64_t ldc, const void* enc_ws, int ft_level, int64_t ks,
+               const ftgemm_inject_t* inj, int32_t n_inj, void* report_ws, void* stream);
+
 /* ---- non-fused ABFT baseline (the paper's comparison scheme) -----------------
  * Ding et al. 2011 as the paper benchmarks it:
  * library GEMMs + separate kernels instead of one fused kernel.  C32 = A B by
@@ -157,7 +173,8 @@ typedef struct ftgemm_event {
     int32_t tile_m, tile_n;      /* check-tile coordinates */
     int32_t kind;                /* FTGEMM_EV_* */
     int32_t n_rows, n_cols;      /* number of flagged rows / columns in the tile */
-    int32_t reserved;
+    int32_t k_checked;           /* K accumulated when the check fired: K for the end-of-K check,
+                                    the end of the K_s step in online-interval mode (ftgemm_run_online) */
     float   resid_row, resid_col;/* residual of the first flagged row / column */
     float   tau_row, tau_col;    /* the thresholds they were compared against */
 } ftgemm_event_t;                /* 56 bytes */

@@ -42,7 +42,7 @@ class Inject(C.Structure):
 class Event(C.Structure):
     _fields_ = [("row", C.c_int64), ("col", C.c_int64),
                 ("tile_m", C.c_int32), ("tile_n", C.c_int32), ("kind", C.c_int32),
-                ("n_rows", C.c_int32), ("n_cols", C.c_int32), ("reserved", C.c_int32),
+                ("n_rows", C.c_int32), ("n_cols", C.c_int32), ("k_checked", C.c_int32),
                 ("resid_row", C.c_double), ("resid_col", C.c_double),
                 ("tau_row", C.c_double), ("tau_col", C.c_double)]
 
@@ -68,7 +68,7 @@ class Problem(C.Structure):
                 ("counts", C.c_void_p),
                 ("events", C.c_void_p), ("max_events", C.c_int32), ("pad0", C.c_int32),
                 ("P_out", C.c_void_p), ("resid_row", C.c_void_p), ("resid_col", C.c_void_p),
-                ("tau_row", C.c_void_p), ("tau_col", C.c_void_p)]
+                ("tau_row", C.c_void_p), ("tau_col", C.c_void_p), ("ks", C.c_int64)]
 
 
 def build(force: bool = False) -> str:
@@ -123,11 +123,13 @@ class Result:
 
 def ftgemm(A, B, Cin=None, *, alpha=1.0, beta=0.0, out="f32", acc="fp64",
            tile_m=128, tile_n=128, bk=8, u_acc=2.0 ** -24, lambda1=16.0, lambda2=32.0,
-           ft_level=FT_CORRECT, injections=(), max_events=4096) -> Result:
+           ft_level=FT_CORRECT, injections=(), max_events=4096, ks=0) -> Result:
     """Run the oracle on float32 operand values A (MxK), B (KxN), C_in (MxN).
 
     injections: iterable of dicts/tuples (row, col, k_elem, bit, mode, target, addend).
+    ks > 0: online verification after every ks of K (FP64 mode).
     """
+    assert ks == 0 or acc == "fp64"
     A = _f32(A); B = _f32(B)
     M, K = A.shape
     K2, N = B.shape
@@ -160,7 +162,8 @@ def ftgemm(A, B, Cin=None, *, alpha=1.0, beta=0.0, out="f32", acc="fp64",
                  ft_level=ft_level, n_inj=len(inj), inj=C.cast(inj_arr, C.c_void_p),
                  counts=C.cast(C.pointer(counts), C.c_void_p),
                  events=C.cast(events, C.c_void_p), max_events=max_events, pad0=0,
-                 P_out=_ptr(P), resid_row=_ptr(rr), resid_col=_ptr(rc), tau_row=_ptr(tr), tau_col=_ptr(tc))
+                 P_out=_ptr(P), resid_row=_ptr(rr), resid_col=_ptr(rc), tau_row=_ptr(tr), tau_col=_ptr(tc),
+                 ks=ks)
     err = lib().oracle_ftgemm(C.byref(pr))
     if err:
         raise ValueError(f"oracle_ftgemm error {err}")
@@ -169,7 +172,7 @@ def ftgemm(A, B, Cin=None, *, alpha=1.0, beta=0.0, out="f32", acc="fp64",
     for i in range(min(cnt["events"], max_events)):
         e = events[i]
         evs.append(dict(row=e.row, col=e.col, tile_m=e.tile_m, tile_n=e.tile_n, kind=e.kind,
-                        n_rows=e.n_rows, n_cols=e.n_cols, resid_row=e.resid_row,
+                        n_rows=e.n_rows, n_cols=e.n_cols, k_checked=e.k_checked, resid_row=e.resid_row,
                         resid_col=e.resid_col, tau_row=e.tau_row, tau_col=e.tau_col))
     evs.sort(key=lambda e: (e["tile_m"], e["tile_n"], e["kind"], e["row"], e["col"]))
     if out == "f32":

@@ -61,7 +61,7 @@ typedef struct {
 
 typedef struct {
     int64_t row, col;
-    int32_t tile_m, tile_n, kind, n_rows, n_cols, reserved;
+    int32_t tile_m, tile_n, kind, n_rows, n_cols, k_checked;
     double resid_row, resid_col, tau_row, tau_col;
 } oracle_event_t;
 
@@ -89,6 +89,7 @@ typedef struct {
     double *resid_col;   /* optional tiles_m x N */
     double *tau_row;     /* optional M x tiles_n */
     double *tau_col;     /* optional tiles_m x N */
+    int64_t ks;          /* > 0: online verification every ks of K (run_tile_intervals) */
 } oracle_problem_t;
 
 /* ---- scalar helpers -------------------------------------------------------- */
@@ -178,9 +179,9 @@ static float inject_value(float x, const oracle_inject_t *in) {
     return flip_bit(x, in->bit);
 }
 
-static void emit_event(const oracle_problem_t *pr, int64_t ti, int64_t tj, int kind,
-                       int64_t row, int64_t col, int nr, int nc,
-                       double rr, double rc, double tr, double tc) {
+static void emit_event_k(const oracle_problem_t *pr, int64_t ti, int64_t tj, int kind,
+                         int64_t row, int64_t col, int nr, int nc,
+                         double rr, double rc, double tr, double tc, int64_t kchk) {
     oracle_counts_t *ct = pr->counts;
     int64_t slot;
 #pragma omp atomic capture
@@ -188,12 +189,18 @@ static void emit_event(const oracle_problem_t *pr, int64_t ti, int64_t tj, int k
     if (pr->events && slot < pr->max_events) {
         oracle_event_t *e = &pr->events[slot];
         e->row = row; e->col = col; e->tile_m = (int32_t)ti; e->tile_n = (int32_t)tj;
-        e->kind = kind; e->n_rows = nr; e->n_cols = nc; e->reserved = 0;
+        e->kind = kind; e->n_rows = nr; e->n_cols = nc; e->k_checked = (int32_t)kchk;
         e->resid_row = rr; e->resid_col = rc; e->tau_row = tr; e->tau_col = tc;
     } else {
 #pragma omp atomic
         ct->dropped++;
     }
+}
+
+static void emit_event(const oracle_problem_t *pr, int64_t ti, int64_t tj, int kind,
+                       int64_t row, int64_t col, int nr, int nc,
+                       double rr, double rc, double tr, double tc) {
+    emit_event_k(pr, ti, tj, kind, row, col, nr, nc, rr, rc, tr, tc, pr->K);
 }
 
 static int run_tile(const oracle_problem_t *pr, int64_t ti, int64_t tj) {
@@ -449,6 +456,170 @@ static int run_tile(const oracle_problem_t *pr, int64_t ti, int64_t tj) {
     return OR_OK;
 }
 
+/* ---- online verification every K_s -----------------
+ * Chen's outer-product online ABFT: C^f = sum_s A^c(:,s) B^r(s,:) keeps the
+ * checksum relation after every step s, so the tile is verified (and one error
+ * corrected) after each K_s-wide step instead of once at the end -- "the online
+ * version, which corrects a single error for each step of the outer-product
+ * update, can handle multiple errors".  Step by step, FP64:
+ *   for each step [k0, k1), k1 = min(K, k0 + ks):
+ *     P += A_i[:, k0:k1] B_j[k0:k1, :];  R_row += A_i[:, k0:k1] Br[k0:k1];
+ *     R_col += Ac[k0:k1] B_j[k0:k1, :]                (the carried C^r, C^c)
+ *     faults whose k-block ends in (k0, k1]: the FP32 view x of the running
+ *       value at that k-block is flipped (or offset) and the difference kept
+ *     verify with tau from DESIGN.md R1 / R17 (sqrt(k1) in place of sqrt(K),
+ *       the full-K norms), decide and correct as at the end of K;
+ *       every step's check counts in tiles_checked; events carry k_checked = k1.
+ * Mode FP64 only (the tensor-core paths). */
+static int run_tile_intervals(const oracle_problem_t *pr, int64_t ti, int64_t tj) {
+    const int64_t M = pr->M, N = pr->N, K = pr->K;
+    const int64_t r0 = ti * pr->tile_m, c0 = tj * pr->tile_n;
+    const int64_t bm = (r0 + pr->tile_m <= M) ? pr->tile_m : M - r0;
+    const int64_t bn = (c0 + pr->tile_n <= N) ? pr->tile_n : N - c0;
+    const float *A = pr->A, *B = pr->B;
+    const int64_t lda = pr->lda, ldb = pr->ldb;
+    double *P = (double *)calloc((size_t)(bm * bn), sizeof(double));
+    double *Ac = (double *)calloc((size_t)K, sizeof(double));
+    double *Br = (double *)calloc((size_t)K, sizeof(double));
+    double *Rr = (double *)calloc((size_t)bm, sizeof(double));
+    double *Rc = (double *)calloc((size_t)bn, sizeof(double));
+    double *na = (double *)calloc((size_t)bm, sizeof(double));
+    double *nb = (double *)calloc((size_t)bn, sizeof(double));
+    double *tr = (double *)calloc((size_t)bm, sizeof(double));
+    double *tc = (double *)calloc((size_t)bn, sizeof(double));
+    double *Sc = (double *)calloc((size_t)bn, sizeof(double));
+    if (!P || !Ac || !Br || !Rr || !Rc || !na || !nb || !tr || !tc || !Sc) return OR_ERR_NOMEM;
+
+    /* encode (Eq. 1, 2) and the full-K norms of the threshold (R1) */
+    for (int64_t p = 0; p < bm; ++p)
+        for (int64_t k = 0; k < K; ++k) {
+            double a = (double)A[(r0 + p) * lda + k];
+            Ac[k] += a; na[p] += a * a;
+        }
+    for (int64_t k = 0; k < K; ++k)
+        for (int64_t q = 0; q < bn; ++q) {
+            double b = (double)B[k * ldb + c0 + q];
+            Br[k] += b; nb[q] += b * b;
+        }
+    double nBr = 0.0, nAc = 0.0;
+    for (int64_t k = 0; k < K; ++k) { nBr += Br[k] * Br[k]; nAc += Ac[k] * Ac[k]; }
+    nBr = sqrt(nBr); nAc = sqrt(nAc);
+    const double u = pr->u_acc, l1 = pr->lambda1, l2 = pr->lambda2;
+
+    for (int64_t k0 = 0; k0 < K; ) {
+        const int64_t k1 = (k0 + pr->ks < K) ? k0 + pr->ks : K;
+        /* faults of this step, applied in (k_eff, list) order at their k-block:
+         * the running value at k_eff = value at k0 + the products in [k0, k_eff) */
+        int64_t kdone = k0;
+        for (;;) {
+            int64_t knext = k1 + 1; int32_t first = -1;
+            for (int32_t t = 0; t < pr->n_inj; ++t) {
+                const oracle_inject_t *in = &pr->inj[t];
+                if (in->row < r0 || in->row >= r0 + bm || in->col < c0 || in->col >= c0 + bn) continue;
+                int64_t ke = eff_k(pr, in->k_elem);
+                if (ke > kdone && ke <= k1 && ke < knext) { knext = ke; first = t; }
+            }
+            if (first < 0) break;
+            /* advance every running sum to knext */
+            for (int64_t p = 0; p < bm; ++p)
+                for (int64_t k = kdone; k < knext; ++k) {
+                    double a = (double)A[(r0 + p) * lda + k];
+                    for (int64_t q = 0; q < bn; ++q) P[p * bn + q] += a * (double)B[k * ldb + c0 + q];
+                    Rr[p] += a * Br[k];
+                }
+            for (int64_t k = kdone; k < knext; ++k)
+                for (int64_t q = 0; q < bn; ++q) Rc[q] += Ac[k] * (double)B[k * ldb + c0 + q];
+            kdone = knext;
+            for (int32_t t = first; t < pr->n_inj; ++t) {       /* every fault at knext, list order */
+                const oracle_inject_t *in = &pr->inj[t];
+                if (in->row < r0 || in->row >= r0 + bm || in->col < c0 || in->col >= c0 + bn) continue;
+                if (eff_k(pr, in->k_elem) != knext) continue;
+                double *v = in->target == OR_TGT_ROW_REF ? &Rr[in->row - r0]
+                          : in->target == OR_TGT_COL_REF ? &Rc[in->col - c0]
+                          : &P[(in->row - r0) * bn + (in->col - c0)];
+                if (!isfinite(*v)) continue;
+                float x = (float)*v, y = inject_value(x, in);
+                if (!isfinite(y)) *v = (double)y; else *v += (double)y - (double)x;
+            }
+        }
+        for (int64_t p = 0; p < bm; ++p)
+            for (int64_t k = kdone; k < k1; ++k) {
+                double a = (double)A[(r0 + p) * lda + k];
+                for (int64_t q = 0; q < bn; ++q) P[p * bn + q] += a * (double)B[k * ldb + c0 + q];
+                Rr[p] += a * Br[k];
+            }
+        for (int64_t k = kdone; k < k1; ++k)
+            for (int64_t q = 0; q < bn; ++q) Rc[q] += Ac[k] * (double)B[k * ldb + c0 + q];
+
+        /* verify this step */
+        const double sqk = sqrt((double)k1);
+        int nr = 0, nc = 0; int64_t pstar = -1, qstar = -1; double rstar = 0.0, cstar = 0.0;
+        for (int64_t q = 0; q < bn; ++q) Sc[q] = 0.0;
+        for (int64_t p = 0; p < bm; ++p) {
+            double s = 0.0;
+            for (int64_t q = 0; q < bn; ++q) { s += P[p * bn + q]; Sc[q] += P[p * bn + q]; }
+            tr[p] = u * (l1 * sqk * fabs(Rr[p]) + l2 * sqrt(na[p]) * nBr);
+            double r = s - Rr[p];
+            if (!(fabs(r) <= tr[p])) { if (nr == 0) { pstar = p; rstar = r; } ++nr; }
+        }
+        for (int64_t q = 0; q < bn; ++q) {
+            tc[q] = u * (l1 * sqk * fabs(Rc[q]) + l2 * nAc * sqrt(nb[q]));
+            double c = Sc[q] - Rc[q];
+            if (!(fabs(c) <= tc[q])) { if (nc == 0) { qstar = q; cstar = c; } ++nc; }
+        }
+#pragma omp atomic
+        pr->counts->tiles_checked++;
+        if (nr > 0 || nc > 0) {
+#pragma omp atomic
+            pr->counts->tiles_detected++;
+        }
+        double trs = pstar >= 0 ? tr[pstar] : 0.0, tcs = qstar >= 0 ? tc[qstar] : 0.0;
+        if (nr == 1 && nc == 1) {
+            double big = fabs(rstar) > fabs(cstar) ? fabs(rstar) : fabs(cstar);
+            int consistent = !(fabs(rstar - cstar) > trs + tcs + 2.0 * u * (double)(bm + bn) * big);
+            if (consistent && pr->ft_level == OR_FT_CORRECT) {
+                double s = 0.0;
+                for (int64_t q = 0; q < bn; ++q) if (q != qstar) s += P[pstar * bn + q];
+                P[pstar * bn + qstar] = Rr[pstar] - s;
+#pragma omp atomic
+                pr->counts->corrected++;
+                emit_event_k(pr, ti, tj, OR_EV_CORRECTED, r0 + pstar, c0 + qstar, nr, nc, rstar, cstar, trs, tcs, k1);
+            } else if (consistent) {
+#pragma omp atomic
+                pr->counts->located++;
+                emit_event_k(pr, ti, tj, OR_EV_LOCATED, r0 + pstar, c0 + qstar, nr, nc, rstar, cstar, trs, tcs, k1);
+            } else {
+#pragma omp atomic
+                pr->counts->uncorrectable++;
+                emit_event_k(pr, ti, tj, OR_EV_UNCORRECTABLE, r0 + pstar, c0 + qstar, nr, nc, rstar, cstar, trs, tcs, k1);
+            }
+        } else if ((nr == 1 && nc == 0) || (nr == 0 && nc == 1)) {
+#pragma omp atomic
+            pr->counts->checksum_only++;
+            emit_event_k(pr, ti, tj, OR_EV_CHECKSUM_ONLY, nr ? r0 + pstar : -1, nc ? c0 + qstar : -1,
+                         nr, nc, rstar, cstar, trs, tcs, k1);
+        } else if (nr > 0 || nc > 0) {
+#pragma omp atomic
+            pr->counts->uncorrectable++;
+            emit_event_k(pr, ti, tj, OR_EV_UNCORRECTABLE, nr ? r0 + pstar : -1, nc ? c0 + qstar : -1,
+                         nr, nc, rstar, cstar, trs, tcs, k1);
+        }
+        k0 = k1;
+    }
+    /* C = alpha P + beta C_in, rounded to the output dtype */
+    for (int64_t p = 0; p < bm; ++p)
+        for (int64_t q = 0; q < bn; ++q) {
+            int64_t g = (r0 + p) * pr->ldc + (c0 + q);
+            double cin = (pr->beta != 0.0 && pr->Cin) ? (double)pr->Cin[g] : 0.0;
+            if (pr->P_out) pr->P_out[(r0 + p) * N + (c0 + q)] = P[p * bn + q];
+            double v = pr->alpha * P[p * bn + q] + pr->beta * cin;
+            if (pr->out_dtype == OR_OUT_F32) ((float *)pr->Cout)[g] = (float)v;
+            else ((uint16_t *)pr->Cout)[g] = double_to_bf16(v);
+        }
+    free(P); free(Ac); free(Br); free(Rr); free(Rc); free(na); free(nb); free(tr); free(tc); free(Sc);
+    return OR_OK;
+}
+
 int oracle_ftgemm(oracle_problem_t *pr) {
     if (!pr || pr->M < 1 || pr->N < 1 || pr->K < 1 || !pr->A || !pr->B || !pr->Cout ||
         pr->tile_m < 1 || pr->tile_n < 1 || pr->bk < 1 || !pr->counts ||
@@ -459,7 +630,8 @@ int oracle_ftgemm(oracle_problem_t *pr) {
     int err = OR_OK;
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t t = 0; t < tm * tn; ++t) {
-        int e = run_tile(pr, t / tn, t % tn);
+        int e = (pr->ks > 0 && pr->ft_level != OR_FT_OFF) ? run_tile_intervals(pr, t / tn, t % tn)
+                                                            : run_tile(pr, t / tn, t % tn);
         if (e) {
 #pragma omp critical
             err = e;

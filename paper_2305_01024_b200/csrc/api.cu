@@ -233,11 +233,15 @@ int ftgemm_encode(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int
     return FTGEMM_OK;
 }
 
-int ftgemm_run(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const void* A, int64_t lda,
-               const void* B, int64_t ldb, float beta, void* C, int64_t ldc, const void* enc_ws, int ft_level,
-               const ftgemm_inject_t* inj, int32_t n_inj, void* report_ws, void* stream) {
+static int run_impl(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const void* A, int64_t lda,
+                    const void* B, int64_t ldb, float beta, void* C, int64_t ldc, const void* enc_ws, int ft_level,
+                    int64_t ks, const ftgemm_inject_t* inj, int32_t n_inj, void* report_ws, void* stream) {
     int e = check_dims(dtype, M, N, K);
     if (e) return e;
+    if (ks < 0) return fail(FTGEMM_ERR_INVALID_VALUE, "ks must be >= 0");
+    if (ks > 0 && dtype == FTGEMM_F32_SIMT) return fail(FTGEMM_ERR_UNSUPPORTED, "online-interval mode: tensor-core dtypes");
+    if (ks > 0 && (ft_level == FTGEMM_FT_OFF || ft_level == FTGEMM_FT_DETECT_ROWS))
+        return fail(FTGEMM_ERR_INVALID_VALUE, "online-interval mode needs ft_level DETECT or CORRECT");
     if (!A || !B || !C) return fail(FTGEMM_ERR_INVALID_VALUE, "null A, B or C");
     if (lda < K || ldb < N || ldc < N) return fail(FTGEMM_ERR_INVALID_VALUE, "leading dimension too small");
     if (ft_level < FTGEMM_FT_OFF || ft_level > FTGEMM_FT_DETECT_ROWS) return fail(FTGEMM_ERR_INVALID_VALUE, "bad ft_level");
@@ -252,6 +256,7 @@ int ftgemm_run(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const vo
 
     ftgemm_plan_t p;
     fill_plan(dtype, M, N, K, &p);
+    if (ks > 0 && ks % p.bk) return fail(FTGEMM_ERR_INVALID_VALUE, "ks must be a multiple of plan.bk (%d)", p.bk);
     const bool ft = ft_level != FTGEMM_FT_OFF;
     const Geometry g = geometry(p, K);
     const EncLayout L = enc_layout(g, M, N);
@@ -347,6 +352,7 @@ int ftgemm_run(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const vo
         a.num_units = a.units_m * a.tiles_n;
         a.group = tc_group(a.units_m, p.cta_group);
         a.ft_level = ft_level; a.alpha = alpha; a.beta = beta; a.C = C; a.ldc = ldc;
+        a.ks_kb = ks > 0 ? (int)std::min<int64_t>(ks / p.bk, num_kb) : 0;
         if (ft) {
             a.Y = enc + L.y; a.kp = g.kp;
             a.rownorm = (const float*)(enc + L.rownorm); a.colnorm = (const float*)(enc + L.colnorm);
@@ -363,6 +369,21 @@ int ftgemm_run(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const vo
     if (ce != cudaSuccess) return fail_cuda(ce, "kernel launch");
     g_err.clear();
     return FTGEMM_OK;
+}
+
+int ftgemm_run(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const void* A, int64_t lda,
+               const void* B, int64_t ldb, float beta, void* C, int64_t ldc, const void* enc_ws, int ft_level,
+               const ftgemm_inject_t* inj, int32_t n_inj, void* report_ws, void* stream) {
+    return run_impl(dtype, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, enc_ws, ft_level, 0, inj, n_inj, report_ws,
+                    stream);
+}
+
+int ftgemm_run_online(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const void* A, int64_t lda,
+                      const void* B, int64_t ldb, float beta, void* C, int64_t ldc, const void* enc_ws, int ft_level,
+                      int64_t ks, const ftgemm_inject_t* inj, int32_t n_inj, void* report_ws, void* stream) {
+    if (ks < 1) return fail(FTGEMM_ERR_INVALID_VALUE, "ks must be >= 1");
+    return run_impl(dtype, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, enc_ws, ft_level, ks, inj, n_inj, report_ws,
+                    stream);
 }
 
 int ftgemm_nonfused_workspace(int dtype, int64_t M, int64_t N, int64_t K, int64_t* bytes) {

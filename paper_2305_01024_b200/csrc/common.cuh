@@ -40,6 +40,7 @@ struct TcArgs {
     int units_m, num_units;   // work units: CG check tiles stacked in M (CG = CTAs per MMA)
     int group;            // M-units per schedule group (tile_coords)
     int ft_level;
+    int ks_kb;            // > 0: verify after every ks_kb k-blocks too (online-interval mode)
     float alpha, beta;
     void* C; int64_t ldc;
     const void* Y; int kp;

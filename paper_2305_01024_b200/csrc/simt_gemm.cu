@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(256, 2) simt_ftgemm_kernel(const SimtArgs a) {
                     e.row = pstar >= 0 ? (int64_t)(r0 + pstar) : -1;
                     e.col = qstar >= 0 ? (int64_t)(c0 + qstar) : -1;
                     e.tile_m = ti; e.tile_n = tj; e.kind = kind;
-                    e.n_rows = nr; e.n_cols = kind == FTGEMM_EV_DETECTED ? 0 : nc; e.reserved = 0;
+                    e.n_rows = nr; e.n_cols = kind == FTGEMM_EV_DETECTED ? 0 : nc; e.k_checked = a.K;
                     e.resid_row = pstar >= 0 ? rres[pstar] : 0.0f;
                     e.resid_col = qstar >= 0 ? cres[qstar] : 0.0f;
                     e.tau_row = pstar >= 0 ? rtau[pstar] : 0.0f;

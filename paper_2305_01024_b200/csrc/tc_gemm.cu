@@ -251,8 +251,10 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         umma<kTF32, CG>(d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
                     }
                     commit(&empty[s]);
-                    if (FT && ii < ie && a.inj[ii].kb == kb) {
-                        // hand the accumulator to the epilogue warps (of both CTAs) for the fault(s)
+                    const bool chk = a.ks_kb > 0 && (kb + 1) % a.ks_kb == 0 && kb + 1 < a.num_kb;
+                    if (FT && ((ii < ie && a.inj[ii].kb == kb) || chk)) {
+                        // hand the accumulator to the epilogue warps (of both CTAs) for the
+                        // fault(s) of this k-block and / or the check closing a K_s step
                         commit(inj_req);
                         mbar_wait(inj_done, injph);
                         injph ^= 1;
@@ -302,51 +304,13 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     if (et + 128 * h < bn) ncol[h] = __ldg(a.colnorm + c0 + et + 128 * h);
             }
 
-            // ---- mid-mainloop fault injection ----
-            if (FT && a.n_inj > 0) {
-                int ii = inj_lower(a.inj, a.n_inj, t);
-                const int ie = inj_lower(a.inj, a.n_inj, t + 1);
-                while (ii < ie) {
-                    const int kb = a.inj[ii].kb;
-                    mbar_wait(inj_req, injph);
-                    injph ^= 1;
-                    tc_fence_after();
-                    for (; ii < ie && a.inj[ii].kb == kb; ++ii) {
-                        const DevInject f = a.inj[ii];
-                        if ((f.target >> 8) != (int)rank) continue;   // fault in the other CTA's check tile
-                        const int tgt = f.target & 0xff;
-                        int trow, tcol;
-                        if (tgt == FTGEMM_TGT_ROW_REF) { trow = f.p; tcol = xoff; }
-                        else if (tgt == FTGEMM_TGT_COL_REF) { trow = Cfg::BMD; tcol = f.q + doff; }
-                        else { trow = f.p; tcol = f.q + doff; }
-                        if ((trow >> 5) == ew) {
-                            const uint32_t addr = tb + lane_off + (uint32_t)tcol;
-                            uint32_t v = tmem_ld1(addr);
-                            if ((int)lane == (trow & 31)) v = apply_fault(v, f);
-                            tmem_st1(addr, v);
-                        }
-                    }
-                    tc_fence_before();
-                    named_bar_sync(1, 128);
-                    if (et == 0) arrive_leader(inj_done);
-                }
-            }
-
-            mbar_wait(&tm_full[acc], accph);
-            tc_fence_after();
-            if (!has_rows) {                                   // padding half of the last pair row
-                __syncwarp();
-                if (lane == 0) arrive_leader(&tm_empty[acc]);
-                continue;
-            }
-
-            int kind = 0, pstar = -1, qstar = -1;
-            float corr = 0.0f;
-#ifdef FTGEMM_EXP_NO_VERIFY
-            if (false) {
-#else
-            if (FT) {
-#endif
+            // Verification of the accumulator in TMEM:
+            // row sums, column sums, residuals against the carried references,
+            // threshold (sqrtk = sqrt of the K accumulated so far), decision and
+            // the corrected value (applied by the caller).  Called once at the
+            // end of K, and after every K_s step in online-interval mode.
+            auto verify = [&](float sqrtk, int kchk, int& kind, int& pstar, int& qstar, float& corr) {
+                kind = 0; pstar = -1; qstar = -1; corr = 0.0f;
                 // ---- pass 1: row sums, row refs, column partial sums ----
                 // previous tile's stores have read the staging area (aliased below) and
                 // every reader of sflag / residual arrays is done
@@ -358,23 +322,6 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 const bool all_rows = ew < 3 && bm >= (ew + 1) * 32;   // warp-uniform: no row of this warp masked
                 float* tbuf = reinterpret_cast<float*>(stg + 12288) + ew * (32 * 36);   // 32 x 36 transpose buffer
                 float srow = 0.0f, rref = 0.0f;
-#if defined(FTGEMM_EXP_PASS1_LDONLY)
-                if (true) {
-                    float acc8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-                    for (int c = 0; c < Cfg::NCHUNK; ++c) {
-                        float v[32];
-                        tmem_ld32(tb + lane_off + c * 32, v);
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) acc8[i & 7] += v[i];
-                        colsum[ew * BN + c * 32 + lane] = 0.f;
-                        if (ew == 0 && lane < 3) refrow[lane * BN + c * 32] = 0.f;
-                    }
-                    if (ew == 0) for (int i = lane; i < 3 * BN; i += 32) refrow[i] = 0.f;
-                    srow = ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
-                    rref = srow;
-                } else
-#endif
                 {
                     // 64 columns per TMEM load; row sums in 4 independent chains
                     float rs[4] = {0.f, 0.f, 0.f, 0.f};
@@ -429,7 +376,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 // ---- row residuals ----
                 if (rvalid) {
                     const float r = srow - rref;
-                    const float tr = a.tau_u * (a.tau_l1 * a.sqrtK * fabsf(rref) + a.tau_l2 * nrow * nbr);
+                    const float tr = a.tau_u * (a.tau_l1 * sqrtk * fabsf(rref) + a.tau_l2 * nrow * nbr);
                     rres[rloc] = r; rtau[rloc] = tr;
                     if (!(fabsf(r) <= tr)) { atomicAdd(&sflag[0], 1); atomicMin(&sflag[2], rloc); }
                 }
@@ -441,7 +388,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         const float sc = (colsum[col] + colsum[BN + col]) + (colsum[2 * BN + col] + colsum[3 * BN + col]);
                         const float rc = (refrow[col] + refrow[BN + col]) + refrow[2 * BN + col];
                         const float c = sc - rc;
-                        const float tc = a.tau_u * (a.tau_l1 * a.sqrtK * fabsf(rc) + a.tau_l2 * nac * ncol[h]);
+                        const float tc = a.tau_u * (a.tau_l1 * sqrtk * fabsf(rc) + a.tau_l2 * nac * ncol[h]);
                         cres[col] = c; ctau[col] = tc;
                         if (!(fabsf(c) <= tc)) { atomicAdd(&sflag[1], 1); atomicMin(&sflag[3], col); }
                     }
@@ -501,7 +448,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                             e.row = pstar >= 0 ? (int64_t)(r0 + pstar) : -1;
                             e.col = qstar >= 0 ? (int64_t)(c0 + qstar) : -1;
                             e.tile_m = ti; e.tile_n = tj; e.kind = kind;
-                            e.n_rows = nr; e.n_cols = kind == FTGEMM_EV_DETECTED ? 0 : nc; e.reserved = 0;
+                            e.n_rows = nr; e.n_cols = kind == FTGEMM_EV_DETECTED ? 0 : nc; e.k_checked = kchk;
                             e.resid_row = pstar >= 0 ? rres[pstar] : 0.0f;
                             e.resid_col = qstar >= 0 ? cres[qstar] : 0.0f;
                             e.tau_row = pstar >= 0 ? rtau[pstar] : 0.0f;
@@ -513,7 +460,75 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 }
                 // the verification arrays alias the staging buffers that pass 2 writes
                 named_bar_sync(1, 128);
+            };
+
+            // ---- mid-mainloop hand-offs: fault injection and, in
+            // online-interval mode, verification after every K_s step
+            // with the correction written back to TMEM ----
+            if (FT && (a.n_inj > 0 || a.ks_kb > 0)) {
+                int ii = a.n_inj > 0 ? inj_lower(a.inj, a.n_inj, t) : 0;
+                const int ie = a.n_inj > 0 ? inj_lower(a.inj, a.n_inj, t + 1) : 0;
+                int next_chk = a.ks_kb > 0 ? a.ks_kb - 1 : 0x7fffffff;     // k-block closing the next step
+                for (;;) {
+                    const int kb_f = ii < ie ? a.inj[ii].kb : 0x7fffffff;
+                    const int kb_c = next_chk < a.num_kb - 1 ? next_chk : 0x7fffffff;
+                    const int kb = min(kb_f, kb_c);
+                    if (kb == 0x7fffffff) break;
+                    mbar_wait(inj_req, injph);
+                    injph ^= 1;
+                    tc_fence_after();
+                    for (; ii < ie && a.inj[ii].kb == kb; ++ii) {
+                        const DevInject f = a.inj[ii];
+                        if ((f.target >> 8) != (int)rank) continue;   // fault in the other CTA's check tile
+                        const int tgt = f.target & 0xff;
+                        int trow, tcol;
+                        if (tgt == FTGEMM_TGT_ROW_REF) { trow = f.p; tcol = xoff; }
+                        else if (tgt == FTGEMM_TGT_COL_REF) { trow = Cfg::BMD; tcol = f.q + doff; }
+                        else { trow = f.p; tcol = f.q + doff; }
+                        if ((trow >> 5) == ew) {
+                            const uint32_t addr = tb + lane_off + (uint32_t)tcol;
+                            uint32_t v = tmem_ld1(addr);
+                            if ((int)lane == (trow & 31)) v = apply_fault(v, f);
+                            tmem_st1(addr, v);
+                        }
+                    }
+                    if (kb == kb_c) {
+                        next_chk += a.ks_kb;
+                        if (has_rows) {
+                            tc_fence_before();
+                            named_bar_sync(1, 128);             // faults of this k-block are in TMEM
+                            tc_fence_after();
+                            const int kdone = min(a.K, (kb + 1) * Cfg::BK);
+                            int k2 = 0, p2 = -1, q2 = -1;
+                            float c2 = 0.0f;
+                            verify(sqrtf((float)kdone), kdone, k2, p2, q2, c2);
+                            if (k2 == FTGEMM_EV_CORRECTED && (p2 >> 5) == ew) {
+                                const uint32_t addr = tb + lane_off + (uint32_t)(q2 + doff);
+                                uint32_t v = tmem_ld1(addr);
+                                if (rloc == p2) v = __float_as_uint(c2);
+                                tmem_st1(addr, v);
+                            }
+                        }
+                    }
+                    tc_fence_before();
+                    named_bar_sync(1, 128);
+                    if (et == 0) arrive_leader(inj_done);
+                }
             }
+
+            mbar_wait(&tm_full[acc], accph);
+            tc_fence_after();
+            if (!has_rows) {                                   // padding half of the last pair row
+                __syncwarp();
+                if (lane == 0) arrive_leader(&tm_empty[acc]);
+                continue;
+            }
+
+            int kind = 0, pstar = -1, qstar = -1;
+            float corr = 0.0f;
+#ifndef FTGEMM_EXP_NO_VERIFY
+            if (FT) verify(a.sqrtK, a.K, kind, pstar, qstar, corr);
+#endif
 
             // ---- pass 2: alpha/beta, SWIZZLE_128B staging, TMA stores ----
             // Output in groups of GW columns (one 128-byte box row per thread).

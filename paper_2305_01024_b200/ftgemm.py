@@ -35,7 +35,7 @@ class Inject(C.Structure):
 
 class Event(C.Structure):
     _fields_ = [("row", C.c_int64), ("col", C.c_int64), ("tile_m", C.c_int32), ("tile_n", C.c_int32),
-                ("kind", C.c_int32), ("n_rows", C.c_int32), ("n_cols", C.c_int32), ("reserved", C.c_int32),
+                ("kind", C.c_int32), ("n_rows", C.c_int32), ("n_cols", C.c_int32), ("k_checked", C.c_int32),
                 ("resid_row", C.c_float), ("resid_col", C.c_float), ("tau_row", C.c_float), ("tau_col", C.c_float)]
 
 
@@ -59,7 +59,7 @@ class Cost(C.Structure):
                 ("online_expected_runs", C.c_double), ("offline_expected_runs", C.c_double)]
 
 
-SYMBOLS = ("ftgemm_plan", "ftgemm_encode", "ftgemm_run", "ftgemm_run_offline", "ftgemm_cost_model",
+SYMBOLS = ("ftgemm_plan", "ftgemm_encode", "ftgemm_run", "ftgemm_run_online", "ftgemm_run_offline", "ftgemm_cost_model",
            "ftgemm_nonfused_workspace", "ftgemm_run_nonfused",
            "ftgemm_report", "ftgemm_report_reset", "ftgemm_last_error", "ftgemm_version", "ftgemm_device_arch")
 
@@ -79,6 +79,8 @@ def lib():
         L.ftgemm_encode.argtypes = [C.c_int, i64, i64, i64, vp, i64, vp, i64, vp, C.c_int, vp]
         L.ftgemm_run.argtypes = [C.c_int, i64, i64, i64, C.c_float, vp, i64, vp, i64, C.c_float, vp, i64,
                                  vp, C.c_int, vp, i32, vp, vp]
+        L.ftgemm_run_online.argtypes = [C.c_int, i64, i64, i64, C.c_float, vp, i64, vp, i64, C.c_float, vp, i64,
+                                        vp, C.c_int, i64, vp, i32, vp, vp]
         L.ftgemm_run_offline.argtypes = [C.c_int, i64, i64, i64, C.c_float, vp, i64, vp, i64, C.c_float, vp, i64,
                                          vp, vp, vp, vp, i32, i32, vp, vp, vp]
         L.ftgemm_cost_model.argtypes = [C.c_double, i64, C.POINTER(Cost)]
@@ -244,6 +246,19 @@ def cost_model(gamma0: float, tiles: int) -> dict:
     return {f: getattr(c, f) for f, _ in Cost._fields_}
 
 
+def run_online(dtype, A: torch.Tensor, B: torch.Tensor, C_: torch.Tensor, *, ks: int, alpha: float = 1.0,
+               beta: float = 0.0, enc_ws: torch.Tensor, ft_level: int = FT_CORRECT, injections=(),
+               report_ws: torch.Tensor, stream=None):
+    """Online ABFT verified after every ks of K."""
+    M, K = A.shape
+    N = B.shape[1]
+    arr, n = _inj_array(injections)
+    _check(lib().ftgemm_run_online(_dt(dtype), M, N, K, alpha, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0),
+                                   beta, C_.data_ptr(), C_.stride(0), enc_ws.data_ptr(), ft_level, ks,
+                                   C.cast(arr, C.c_void_p) if arr is not None else None, n, report_ws.data_ptr(),
+                                   _stream(stream)), "ftgemm_run_online")
+
+
 def report(report_ws: torch.Tensor, max_events: int = 4096, stream=None):
     cnt = Counts()
     evs = (Event * max(1, max_events))()
@@ -254,7 +269,7 @@ def report(report_ws: torch.Tensor, max_events: int = 4096, stream=None):
     for i in range(min(counts["events"], max_events)):
         e = evs[i]
         out.append(dict(row=e.row, col=e.col, tile_m=e.tile_m, tile_n=e.tile_n, kind=e.kind, n_rows=e.n_rows,
-                        n_cols=e.n_cols, resid_row=e.resid_row, resid_col=e.resid_col, tau_row=e.tau_row,
+                        n_cols=e.n_cols, k_checked=e.k_checked, resid_row=e.resid_row, resid_col=e.resid_col, tau_row=e.tau_row,
                         tau_col=e.tau_col))
     out.sort(key=lambda e: (e["tile_m"], e["tile_n"], e["kind"], e["row"], e["col"]))
     return counts, out
@@ -282,6 +297,10 @@ class FTGemm:
     def run(self, A, B, C_, *, alpha=1.0, beta=0.0, ft_level=FT_CORRECT, injections=(), stream=None):
         run(self.dtype, A, B, C_, alpha=alpha, beta=beta, enc_ws=self.enc_ws, ft_level=ft_level,
             injections=injections, report_ws=self.report_ws, stream=stream)
+
+    def run_online(self, A, B, C_, *, ks, alpha=1.0, beta=0.0, ft_level=FT_CORRECT, injections=(), stream=None):
+        run_online(self.dtype, A, B, C_, ks=ks, alpha=alpha, beta=beta, enc_ws=self.enc_ws, ft_level=ft_level,
+                   injections=injections, report_ws=self.report_ws, stream=stream)
 
     def run_offline(self, A, B, C_, *, alpha=1.0, beta=0.0, injections=(), inj_run=None, max_runs=4,
                     c_backup=None, stream=None):

@@ -215,6 +215,60 @@ def test_false_positive_sweep(dtype):
         assert c.counts["tiles_checked"] == c.plan.tiles_m * c.plan.tiles_n
 
 
+# ------------------------------------------ online verification every K_s ---
+
+@pytest.mark.parametrize("cg", [1, 2])
+@pytest.mark.parametrize("dtype", ["tf32", "bf16"])
+def test_online_interval_parity(dtype, cg, monkeypatch):
+    """ftgemm_run_online: the fused kernel verifies
+    after every K_s step and corrects in TMEM.  Several faults per tile in
+    different steps are all corrected; a double fault within one step is
+    uncorrectable at that step and after; a reference fault is reported at
+    every later check; events (with k_checked) and counts as in the oracle."""
+    import torch
+    monkeypatch.setenv("FTGEMM_CG", str(cg))
+    F = ftmod()
+    M, N, K = 845, 600, 1024
+    A, B, Cin = synth.problem(M, N, K, dtype=odt(dtype))
+    plan = F.plan(dtype, M, N, K)
+    tm, tn = plan.check_tile_m, plan.check_tile_n
+    ks = 256
+    inj = [(5, 7, 40, 0, oracle.INJ_ADD, 0, 1000.0), (5, 90, 300, 0, oracle.INJ_ADD, 0, -800.0),      # tile (0,0)
+           (60, 7, 700, 0, oracle.INJ_ADD, 0, 900.0), (6, 7, 1000, 0, oracle.INJ_ADD, 0, 1200.0),
+           (tm + 3, tn + 4, 100, 30, oracle.INJ_FLIP, 0, 0.0), (tm + 3, tn + 40, 600, 0, oracle.INJ_ADD, 0, 500.0),
+           (3 * tm + 1, 2, 520, 0, oracle.INJ_ADD, 0, 700.0), (3 * tm + 8, 9, 600, 0, oracle.INJ_ADD, 0, -700.0),  # same step
+           (4 * tm + 2, tn + 1, 300, 0, oracle.INJ_ADD, oracle.TGT_ROW_REF, 600.0),
+           (6 * tm + 1, 3, 10, 0, oracle.INJ_ADD, 0, 900.0), (6 * tm + 2, 4, 900, 0, oracle.INJ_ADD, 0, 900.0)]
+    g = F.FTGemm(dtype, M, N, K)
+    assert g.plan.cta_group == cg
+    Ad, Bd = synth.to_torch(A, odt(dtype)).cuda(), synth.to_torch(B, odt(dtype)).cuda()
+    Cd = synth.to_torch(Cin, odt(dtype)).cuda()
+    g.encode(Ad, Bd)
+    g.run_online(Ad, Bd, Cd, ks=ks, alpha=1.5, beta=-0.5, injections=inj)
+    torch.cuda.synchronize()
+    counts, events = g.report()
+    ref = oracle.ftgemm(A, B, Cin, alpha=1.5, beta=-0.5, out=odt(dtype), tile_m=tm, tile_n=tn, bk=plan.bk,
+                        u_acc=plan.u_acc, lambda1=plan.lambda1, lambda2=plan.lambda2, injections=inj, ks=ks)
+    keys = ("tiles_checked", "tiles_detected", "corrected", "checksum_only", "uncorrectable", "located", "events")
+    assert all(int(counts[k]) == int(ref.counts[k]) for k in keys), (counts, ref.counts)
+    ek = lambda evs: sorted((e["tile_m"], e["tile_n"], e["kind"], e["row"], e["col"], e["n_rows"], e["n_cols"],
+                             e["k_checked"]) for e in evs)
+    assert ek(events) == ek(ref.events)
+    assert counts["corrected"] >= 7 and counts["tiles_checked"] == plan.tiles_m * plan.tiles_n * 4
+    bad = np.zeros((M, N), bool)
+    for e in ref.events:
+        if e["kind"] == oracle.EV_UNCORRECTABLE:
+            bad[e["tile_m"] * tm:(e["tile_m"] + 1) * tm, e["tile_n"] * tn:(e["tile_n"] + 1) * tn] = True
+    assert frob(Cd.float().cpu().numpy(), ref.C, ~bad) < TOL[dtype]
+    # a step >= K is the end-of-K check; DETECT_ROWS / SIMT are refused
+    g.reset()
+    g.run_online(Ad, Bd, Cd, ks=((K + plan.bk - 1) // plan.bk) * plan.bk, injections=inj[:1])
+    c2, _ = g.report()
+    assert c2["corrected"] == 1 and c2["tiles_checked"] == plan.tiles_m * plan.tiles_n
+    with pytest.raises(F.FtgemmError):
+        g.run_online(Ad, Bd, Cd, ks=plan.bk + 1)
+
+
 # ------------------------------------------------ non-fused baseline -------
 
 @pytest.mark.parametrize("dtype", ["f32_simt", "bf16"])

@@ -277,6 +277,49 @@ def test_detect_rows_level_offline(oracle_lib):
     assert r.counts["tiles_detected"] == 1 and r.events[0]["n_rows"] == 2 and r.events[0]["row"] == 1
 
 
+def test_online_interval_mode(oracle_lib):
+    """Per-K_s online verification (PAPER.md:170-173 / :515, R17).
+    Integer inputs keep every partial sum exact, so the outcome is decided by
+    the algorithm alone: two faults on one row in different steps are both
+    corrected (C exact) where the end-of-K check must give up (1 row, 2 columns
+    -> uncorrectable); two faults in one step stay uncorrectable at that check
+    and at every later one; a reference fault persists (checksum_only at each
+    later check); every step is a check; ks >= K is the end-of-K check."""
+    A, B = ints(61, 32, 96), ints(62, 96, 32)
+    exact = (A.astype(np.int64) @ B.astype(np.int64)).astype(np.float64)
+    kw = dict(tile_m=16, tile_n=16, bk=8)
+    two = [(3, 4, 5, 0, oracle.INJ_ADD, 0, 6.0), (3, 9, 70, 0, oracle.INJ_ADD, 0, -9.0)]    # steps 1 and 3 (ks=32)
+    r = oracle.ftgemm(A, B, ks=32, injections=two, **kw)
+    assert r.counts["corrected"] == 2 and r.counts["tiles_checked"] == 4 * 3
+    assert sorted(e["k_checked"] for e in r.events) == [32, 96]
+    assert np.array_equal(r.C.astype(np.float64), exact)
+    r0 = oracle.ftgemm(A, B, injections=two, **kw)
+    assert r0.counts["uncorrectable"] == 1 and r0.counts["corrected"] == 0 and r0.events[0]["k_checked"] == 96
+    same = [(3, 4, 40, 0, oracle.INJ_ADD, 0, 6.0), (7, 9, 50, 0, oracle.INJ_ADD, 0, -9.0)]  # both in step 2
+    r = oracle.ftgemm(A, B, ks=32, injections=same, **kw)
+    assert r.counts["uncorrectable"] == 2 and [e["k_checked"] for e in r.events] == [64, 96]
+    ref = [(18, 20, 10, 0, oracle.INJ_ADD, oracle.TGT_ROW_REF, 50.0)]
+    r = oracle.ftgemm(A, B, ks=32, injections=ref, **kw)
+    assert r.counts["checksum_only"] == 3 and np.array_equal(r.C.astype(np.float64), exact)
+    for ks in (96, 200):
+        a = oracle.ftgemm(A, B, ks=ks, injections=two[:1], **kw)
+        b = oracle.ftgemm(A, B, injections=two[:1], **kw)
+        assert a.counts == b.counts and np.array_equal(a.C, b.C)
+    # ragged last step (K = 96 = 40 + 40 + 16) and a fault in it
+    r = oracle.ftgemm(A, B, ks=40, injections=[(30, 31, 90, 0, oracle.INJ_ADD, 0, 3.0)], **kw)
+    assert r.counts["tiles_checked"] == 12 and r.events[0]["k_checked"] == 96 and r.counts["corrected"] == 1
+
+
+def test_online_interval_no_false_positives(oracle_lib):
+    """Fault-free signed data checked after every step of 64: every partial
+    check stays below tau with margin (the threshold of R17 scales with the
+    partial reference and sqrt(k))."""
+    A = synth.matrix(71, 128, 1024)
+    B = synth.matrix(72, 1024, 128)
+    r = oracle.ftgemm(A, B, tile_m=64, tile_n=64, bk=64, ks=64, u_acc=2.0 ** -23, lambda1=8.0, lambda2=16.0)
+    assert r.counts["tiles_checked"] == 4 * 16 and r.counts["tiles_detected"] == 0
+
+
 def test_cost_model_online_vs_offline():
     """gamma = 1-(1-gamma0)^tiles, offline expected executions
     (1-gamma)/(1-2gamma).  Pinned by (a) the survey's evaluation for gamma0 = 1/256
