@@ -290,6 +290,9 @@ def run_ours(args):
             # the paper's comparison scheme (Ding 2011): cuBLAS GEMMs + separate verification
             "nonfused_step": lambda: (g.encode(A, B, which=3 | 4), g.run_nonfused(A, B, C, ft_level=F.FT_CORRECT)),
             "nonfused_run": lambda: g.run_nonfused(A, B, C, ft_level=F.FT_CORRECT),
+            # online verification after every K_s = 256 step: 32 checks per tile
+            "online_ks256_run": lambda: g.run_online(A, B, C, ks=256),
+            "online_ks2048_run": lambda: g.run_online(A, B, C, ks=2048),
         }
         samples = {k: [] for k in configs}
         rate_samples = {str(int(r)): [] for r in SWEEP_RATES}
@@ -365,6 +368,7 @@ def run_ours(args):
         g.encode(A, B)                               # restore the fused path's encoded operand
         extra = {
             "nonfused_step_ms": med["nonfused_step"], "nonfused_run_ms": med["nonfused_run"],
+            "online_ks256_run_ms": med["online_ks256_run"], "online_ks2048_run_ms": med["online_ks2048_run"],
             "fused_speedup_vs_nonfused_pct": 100.0 * (med["nonfused_step"] - med["ft_step"]) / med["ft_step"],
             "detect_rows_run_ms": t_rows,
             "detect_rows_overhead_vs_ft_off_pct": 100.0 * (t_rows - med["ft_off"]) / med["ft_off"],
