@@ -23,7 +23,20 @@
 
 namespace ftg {
 
-constexpr int SB = 128, SK = 8;
+constexpr int SB = 128, SK = 8, NST = 4;   // tile, k-block, smem pipeline stages
+
+// cp.async with zero fill: src_bytes < cp bytes fills the rest of dst with 0
+__device__ __forceinline__ void cp_async4(void* dst, const void* src, int src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;"
+                 :: "r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
+                 :: "r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
 
 __device__ __forceinline__ int simt_inj_lower(const DevInject* inj, int n, int t) {
     int lo = 0, hi = n;
@@ -39,11 +52,14 @@ __device__ __forceinline__ float simt_fault(float x, const DevInject& f) {
     return __uint_as_float(__float_as_uint(x) ^ (1u << (f.bit & 31)));
 }
 
+#ifndef FTGEMM_SIMT_MINB
+#define FTGEMM_SIMT_MINB 2
+#endif
 template <bool FT>
-__global__ void __launch_bounds__(256, 2) simt_ftgemm_kernel(const SimtArgs a) {
-    __shared__ __align__(16) float As[2][SK][SB];      // A tile, k-major (transposed)
-    __shared__ __align__(16) float Bs[2][SK][SB];
-    __shared__ float acs[2][SK], brs[2][SK];           // e^T A_i, B_j e for the k-block
+__global__ void __launch_bounds__(256, FTGEMM_SIMT_MINB) simt_ftgemm_kernel(const SimtArgs a) {
+    __shared__ __align__(16) float As[NST][SB][SK];    // A tile, row-major (k contiguous)
+    __shared__ __align__(16) float Bs[NST][SK][SB];
+    __shared__ __align__(16) float acs[NST][SK], brs[NST][SK];   // e^T A_i, B_j e for the k-block
     __shared__ float red_col[8][SB];                   // column partial sums per warp
     __shared__ float srow_s[SB], rref_s[SB], cref_s[SB], rres[SB], rtau[SB], cres[SB], ctau[SB];
     __shared__ int sflag[5];
@@ -79,77 +95,81 @@ __global__ void __launch_bounds__(256, 2) simt_ftgemm_kernel(const SimtArgs a) {
         s_ninj = n;
     }
 
-    // global -> register staging for one k-block
+    // global -> shared copies of one k-block (16-byte cp.async, NST-stage ring,
+    // out-of-range elements zero-filled), issued NST-1 k-blocks ahead
     const int a_row = tid >> 1, a_k = (tid & 1) * 4;     // 128 rows x 8 k
     const int b_k = tid >> 5, b_col = (tid & 31) * 4;    // 8 k x 128 cols
-    float4 ra, rb;
-    float rchk = 0.0f;
-    auto load_regs = [&](int kb) {
+    auto issue = [&](int kb, int s) {
         const int k0 = kb * SK;
         const int gr = r0 + a_row, gk = k0 + a_k;
-        if (gr < a.M && gk + 3 < a.K) {
-            ra = __ldg(reinterpret_cast<const float4*>(a.A + (int64_t)gr * a.lda + gk));
-        } else {
-            float t4[4];
-            for (int e = 0; e < 4; ++e) t4[e] = (gr < a.M && gk + e < a.K) ? __ldg(a.A + (int64_t)gr * a.lda + gk + e) : 0.0f;
-            ra = make_float4(t4[0], t4[1], t4[2], t4[3]);
-        }
+        const int na = gr < a.M ? max(0, min(4, a.K - gk)) : 0;
+        cp_async16(&As[s][a_row][a_k], a.A + (int64_t)min(gr, a.M - 1) * a.lda + (na ? gk : 0), 4 * na);
         const int bk = k0 + b_k, gc = c0 + b_col;
-        if (bk < a.K && gc + 3 < a.N) {
-            rb = __ldg(reinterpret_cast<const float4*>(a.B + (int64_t)bk * a.ldb + gc));
-        } else {
-            float t4[4];
-            for (int e = 0; e < 4; ++e) t4[e] = (bk < a.K && gc + e < a.N) ? __ldg(a.B + (int64_t)bk * a.ldb + gc + e) : 0.0f;
-            rb = make_float4(t4[0], t4[1], t4[2], t4[3]);
-        }
+        const int nv = bk < a.K ? max(0, min(4, a.N - gc)) : 0;
+        cp_async16(&Bs[s][b_k][b_col], a.B + (int64_t)min(bk, a.K - 1) * a.ldb + (nv ? gc : 0), 4 * nv);
         if (FT) {
-            if (tid < SK) rchk = __ldg(a.Ac + (int64_t)ti * a.kp + k0 + tid);
-            else if (tid < 2 * SK) rchk = __ldg(a.Br + (int64_t)tj * a.kp + k0 + tid - SK);
-        }
-    };
-    auto store_regs = [&](int buf) {
-        As[buf][a_k + 0][a_row] = ra.x;
-        As[buf][a_k + 1][a_row] = ra.y;
-        As[buf][a_k + 2][a_row] = ra.z;
-        As[buf][a_k + 3][a_row] = ra.w;
-        *reinterpret_cast<float4*>(&Bs[buf][b_k][b_col]) = rb;
-        if (FT) {
-            if (tid < SK) acs[buf][tid] = rchk;
-            else if (tid < 2 * SK) brs[buf][tid - SK] = rchk;
+            if (tid < SK) cp_async4(&acs[s][tid], a.Ac + (int64_t)ti * a.kp + k0 + tid, 4);
+            else if (tid < 2 * SK) cp_async4(&brs[s][tid - SK], a.Br + (int64_t)tj * a.kp + k0 + tid - SK, 4);
         }
     };
 
-    float acc[8][8];
+    // 8 x 8 accumulators as column pairs: one FFMA2 (two independent,
+    // individually rounded fmaf -- the same arithmetic as fmaf per element)
+    // updates two outputs of a row per issue slot
+    float2 acc2[8][4];
+#define ACC(i, j) (((j) & 1) ? acc2[i][(j) >> 1].y : acc2[i][(j) >> 1].x)
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+        for (int j = 0; j < 4; ++j) acc2[i][j] = make_float2(0.0f, 0.0f);
     float ref = 0.0f;   // row ref (tid < 128) or col ref (tid >= 128)
 
-    load_regs(0);
-    store_regs(0);
-    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < NST - 1; ++s) {
+        if (s < a.num_kb) issue(s, s);
+        cp_async_commit();
+    }
+    __syncthreads();                                   // s_ninj / sinj visible
     int ninj = FT ? s_ninj : 0;
     int next_inj = 0;
 
     for (int kb = 0; kb < a.num_kb; ++kb) {
-        const int buf = kb & 1;
-        if (kb + 1 < a.num_kb) load_regs(kb + 1);
+        const int buf = kb % NST;
+        cp_async_wait<NST - 2>();                      // this thread's copies of k-block kb landed
+        __syncthreads();                               // everyone's, and stage (kb-1) % NST is free
+        if (kb + NST - 1 < a.num_kb) issue(kb + NST - 1, (kb + NST - 1) % NST);
+        cp_async_commit();
+        // two halves of 4 k: the thread's 8 rows x 4 k of A (one 16-byte load
+        // per row), then per k the 8 columns of B; every output still sees
+        // one fmaf per k in ascending k
 #pragma unroll
-        for (int k = 0; k < SK; ++k) {
-            const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][k][ty * 4]);
-            const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][k][64 + ty * 4]);
-            const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][k][tx * 4]);
-            const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][k][64 + tx * 4]);
-            const float af[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-            const float bf[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+        for (int kh = 0; kh < SK; kh += 4) {
+            float4 ar[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i)
+                ar[i] = *reinterpret_cast<const float4*>(&As[buf][(i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4)][kh]);
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(af[i], bf[j], acc[i][j]);
-            if (FT) {
-                if (tid < SB) ref = fmaf(As[buf][k][tid], brs[buf][k], ref);
-                else ref = fmaf(acs[buf][k], Bs[buf][k][tid - SB], ref);
+            for (int k = 0; k < 4; ++k) {
+                const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kh + k][tx * 4]);
+                const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][kh + k][64 + tx * 4]);
+                const float2 bf2[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                                       make_float2(b1.z, b1.w)};
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const float av = k == 0 ? ar[i].x : k == 1 ? ar[i].y : k == 2 ? ar[i].z : ar[i].w;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc2[i][j] = __ffma2_rn(make_float2(av, av), bf2[j], acc2[i][j]);
+                }
+            }
+        }
+        if (FT) {
+            // carried references, ascending k, once per k-block (one branch per warp)
+            if (tid < SB) {
+#pragma unroll
+                for (int k = 0; k < SK; ++k) ref = fmaf(As[buf][tid][k], brs[buf][k], ref);
+            } else {
+#pragma unroll
+                for (int k = 0; k < SK; ++k) ref = fmaf(acs[buf][k], Bs[buf][k][tid - SB], ref);
             }
         }
         // fault injection after this k-block, warp-uniform check
@@ -166,7 +186,7 @@ __global__ void __launch_bounds__(256, 2) simt_ftgemm_kernel(const SimtArgs a) {
                         for (int i = 0; i < 8; ++i)
 #pragma unroll
                             for (int j = 0; j < 8; ++j)
-                                if (i == ii && j == jj) acc[i][j] = simt_fault(acc[i][j], f);
+                                if (i == ii && j == jj) ACC(i, j) = simt_fault(ACC(i, j), f);
                     }
                 } else if (f.target == FTGEMM_TGT_ROW_REF) {
                     if (tid == f.p) ref = simt_fault(ref, f);
@@ -176,9 +196,9 @@ __global__ void __launch_bounds__(256, 2) simt_ftgemm_kernel(const SimtArgs a) {
                 ++next_inj;
             }
         }
-        if (kb + 1 < a.num_kb) store_regs(buf ^ 1);
-        __syncthreads();
     }
+    cp_async_wait<0>();
+    __syncthreads();
 
     int kind = 0, pstar = -1, qstar = -1;
     if (FT) {
@@ -189,14 +209,14 @@ __global__ void __launch_bounds__(256, 2) simt_ftgemm_kernel(const SimtArgs a) {
         for (int i = 0; i < 8; ++i) {
             float s = 0.0f;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) s += acc[i][j];
+            for (int j = 0; j < 8; ++j) s += ACC(i, j);
             rs[i] = s;
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             float s = 0.0f;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) s += acc[i][j];
+            for (int i = 0; i < 8; ++i) s += ACC(i, j);
             cs[j] = s;
         }
         // rows: reduce across the 16 tx of the same ty (same warp, lanes xor 1..8)
@@ -273,7 +293,7 @@ __global__ void __launch_bounds__(256, 2) simt_ftgemm_kernel(const SimtArgs a) {
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
                             const int q = (j < 4) ? tx * 4 + j : 64 + tx * 4 + j - 4;
-                            if (q != qstar) part += acc[i][j];
+                            if (q != qstar) part += ACC(i, j);
                         }
                     }
             }
@@ -287,7 +307,7 @@ __global__ void __launch_bounds__(256, 2) simt_ftgemm_kernel(const SimtArgs a) {
                 for (int i = 0; i < 8; ++i)
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
-                        if (i == ii && j == jj) acc[i][j] = val;
+                        if (i == ii && j == jj) ACC(i, j) = val;
             }
         }
         if (tid == 0) {
@@ -335,12 +355,12 @@ __global__ void __launch_bounds__(256, 2) simt_ftgemm_kernel(const SimtArgs a) {
                 if (a.beta != 0.0f) cin = *reinterpret_cast<const float4*>(Cp);
                 const float ci[4] = {cin.x, cin.y, cin.z, cin.w};
 #pragma unroll
-                for (int j = 0; j < 4; ++j) o[j] = fmaf(a.alpha, acc[i][h * 4 + j], a.beta != 0.0f ? a.beta * ci[j] : 0.0f);
+                for (int j = 0; j < 4; ++j) o[j] = fmaf(a.alpha, ACC(i, h * 4 + j), a.beta != 0.0f ? a.beta * ci[j] : 0.0f);
                 *reinterpret_cast<float4*>(Cp) = make_float4(o[0], o[1], o[2], o[3]);
             } else {
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
-                    if (q + j < bn) Cp[j] = fmaf(a.alpha, acc[i][h * 4 + j], a.beta != 0.0f ? a.beta * Cp[j] : 0.0f);
+                    if (q + j < bn) Cp[j] = fmaf(a.alpha, ACC(i, h * 4 + j), a.beta != 0.0f ? a.beta * Cp[j] : 0.0f);
             }
         }
     }

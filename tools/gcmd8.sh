@@ -1,0 +1,13 @@
+#!/bin/bash
+export PYTHONUNBUFFERED=1
+D=gpurun_out/r34; mkdir -p $D
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:simt_ftgemm -s 1 -c 1 -o $D/simt_off python tools/prof_shape.py f32_simt 4096 4096 4096 0 > $D/a.log 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:simt_ftgemm -s 1 -c 1 -o $D/simt_ft python tools/prof_shape.py f32_simt 4096 4096 4096 2 > $D/b.log 2>&1
+timeout 300 ncu --set full --clock-control none -k regex:sgemm\|gemm\|Kernel -s 2 -c 1 -o $D/cublas_sgemm python -c "
+import torch
+torch.backends.cuda.matmul.allow_tf32=False
+a=torch.randn(4096,4096,device='cuda');b=torch.randn(4096,4096,device='cuda')
+for _ in range(4): c=a@b
+torch.cuda.synchronize()
+" > $D/c.log 2>&1
+echo done
