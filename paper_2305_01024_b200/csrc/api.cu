@@ -31,6 +31,7 @@ cudaError_t launch_tc(bool tf32, int bn, bool ft, int cg, const CUtensorMap& mA,
                       const CUtensorMap& mC, const CUtensorMap& mC29, const CUtensorMap& mY, const TcArgs& a,
                       cudaStream_t st);
 cudaError_t launch_simt(bool ft, const SimtArgs& a, cudaStream_t st);
+int simt_bk();
 struct NfInject {
     int64_t row, col;
     int32_t bit, mode, target;
@@ -74,7 +75,7 @@ void fill_plan(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* p) {
     p->max_inject = kMaxInject;
     if (dtype == FTGEMM_F32_SIMT) {
         p->shape_class = FTGEMM_SHAPE_SQUARE;
-        p->bm = 128; p->bn = 128; p->bk = 8;
+        p->bm = 128; p->bn = 128; p->bk = simt_bk();
         p->check_tile_m = 128; p->check_tile_n = 128;
         p->off_tile_m = 128; p->off_tile_n = 128;
         p->stages = 2; p->cta_group = 1;

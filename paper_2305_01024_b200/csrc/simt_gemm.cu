@@ -23,7 +23,13 @@
 
 namespace ftg {
 
-constexpr int SB = 128, SK = 8, NST = 4;   // tile, k-block, smem pipeline stages
+#ifndef FTGEMM_SIMT_SK
+#define FTGEMM_SIMT_SK 16
+#endif
+constexpr int SB = 128, SK = FTGEMM_SIMT_SK;       // tile, k-block (plan.bk)
+constexpr int NST = SK == 8 ? 4 : 3;                // smem pipeline stages
+constexpr int STAGE_FLOATS = SB * SK + SK * SB + 2 * SK;
+constexpr int SIMT_DSMEM = NST * STAGE_FLOATS * 4;  // dynamic smem: the stage ring
 
 // cp.async with zero fill: src_bytes < cp bytes fills the rest of dst with 0
 __device__ __forceinline__ void cp_async4(void* dst, const void* src, int src_bytes) {
@@ -57,9 +63,13 @@ __device__ __forceinline__ float simt_fault(float x, const DevInject& f) {
 #endif
 template <bool FT>
 __global__ void __launch_bounds__(256, FTGEMM_SIMT_MINB) simt_ftgemm_kernel(const SimtArgs a) {
-    __shared__ __align__(16) float As[NST][SB][SK];    // A tile, row-major (k contiguous)
-    __shared__ __align__(16) float Bs[NST][SK][SB];
-    __shared__ __align__(16) float acs[NST][SK], brs[NST][SK];   // e^T A_i, B_j e for the k-block
+    // stage ring (dynamic smem): A tile row-major (k contiguous), B tile, and
+    // e^T A_i, B_j e for the k-block
+    extern __shared__ __align__(16) float simt_dsmem[];
+    float (*As)[SB][SK] = reinterpret_cast<float (*)[SB][SK]>(simt_dsmem);
+    float (*Bs)[SK][SB] = reinterpret_cast<float (*)[SK][SB]>(simt_dsmem + NST * SB * SK);
+    float (*acs)[SK] = reinterpret_cast<float (*)[SK]>(simt_dsmem + 2 * NST * SB * SK);
+    float (*brs)[SK] = reinterpret_cast<float (*)[SK]>(simt_dsmem + 2 * NST * SB * SK + NST * SK);
     __shared__ float red_col[8][SB];                   // column partial sums per warp
     __shared__ float srow_s[SB], rref_s[SB], cref_s[SB], rres[SB], rtau[SB], cres[SB], ctau[SB];
     __shared__ int sflag[5];
@@ -97,16 +107,24 @@ __global__ void __launch_bounds__(256, FTGEMM_SIMT_MINB) simt_ftgemm_kernel(cons
 
     // global -> shared copies of one k-block (16-byte cp.async, NST-stage ring,
     // out-of-range elements zero-filled), issued NST-1 k-blocks ahead
-    const int a_row = tid >> 1, a_k = (tid & 1) * 4;     // 128 rows x 8 k
-    const int b_k = tid >> 5, b_col = (tid & 31) * 4;    // 8 k x 128 cols
     auto issue = [&](int kb, int s) {
         const int k0 = kb * SK;
-        const int gr = r0 + a_row, gk = k0 + a_k;
-        const int na = gr < a.M ? max(0, min(4, a.K - gk)) : 0;
-        cp_async16(&As[s][a_row][a_k], a.A + (int64_t)min(gr, a.M - 1) * a.lda + (na ? gk : 0), 4 * na);
-        const int bk = k0 + b_k, gc = c0 + b_col;
-        const int nv = bk < a.K ? max(0, min(4, a.N - gc)) : 0;
-        cp_async16(&Bs[s][b_k][b_col], a.B + (int64_t)min(bk, a.K - 1) * a.ldb + (nv ? gc : 0), 4 * nv);
+#pragma unroll
+        for (int u = 0; u < SK / 8; ++u) {                  // A: 128 rows x SK k, 16-byte chunks
+            const int L = tid + 256 * u;
+            const int a_row = L / (SK / 4), a_k = (L % (SK / 4)) * 4;
+            const int gr = r0 + a_row, gk = k0 + a_k;
+            const int na = gr < a.M ? max(0, min(4, a.K - gk)) : 0;
+            cp_async16(&As[s][a_row][a_k], a.A + (int64_t)min(gr, a.M - 1) * a.lda + (na ? gk : 0), 4 * na);
+        }
+#pragma unroll
+        for (int u = 0; u < SK / 8; ++u) {                  // B: SK k x 128 cols
+            const int L = tid + 256 * u;
+            const int b_k = L >> 5, b_col = (L & 31) * 4;
+            const int bk = k0 + b_k, gc = c0 + b_col;
+            const int nv = bk < a.K ? max(0, min(4, a.N - gc)) : 0;
+            cp_async16(&Bs[s][b_k][b_col], a.B + (int64_t)min(bk, a.K - 1) * a.ldb + (nv ? gc : 0), 4 * nv);
+        }
         if (FT) {
             if (tid < SK) cp_async4(&acs[s][tid], a.Ac + (int64_t)ti * a.kp + k0 + tid, 4);
             else if (tid < 2 * SK) cp_async4(&brs[s][tid - SK], a.Br + (int64_t)tj * a.kp + k0 + tid - SK, 4);
@@ -367,10 +385,20 @@ __global__ void __launch_bounds__(256, FTGEMM_SIMT_MINB) simt_ftgemm_kernel(cons
 }
 
 cudaError_t launch_simt(bool ft, const SimtArgs& a, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(simt_ftgemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SIMT_DSMEM);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(simt_ftgemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SIMT_DSMEM);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
     const int grid = a.tiles_m * a.tiles_n;
-    if (ft) simt_ftgemm_kernel<true><<<grid, 256, 0, st>>>(a);
-    else simt_ftgemm_kernel<false><<<grid, 256, 0, st>>>(a);
+    if (ft) simt_ftgemm_kernel<true><<<grid, 256, SIMT_DSMEM, st>>>(a);
+    else simt_ftgemm_kernel<false><<<grid, 256, SIMT_DSMEM, st>>>(a);
     return cudaGetLastError();
 }
+
+int simt_bk() { return SK; }
 
 }  // namespace ftg
