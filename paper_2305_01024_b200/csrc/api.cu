@@ -23,7 +23,7 @@
 namespace ftg {
 cudaError_t launch_encode(const Geometry& g, const EncLayout& L, int64_t M, int64_t N, int64_t K,
                           const void* A, int64_t lda, const void* B, int64_t ldb, void* enc, int which,
-                          cudaStream_t st);
+                          const CUtensorMap* mapA, int nkc_tma, cudaStream_t st);
 }  // namespace ftg
 
 namespace ftg {
@@ -116,8 +116,8 @@ Geometry geometry(const ftgemm_plan_t& p, int64_t K) {
     g.nkb = g.kp / p.bk;
     g.elt = p.dtype == FTGEMM_BF16 ? 2 : 4;
     g.tc = p.dtype != FTGEMM_F32_SIMT;
-    g.nkc_a = (g.kp + 255) / 256;
-    g.nkc_b = (g.kp + 255) / 256;
+    g.nkc_a = (g.kp + 512 / g.elt - 1) / (512 / g.elt);   // encode-A k chunks (512-byte rows)
+    g.nkc_b = (g.kp + kEncBRows - 1) / kEncBRows;
     return g;
 }
 
@@ -228,7 +228,15 @@ int ftgemm_encode(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int
     fill_plan(dtype, M, N, K, &p);
     const Geometry g = geometry(p, K);
     const EncLayout L = enc_layout(g, M, N);
-    cudaError_t ce = launch_encode(g, L, M, N, K, A, lda, B, ldb, enc_ws, which, (cudaStream_t)stream);
+    // encode A streams the operand through TMA: one (check-tile rows x 512 bytes) box per block
+    CUtensorMap mA{};
+    if (which & 1) {
+        const CUtensorMapDataType dt = dtype == FTGEMM_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+        if ((e = make_map(&mA, dt, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * elt, (uint32_t)(512 / elt),
+                          (uint32_t)g.bmd, CU_TENSOR_MAP_SWIZZLE_NONE))) return e;
+    }
+    cudaError_t ce = launch_encode(g, L, M, N, K, A, lda, B, ldb, enc_ws, which, (which & 1) ? &mA : nullptr,
+                                   g.nkc_a, (cudaStream_t)stream);
     if (ce != cudaSuccess) return fail_cuda(ce, "encode launch");
     g_err.clear();
     return FTGEMM_OK;

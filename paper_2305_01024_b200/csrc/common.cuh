@@ -13,6 +13,7 @@ namespace ftg {
 constexpr int kNumSMsB200 = 148;
 constexpr int kMaxEvents = 4096;
 constexpr int kMaxInject = 65536;
+constexpr int kEncBRows = 256;     // k-rows of B per encode-B block
 
 // ---- report workspace (device) --------------------------------------------
 struct DevInject {        // one fault, resolved to (check tile, k-block, in-tile position)

@@ -11,18 +11,22 @@
 //       Bt_j    = B^r_j = [B_j, split(B_j e), 0], K-major (tensor-core paths)
 //       ||B[:,q]||_2 per column, ||Br_j||_2 per tile.
 //
-// Single streaming passes over each operand (HBM bound): loads are 8- or
-// 16-byte vectors, issued in unrolled batches before use (memory-level
-// parallelism), reductions go through warp shuffles and shared memory.  The
+// Single streaming passes over each operand (HBM bound).  Encode A is fed by
+// one TMA box per block (check-tile rows x 512 bytes); encode B streams 8- or
+// 16-byte vectors in unrolled batches; reductions go through warp shuffles
+// and shared memory; with both operands, encode B runs on a side stream
+// beside encode A (launch_encode).  The
 // per-row / per-column norms are reduced across K-chunk blocks by the LAST
 // block of each tile (atomic ticket, self-resetting), so no extra launch is
 // needed.  TF32 mode sums the values exactly as the tensor core will see them
 // (low 13 mantissa bits dropped), so the carried references and the main
 // product are built from the same operands.
 #include <cstdint>
+#include <mutex>
 #include <type_traits>
 
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace ftg {
 
@@ -30,52 +34,6 @@ __device__ __forceinline__ float warp_sum(float x) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
     return x;
-}
-
-// sum over the 256 threads of a block (result valid in every thread)
-__device__ __forceinline__ float block_sum256(float x, float* red8) {
-    x = warp_sum(x);
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) red8[threadIdx.x >> 5] = x;
-    __syncthreads();
-    float t = 0.0f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) t += red8[i];
-    return t;
-}
-
-// 8 consecutive operand values of a row starting at p (valid = elements inside K)
-template <int MODE>
-__device__ __forceinline__ void load8(const void* base, int64_t off, int valid, float (&v)[8]) {
-    if constexpr (MODE == 0) {
-        const uint16_t* p = reinterpret_cast<const uint16_t*>(base) + off;
-        if (valid >= 8) {
-            const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
-            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                v[2 * i] = __uint_as_float(w[i] << 16);
-                v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
-            }
-        } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) v[i] = (i < valid) ? bf16_to_f32(__ldg(p + i)) : 0.0f;
-        }
-    } else {
-        const float* p = reinterpret_cast<const float*>(base) + off;
-        if (valid >= 8) {
-            const float4 a = __ldg(reinterpret_cast<const float4*>(p));
-            const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
-            v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-        } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) v[i] = (i < valid) ? __ldg(p + i) : 0.0f;
-        }
-        if constexpr (MODE == 1) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) v[i] = tf32_trunc(v[i]);
-        }
-    }
 }
 
 // sum_{c < n} p[c * stride]: independent loads in flight (the partial-norm
@@ -109,115 +67,86 @@ __device__ __forceinline__ bool last_block(int* ticket, int idx, int nblocks, in
     return last;
 }
 
-// ---------------------------------------------------------------- encode A --
-// grid (nkc = ceil(kp/256), tiles_m); block 256 = 8 warps.  Lane l owns k in
-// [kc*256 + 8l, +8); warp w sums rows w, w+8, ... of the tile (4 rows per batch).
-// MODE: 0 = BF16, 1 = TF32 (FP32 storage, truncated), 2 = FP32 SIMT (no split).
+// ------------------------------------------------ encode A (TMA-fed) -------
+// grid (nkc = ceil(kp/KC), tiles_m); block 256.  One TMA load brings the tile's
+// bmd rows x KC k (512-byte rows, 64 KB) into shared memory -- a single bulk
+// request per block, so every SM keeps ~3 x 64 KB in flight with no registers
+// tied up -- then (a) thread pairs sum columns over the rows, (b) warps reduce
+// the row sums of squares.  KC = 256 (BF16) / 128 (FP32 storage).
 template <int MODE>
-__global__ void __launch_bounds__(256) encode_a_kernel(const void* __restrict__ A, int64_t lda, int M, int K,
-                                                       int bmd, int kp, int bk, int nkc, float* __restrict__ Ac,
-                                                       uint8_t* __restrict__ Y, float* rn2, float* acn2, int* ticket,
-                                                       float* __restrict__ rownorm, float* __restrict__ acnorm) {
-    __shared__ float red[8][257];
+__global__ void __launch_bounds__(256) encode_a_tma_kernel(const __grid_constant__ CUtensorMap tmA, int M, int K,
+                                                           int bmd, int kp, int bk, int nkc, float* __restrict__ Ac,
+                                                           uint8_t* __restrict__ Y, float* rn2, float* acn2, int* ticket,
+                                                           float* __restrict__ rownorm, float* __restrict__ acnorm) {
+    constexpr int ELT = MODE == 0 ? 2 : 4;
+    constexpr int KC = 512 / ELT;                       // k per block (512-byte rows)
+    extern __shared__ __align__(128) uint8_t enc_smem[];
+    uint8_t* tile = enc_smem;                           // [bmd][512 B]
+    float* colp = reinterpret_cast<float*>(enc_smem + 128 * 512);   // [2][KC] half-tile column sums
+    __shared__ __align__(8) uint64_t bar;
     __shared__ float red8[8];
     __shared__ int s_flag;
     const int kc = blockIdx.x, ti = blockIdx.y;
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int k0 = kc * 256 + lane * 8;
-    const int valid = K - k0;
-    float ac[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) ac[i] = 0.0f;
-    const int rbeg = ti * bmd;
-    const int rend = min(M, rbeg + bmd);
-    // rows w, w+8, ... of the tile; RB rows per batch so that RB independent
-    // 16-byte loads per lane are in flight (BF16 keeps them packed until use)
-    constexpr int RB = MODE == 0 ? 8 : 4;
-    for (int row = rbeg + w; row < rend; row += 8 * RB) {
-        float sq[RB];
-        if constexpr (MODE == 0) {
-            uint4 raw[RB];
-#pragma unroll
-            for (int u = 0; u < RB; ++u) {
-                const int r = row + 8 * u;
-                raw[u] = make_uint4(0u, 0u, 0u, 0u);
-                if (r < rend && valid >= 8) {
-                    raw[u] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(A) + (int64_t)r * lda + k0));
-                } else if (r < rend && valid > 0) {
-                    float v[8];
-                    load8<0>(A, (int64_t)r * lda + k0, valid, v);
-                    uint32_t pk[4];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        pk[i] = (__float_as_uint(v[2 * i]) >> 16) | (__float_as_uint(v[2 * i + 1]) & 0xFFFF0000u);
-                    raw[u] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < RB; ++u) {
-                const uint32_t wd[4] = {raw[u].x, raw[u].y, raw[u].z, raw[u].w};
-                float q = 0.0f;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const float lo = __uint_as_float(wd[i] << 16), hi = __uint_as_float(wd[i] & 0xFFFF0000u);
-                    ac[2 * i] += lo;
-                    ac[2 * i + 1] += hi;
-                    q = fmaf(lo, lo, q);
-                    q = fmaf(hi, hi, q);
-                }
-                sq[u] = q;
-            }
-        } else {
-            float v[RB][8];
-#pragma unroll
-            for (int u = 0; u < RB; ++u) {
-                const int r = row + 8 * u;
-                if (r < rend && valid > 0) load8<MODE>(A, (int64_t)r * lda + k0, valid, v[u]);
-                else {
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) v[u][i] = 0.0f;
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < RB; ++u) {
-                float q = 0.0f;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    ac[i] += v[u][i];
-                    q = fmaf(v[u][i], v[u][i], q);
-                }
-                sq[u] = q;
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-            for (int u = 0; u < RB; ++u) sq[u] += __shfl_xor_sync(0xffffffffu, sq[u], o);
-        if (lane == 0) {
-#pragma unroll
-            for (int u = 0; u < RB; ++u)
-                if (row + 8 * u < rend) rn2[(int64_t)kc * M + row + 8 * u] = sq[u];
-        }
+    const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+    const int rbeg = ti * bmd, rows = min(bmd, M - rbeg);
+    if (t == 0) {
+        mbar_init(&bar, 1);
+        fence_barrier_init();
+        mbar_arrive_expect_tx(&bar, (uint32_t)(bmd * 512));
+        tma_load_2d(tile, &tmA, &bar, kc * KC, rbeg);
     }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) red[w][lane * 8 + i] = ac[i];
     __syncthreads();
-    const int t = threadIdx.x;
-    const int k = kc * 256 + t;
-    float s = 0.0f;
-    if (k < kp) {
+    mbar_wait(&bar, 0);
+    auto val = [&](int r, int c) -> float {             // element (row r, k-col c) as the MMA sees it
+        if constexpr (MODE == 0) return bf16_to_f32(reinterpret_cast<const uint16_t*>(tile + r * 512)[c]);
+        else if constexpr (MODE == 1) return tf32_trunc(reinterpret_cast<const float*>(tile + r * 512)[c]);
+        else return reinterpret_cast<const float*>(tile + r * 512)[c];
+    };
+    // (a) column sums: thread t: column c = t % KC over one half of the rows (BF16:
+    // 256 columns x 1 half; FP32: 128 columns x 2 halves)
+    {
+        constexpr int HALVES = 256 / KC;
+        const int c = t % KC, h = t / KC;
+        const int r_lo = h * ((rows + HALVES - 1) / HALVES), r_hi = min(rows, r_lo + (rows + HALVES - 1) / HALVES);
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        int r = r_lo;
+        for (; r + 4 <= r_hi; r += 4) { s0 += val(r, c); s1 += val(r + 1, c); s2 += val(r + 2, c); s3 += val(r + 3, c); }
+        for (; r < r_hi; ++r) s0 += val(r, c);
+        colp[h * KC + c] = (s0 + s1) + (s2 + s3);
+    }
+    // (b) row sums of squares: warp w, rows w, w + 8, ...; lane reads 16 bytes
+    for (int r = w; r < rows; r += 8) {
+        const uint4 u = *reinterpret_cast<const uint4*>(tile + r * 512 + lane * 16);
+        const uint32_t wd[4] = {u.x, u.y, u.z, u.w};
+        float q = 0.0f;
 #pragma unroll
-        for (int ww = 0; ww < 8; ++ww) s += red[ww][t];
+        for (int i = 0; i < 4; ++i) {
+            if constexpr (MODE == 0) {
+                const float lo = __uint_as_float(wd[i] << 16), hi = __uint_as_float(wd[i] & 0xFFFF0000u);
+                q = fmaf(lo, lo, q); q = fmaf(hi, hi, q);
+            } else {
+                const float x = MODE == 1 ? tf32_trunc(__uint_as_float(wd[i])) : __uint_as_float(wd[i]);
+                q = fmaf(x, x, q);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+        if (lane == 0) rn2[(int64_t)kc * M + rbeg + r] = q;
+    }
+    __syncthreads();
+    // Ac, its split rows (pre-swizzled Ypack) and the partial ||Ac||^2
+    float s2 = 0.0f;
+    for (int c = t; c < KC; c += 256) {
+        const int k = kc * KC + c;
+        if (k >= kp) break;
+        float s = 0.0f;
+        for (int h = 0; h < 256 / KC; ++h) s += colp[h * KC + c];
         if (k >= K) s = 0.0f;
         Ac[(int64_t)ti * kp + k] = s;
+        s2 = fmaf(s, s, s2);
         if constexpr (MODE != 2) {
             float hi, mid, lo;
             split3<MODE>(s, hi, mid, lo);
-            // Ypack[tile][k-block][r][128 bytes]: split row r lands in MMA row
-            // 125 + r of the A tile, whose 16-byte chunks are stored in the
-            // SWIZZLE_128B order (chunk c at c ^ (row & 7)) so the fused kernel
-            // bulk-copies the 384 bytes straight into shared memory.
-            constexpr int ELT = MODE == 0 ? 2 : 4;
             const int kb = k / bk, kk = k % bk;
             const int chunk = (kk * ELT) >> 4, within = (kk * ELT) & 15;
             uint8_t* yb = Y + ((int64_t)ti * (kp / bk) + kb) * 384;
@@ -231,16 +160,25 @@ __global__ void __launch_bounds__(256) encode_a_kernel(const void* __restrict__ 
             }
         }
     }
-    const float s2 = block_sum256(s * s, red8);
-    if (t == 0) acn2[(int64_t)ti * nkc + kc] = s2;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    if (lane == 0) red8[w] = s2;
+    __syncthreads();
+    if (t == 0) {
+        float q = 0.0f;
+        for (int i = 0; i < 8; ++i) q += red8[i];
+        acn2[(int64_t)ti * nkc + kc] = q;
+    }
     if (last_block(ticket, ti, nkc, &s_flag)) {
-        for (int p = rbeg + t; p < rend; p += 256) rownorm[p] = sqrtf(strided_sum(rn2 + p, nkc, M));
+        for (int p = rbeg + t; p < rbeg + rows; p += 256) rownorm[p] = sqrtf(strided_sum(rn2 + p, nkc, M));
         if (t == 0) acnorm[ti] = sqrtf(strided_sum(acn2 + (int64_t)ti * nkc, nkc, 1));
     }
 }
 
+size_t encode_a_tma_smem() { return 128 * 512 + 2 * 256 * sizeof(float); }
+
 // ----------------------------------------------------- encode B (FP32 SIMT) --
-// grid (nkc = ceil(kp/256), tiles_n): Br_j (warp per k-row) and column squares.
+// grid (nkc = ceil(kp/kEncBRows), tiles_n): Br_j (warp per k-row) and column squares.
 __global__ void __launch_bounds__(256) encode_b_simt_kernel(const float* __restrict__ B, int64_t ldb, int N, int K,
                                                             int bnd, int kp, int nkc, float* __restrict__ Br,
                                                             float* cn2, float* brn2, int* ticket,
@@ -256,8 +194,8 @@ __global__ void __launch_bounds__(256) encode_b_simt_kernel(const float* __restr
 #pragma unroll
     for (int i = 0; i < 8; ++i) csq[i] = 0.0f;
     float bq = 0.0f;
-    for (int r = w; r < 256; r += 8) {
-        const int k = kc * 256 + r;
+    for (int r = w; r < kEncBRows; r += 8) {
+        const int k = kc * kEncBRows + r;
         if (k >= kp) break;
         float s = 0.0f;
         if (k < K) {
@@ -320,7 +258,7 @@ __global__ void __launch_bounds__(256) encode_b_simt_kernel(const float* __restr
 }
 
 // -------------------------------------------- encode B (tensor-core paths) --
-// grid (nkc = ceil(kp/256), tiles_n); warp w handles k-rows kc*256 + w + 8i.
+// grid (nkc = ceil(kp/kEncBRows), tiles_n); warp w handles k-rows kc*kEncBRows + w + 8i.
 // Per k-row of check tile j the warp streams the bnd data columns (4-element
 // chunks: lane l owns chunks l and l+32), reduces B_j e with warp shuffles,
 // accumulates column squares in registers, and writes the encoded operand row
@@ -352,12 +290,12 @@ __global__ void __launch_bounds__(256) encode_b_tc_kernel(const void* __restrict
         if constexpr (MODE == 0) return bf16_to_f32(x);
         else return tf32_trunc(x);
     };
-    for (int r = w; r < 256; r += 8 * RB) {
+    for (int r = w; r < kEncBRows; r += 8 * RB) {
         V raw[RB][2];
         float s[RB];
 #pragma unroll
         for (int u = 0; u < RB; ++u) {
-            const int k = kc * 256 + r + 8 * u;
+            const int k = kc * kEncBRows + r + 8 * u;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int ch = lane + 32 * h;
@@ -399,7 +337,7 @@ __global__ void __launch_bounds__(256) encode_b_tc_kernel(const void* __restrict
             for (int u = 0; u < RB; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
 #pragma unroll
         for (int u = 0; u < RB; ++u) {
-            const int k = kc * 256 + r + 8 * u;
+            const int k = kc * kEncBRows + r + 8 * u;
             if (k >= kp) continue;
             uint8_t* row = Bt + ((int64_t)k * ldt + (int64_t)tj * bn) * ELT;
 #pragma unroll
@@ -457,41 +395,86 @@ __global__ void __launch_bounds__(256) encode_b_tc_kernel(const void* __restrict
 }
 
 // ---------------------------------------------------------------- launch ---
+namespace {
+// side stream + events for running encode B beside encode A (one per device)
+struct EncodeFork {
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+std::mutex g_fork_mu;
+EncodeFork g_fork[64];
+}  // namespace
+
 cudaError_t launch_encode(const Geometry& g, const EncLayout& L, int64_t M, int64_t N, int64_t K,
                           const void* A, int64_t lda, const void* B, int64_t ldb, void* enc, int which,
-                          cudaStream_t st) {
+                          const CUtensorMap* mapA, int nkc_tma, cudaStream_t st) {
     char* base = reinterpret_cast<char*>(enc);
     const int mode = g.dtype == FTGEMM_BF16 ? 0 : (g.dtype == FTGEMM_TF32 ? 1 : 2);
     auto F = [&](size_t off) { return reinterpret_cast<float*>(base + off); };
-    if (which & 1) {
-        cudaError_t e = cudaMemsetAsync(base + L.cnt_a, 0, sizeof(int) * (size_t)g.tiles_m, st);
-        if (e != cudaSuccess) return e;
-        dim3 grid(g.nkc_a, g.tiles_m);
-        uint8_t* Y = reinterpret_cast<uint8_t*>(base + L.y);
-        int* tk = reinterpret_cast<int*>(base + L.cnt_a);
-#define ENC_A(MD) encode_a_kernel<MD><<<grid, 256, 0, st>>>(A, lda, (int)M, (int)K, g.bmd, g.kp, g.bk, g.nkc_a, \
-            F(L.ac), Y, F(L.rn2), F(L.acn2), tk, F(L.rownorm), F(L.acnorm))
-        if (mode == 0) ENC_A(0); else if (mode == 1) ENC_A(1); else ENC_A(2);
-#undef ENC_A
+    cudaError_t e;
+    // Both operands: encode B runs on a side stream beside encode A (both are
+    // HBM streams far smaller than the machine's concurrency, so the two
+    // overlap their ramp-up and tails); the caller's stream waits for both.
+    cudaStream_t sb = st;
+    EncodeFork* fk = nullptr;
+    if ((which & 3) == 3) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::lock_guard<std::mutex> lk(g_fork_mu);
+        fk = (dev >= 0 && dev < 64) ? &g_fork[dev] : nullptr;
+        if (fk && !fk->side) {
+            if ((e = cudaStreamCreateWithFlags(&fk->side, cudaStreamNonBlocking)) != cudaSuccess) return e;
+            if ((e = cudaEventCreateWithFlags(&fk->fork, cudaEventDisableTiming)) != cudaSuccess) return e;
+            if ((e = cudaEventCreateWithFlags(&fk->join, cudaEventDisableTiming)) != cudaSuccess) return e;
+        }
+        if (fk) {
+            if ((e = cudaEventRecord(fk->fork, st)) != cudaSuccess) return e;
+            if ((e = cudaStreamWaitEvent(fk->side, fk->fork, 0)) != cudaSuccess) return e;
+            sb = fk->side;
+        }
     }
     if (which & 2) {
-        cudaError_t e = cudaMemsetAsync(base + L.cnt_b, 0, sizeof(int) * (size_t)g.tiles_n, st);
-        if (e != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(base + L.cnt_b, 0, sizeof(int) * (size_t)g.tiles_n, sb)) != cudaSuccess) return e;
         int* tk = reinterpret_cast<int*>(base + L.cnt_b);
         dim3 grid(g.nkc_b, g.tiles_n);
         if (mode == 2) {
-            encode_b_simt_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(B), ldb, (int)N, (int)K, g.bnd,
+            encode_b_simt_kernel<<<grid, 256, 0, sb>>>(reinterpret_cast<const float*>(B), ldb, (int)N, (int)K, g.bnd,
                                                        g.kp, g.nkc_b, F(L.br), F(L.cn2), F(L.brn2), tk,
                                                        F(L.colnorm), F(L.brnorm));
         } else {
             uint8_t* Bt = (which & 4) ? nullptr : reinterpret_cast<uint8_t*>(base + L.bt);   // 4: no encoded operand
-#define ENC_B(MD) encode_b_tc_kernel<MD><<<grid, 256, 0, st>>>(B, ldb, (int)N, (int)K, g.bnd, g.bn, g.kp, \
+#define ENC_B(MD) encode_b_tc_kernel<MD><<<grid, 256, 0, sb>>>(B, ldb, (int)N, (int)K, g.bnd, g.bn, g.kp, \
             g.tiles_n * g.bn, g.nkc_b, F(L.br), Bt, F(L.cn2), F(L.brn2), tk, F(L.colnorm), F(L.brnorm))
             if (mode == 0) ENC_B(0); else ENC_B(1);
 #undef ENC_B
         }
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    return cudaGetLastError();
+    if (which & 1) {
+        if (!mapA) return cudaErrorInvalidValue;
+        if ((e = cudaMemsetAsync(base + L.cnt_a, 0, sizeof(int) * (size_t)g.tiles_m, st)) != cudaSuccess) return e;
+        uint8_t* Y = reinterpret_cast<uint8_t*>(base + L.y);
+        int* tk = reinterpret_cast<int*>(base + L.cnt_a);
+        static bool attr[3] = {false, false, false};
+        const int smem = (int)encode_a_tma_smem();
+        dim3 grid(nkc_tma, g.tiles_m);
+#define ENC_AT(MD) do { \
+            if (!attr[MD]) { \
+                cudaError_t ea = cudaFuncSetAttribute(encode_a_tma_kernel<MD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+                if (ea != cudaSuccess) return ea; \
+                attr[MD] = true; \
+            } \
+            encode_a_tma_kernel<MD><<<grid, 256, smem, st>>>(*mapA, (int)M, (int)K, g.bmd, g.kp, g.bk, nkc_tma, \
+                F(L.ac), Y, F(L.rn2), F(L.acn2), tk, F(L.rownorm), F(L.acnorm)); } while (0)
+        if (mode == 0) ENC_AT(0); else if (mode == 1) ENC_AT(1); else ENC_AT(2);
+#undef ENC_AT
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if (sb != st) {
+        if ((e = cudaEventRecord(fk->join, sb)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(st, fk->join, 0)) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 }  // namespace ftg

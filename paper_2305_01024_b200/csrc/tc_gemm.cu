@@ -37,6 +37,14 @@
 
 namespace ftg {
 
+// epilogue warpgroups: 2 = one warpgroup per TMEM accumulator buffer, so the
+// epilogues (verification included) of two consecutive tiles run concurrently
+#ifndef FTGEMM_EPI_WG
+#define FTGEMM_EPI_WG 2
+#endif
+constexpr int kEpiWG = FTGEMM_EPI_WG;
+constexpr int kThreads = 128 + 128 * kEpiWG;
+
 template <bool kTF32, int BN_, bool FT, int CG_ = 1>
 struct TcCfg {
     static constexpr int CG = CG_;                 // 1: one CTA per MMA; 2: CTA pair (M = 256)
@@ -52,7 +60,10 @@ struct TcCfg {
     static constexpr int B_BYTES = (NBOX / CG) * B_BOX_BYTES;   // this CTA's share of the B tile
     static constexpr int Y_BYTES = 384;            // 3 split rows x 128 bytes
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int STAGES = (196 * 1024) / (A_BYTES + B_BYTES) < 8 ? (196 * 1024) / (A_BYTES + B_BYTES) : 8;
+    static constexpr int STG_BYTES = 4 * 2 * 4096;     // per epilogue warpgroup (see below)
+    static constexpr int EPI_BYTES = kEpiWG * STG_BYTES;
+    static constexpr int STAGE_FIT = (227 * 1024 - 1280 - EPI_BYTES) / (A_BYTES + B_BYTES);
+    static constexpr int STAGES = STAGE_FIT < 8 ? STAGE_FIT : 8;
     static constexpr int BMD = FT ? BM - 3 : BM;   // data rows of a check tile
     static constexpr int BND = FT ? BN - 4 : BN;   // data cols of a check tile
     static constexpr int TMEM_COLS = 2 * BN;
@@ -61,11 +72,9 @@ struct TcCfg {
     // staging for the TMA stores; the verification arrays (column partial sums,
     // reference rows, residuals, thresholds) alias the staging area (pass 1 runs
     // only after the previous tile's stores have read it)
-    static constexpr int STG_BYTES = 4 * 2 * 4096;
     static constexpr int VER_BYTES = (4 * BN + 3 * BN + 2 * BN + 2 * BM) * 4 + 64;
     static_assert(VER_BYTES <= 12288, "verification arrays must fit below the transpose buffers");
     static_assert(12288 + 4 * 32 * 36 * 4 <= STG_BYTES, "transpose buffers must fit in the staging area");
-    static constexpr int EPI_BYTES = STG_BYTES;
     static constexpr int GW = kTF32 ? 32 : 64;     // output columns per 128-byte store box
     static constexpr int NG = (BND + GW - 1) / GW; // store groups per tile
     static constexpr int LAST = BND - GW;          // start of the last group (overlaps the previous one by BND % GW)
@@ -115,7 +124,7 @@ __device__ __forceinline__ uint32_t apply_fault(uint32_t bits, const DevInject& 
 }
 
 template <bool kTF32, int BN, bool FT, int CG>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kThreads, 1)
 tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC29,
                  const __grid_constant__ CUtensorMap tmY, const TcArgs a) {
@@ -126,23 +135,16 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     // __shared__ array keeps the shared address space visible to the compiler
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* stage_base = smem;
-    uint8_t* stg = smem + S * Cfg::STAGE_BYTES;                               // [4][4096] (1024-aligned)
-    float* colsum = reinterpret_cast<float*>(stg);                            // [4][BN] (aliases staging)
-    float* refrow = colsum + 4 * BN;                                          // [3][BN] split rows of C^c
-    float* cres = refrow + 3 * BN;                                            // [BN]
-    float* ctau = cres + BN;                                                  // [BN]
-    float* rres = ctau + BN;                                                  // [BM]
-    float* rtau = rres + Cfg::BM;                                             // [BM]
-    int* sflag = reinterpret_cast<int*>(rtau + Cfg::BM);                      // nr, nc, p*, q*, corr
+    uint8_t* const stg0 = smem + S * Cfg::STAGE_BYTES;                        // [kEpiWG][4][2][4096] (1024-aligned)
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * Cfg::STAGE_BYTES + Cfg::EPI_BYTES);
     uint64_t* full = bars;              // [S]  stage landed (TMA + bulk bytes)
     uint64_t* empty = bars + S;         // [S]  producer may refill
     uint64_t* tm_full = bars + 2 * S;   // [2]  accumulator complete
     uint64_t* tm_empty = tm_full + 2;   // [2]
-    uint64_t* inj_req = tm_empty + 2;
-    uint64_t* inj_done = inj_req + 1;
-    uint64_t* cbar = inj_done + 1;      // [4]  C_in tile loads (beta != 0), one per epilogue warp
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(cbar + 4);
+    uint64_t* inj_req = tm_empty + 2;   // [2]  mid-mainloop hand-off, per accumulator buffer
+    uint64_t* inj_done = inj_req + 2;   // [2]
+    uint64_t* cbar = inj_done + 2;      // [4 kEpiWG]  C_in tile loads (beta != 0), one per epilogue warp
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(cbar + 4 * kEpiWG);
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
@@ -166,9 +168,11 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             mbar_init(&tm_full[b], 1);
             mbar_init(&tm_empty[b], 4 * CG);     // every epilogue warp of the pair
         }
-        mbar_init(inj_req, 1);
-        mbar_init(inj_done, CG);
-        for (int w = 0; w < 4; ++w) mbar_init(&cbar[w], 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&inj_req[b], 1);
+            mbar_init(&inj_done[b], CG);
+        }
+        for (int w = 0; w < 4 * kEpiWG; ++w) mbar_init(&cbar[w], 1);
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc<Cfg::TMEM_COLS, CG>(tmem_holder);
@@ -224,7 +228,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             auto commit = [&](uint64_t* bar) {
                 if constexpr (CG == 2) umma_commit_pair(bar, pair); else umma_commit(bar);
             };
-            int s = 0; uint32_t ph = 0; uint32_t injph = 0;
+            int s = 0; uint32_t ph = 0; uint32_t injph[2] = {0, 0};
             int lt = 0;
             for (int t = cluster_id; t < a.num_units; t += num_clusters, ++lt) {
                 const int acc = lt & 1;
@@ -255,9 +259,9 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     if (FT && ((ii < ie && a.inj[ii].kb == kb) || chk)) {
                         // hand the accumulator to the epilogue warps (of both CTAs) for the
                         // fault(s) of this k-block and / or the check closing a K_s step
-                        commit(inj_req);
-                        mbar_wait(inj_done, injph);
-                        injph ^= 1;
+                        commit(&inj_req[acc]);
+                        mbar_wait(&inj_done[acc], injph[acc]);
+                        injph[acc] ^= 1;
                         tc_fence_after();
                         while (ii < ie && a.inj[ii].kb == kb) ++ii;
                     }
@@ -269,11 +273,23 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         __syncwarp();
     } else if (warp >= 4) {
         // ----------------------------------------------------- epilogue -----
-        const int ew = warp - 4;                 // TMEM lane quadrant
+        const int wg = (warp - 4) >> 2;          // epilogue warpgroup (owns accumulator buffer wg when kEpiWG == 2)
+        const int ew = (warp - 4) & 3;           // TMEM lane quadrant
         const int rloc = ew * 32 + (int)lane;    // row of the 128-row tile
         const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
-        const int et = threadIdx.x - 128;        // 0..127
-        uint32_t injph = 0, cph = 0, gcount = 0;   // gcount: store groups issued by this warp
+        const int et = threadIdx.x - 128 - 128 * wg;   // 0..127
+        const uint32_t ebar = 1 + wg;            // named barrier of this warpgroup
+        uint32_t injph[2] = {0, 0}, cph = 0, gcount = 0;   // gcount: store groups issued by this warp
+        uint64_t* cbw = &cbar[4 * wg + ew];
+        uint8_t* stg = stg0 + wg * Cfg::STG_BYTES;
+        float* colsum = reinterpret_cast<float*>(stg);                            // [4][BN] (aliases staging)
+        float* refrow = colsum + 4 * BN;                          // [3][BN] split rows of C^c
+        float* cres = refrow + 3 * BN;                            // [BN]
+        float* ctau = cres + BN;                                  // [BN]
+        float* rres = ctau + BN;                                  // [BM]
+        float* rtau = rres + Cfg::BM;                             // [BM]
+        int* sflag = reinterpret_cast<int*>(rtau + Cfg::BM);      // nr, nc, p*, q*, corr
+
         unsigned long long n_checked = 0;
         int lt = 0;
         // arrival on a barrier of the MMA leader (remote for the peer CTA)
@@ -291,6 +307,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             constexpr int doff = 0;                            // data col q <-> MMA col q
             constexpr int xoff = BN - 4;                       // row-reference split columns
             const int acc = lt & 1;
+            if (kEpiWG == 2 && acc != wg) continue;            // the other warpgroup's tile
             const uint32_t accph = (lt >> 1) & 1;
             const uint32_t tb = tmem_base + acc * BN;
             // norms for this tile's thresholds, fetched before the accumulator is ready
@@ -315,7 +332,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 // previous tile's stores have read the staging area (aliased below) and
                 // every reader of sflag / residual arrays is done
                 if (lane == 0) bulk_wait_read0();
-                named_bar_sync(1, 128);
+                named_bar_sync(ebar, 128);
                 if (et == 0) { sflag[0] = 0; sflag[1] = 0; sflag[2] = 1 << 30; sflag[3] = 1 << 30; }
                 const bool rvalid = rloc < bm;
                 const bool isref = rloc >= Cfg::BMD;      // lanes 29..31 of warp 3: split rows of e^T A B
@@ -372,7 +389,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     }
                     srow = (rs[0] + rs[1]) + (rs[2] + rs[3]);
                 }
-                named_bar_sync(1, 128);
+                named_bar_sync(ebar, 128);
                 // ---- row residuals ----
                 if (rvalid) {
                     const float r = srow - rref;
@@ -393,7 +410,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         if (!(fabsf(c) <= tc)) { atomicAdd(&sflag[1], 1); atomicMin(&sflag[3], col); }
                     }
                 }
-                named_bar_sync(1, 128);
+                named_bar_sync(ebar, 128);
                 // ---- decide (R3-R5) ----
                 const int nr = sflag[0], nc = sflag[1];
                 pstar = nr ? sflag[2] : -1;
@@ -429,7 +446,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         }
                         if (rloc == pstar) sflag[4] = __float_as_int(rref - sx);
                     }
-                    named_bar_sync(1, 128);
+                    named_bar_sync(ebar, 128);
                     corr = __int_as_float(sflag[4]);
                 }
                 if (et == 0) {
@@ -459,7 +476,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     }
                 }
                 // the verification arrays alias the staging buffers that pass 2 writes
-                named_bar_sync(1, 128);
+                named_bar_sync(ebar, 128);
             };
 
             // ---- mid-mainloop hand-offs: fault injection and, in
@@ -474,8 +491,8 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     const int kb_c = next_chk < a.num_kb - 1 ? next_chk : 0x7fffffff;
                     const int kb = min(kb_f, kb_c);
                     if (kb == 0x7fffffff) break;
-                    mbar_wait(inj_req, injph);
-                    injph ^= 1;
+                    mbar_wait(&inj_req[acc], injph[acc]);
+                    injph[acc] ^= 1;
                     tc_fence_after();
                     for (; ii < ie && a.inj[ii].kb == kb; ++ii) {
                         const DevInject f = a.inj[ii];
@@ -496,7 +513,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         next_chk += a.ks_kb;
                         if (has_rows) {
                             tc_fence_before();
-                            named_bar_sync(1, 128);             // faults of this k-block are in TMEM
+                            named_bar_sync(ebar, 128);             // faults of this k-block are in TMEM
                             tc_fence_after();
                             const int kdone = min(a.K, (kb + 1) * Cfg::BK);
                             int k2 = 0, p2 = -1, q2 = -1;
@@ -511,8 +528,8 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         }
                     }
                     tc_fence_before();
-                    named_bar_sync(1, 128);
-                    if (et == 0) arrive_leader(inj_done);
+                    named_bar_sync(ebar, 128);
+                    if (et == 0) arrive_leader(&inj_done[acc]);
                 }
             }
 
@@ -630,10 +647,10 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 const int gcol = c0 + cs, grow = r0 + ew * 32;
                 if (a.beta != 0.0f) {
                     if (lane == 0) {
-                        mbar_arrive_expect_tx(&cbar[ew], (FT && ew == 3 ? 29 : 32) * 128);
-                        tma_load_2d(sbuf, cmap, &cbar[ew], gcol, grow);
+                        mbar_arrive_expect_tx(cbw, (FT && ew == 3 ? 29 : 32) * 128);
+                        tma_load_2d(sbuf, cmap, cbw, gcol, grow);
                     }
-                    mbar_wait(&cbar[ew], cph);
+                    mbar_wait(cbw, cph);
                     cph ^= 1;
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
@@ -712,7 +729,7 @@ cudaError_t launch_tc_t(const CUtensorMap& mA, const CUtensorMap& mB, const CUte
     const int clusters = a.num_units < kNumSMsB200 / CG ? a.num_units : kNumSMsB200 / CG;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(clusters * CG, 1, 1);
-    cfg.blockDim = dim3(256, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
