@@ -269,8 +269,6 @@ def run_ours(args):
 
     extra = {}
     if not args.no_sweep:
-        # comparators, measured in ROUNDS interleaved across configurations
-        # (median per configuration) so that clock / power drift hits all alike
         reps, rounds = max(20, args.steps), 3
         stress = []
         for ti in range(pl.tiles_m):
@@ -297,14 +295,30 @@ def run_ours(args):
         samples = {k: [] for k in configs}
         rate_samples = {str(int(r)): [] for r in SWEEP_RATES}
         rate_inj = {str(int(r)): 0 for r in SWEEP_RATES}
+        # comparators interleaved CALL BY CALL (each call timed by its own event
+        # pair on the launch stream; median per configuration), so that every
+        # configuration sees the same clock / power state -- under the B200's
+        # power cap, back-to-back blocks of one configuration drift apart
+        names = list(configs)
+        evs = {k: [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(reps * rounds)] for k in names}
+        for k in names:
+            configs[k]()
+        barrier(); torch.cuda.synchronize()
+        for i in range(reps * rounds):
+            for k in names:
+                evs[k][i][0].record(stream)
+                configs[k]()
+                evs[k][i][1].record(stream)
+        torch.cuda.synchronize()
+        for k in names:
+            samples[k] = [a.elapsed_time(b) for a, b in evs[k]]
         for _ in range(rounds):
-            for k, fn in configs.items():
-                samples[k].append(timed([fn] * reps, 2))
             for rate in SWEEP_RATES:
                 sc = schedule(rate, reps, est)
                 rate_inj[str(int(rate))] += sum(len(x) for x in sc)
                 rate_samples[str(int(rate))].append(timed([(lambda inj: (lambda: step(inj)))(x) for x in sc], 2))
-        med = {k: statistics.median(v) for k, v in samples.items()}
+        med = {k: max_over_ranks(statistics.median(v)) for k, v in samples.items()}
         g.reset()
         t_stress = timed([lambda: g.run(A, B, C, ft_level=F.FT_CORRECT, injections=stress)] * 3, 1)
         cs, _ = g.report(0)

@@ -78,23 +78,29 @@ void fill_plan(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* p) {
         p->bm = 128; p->bn = 128; p->bk = simt_bk();
         p->check_tile_m = 128; p->check_tile_n = 128;
         p->off_tile_m = 128; p->off_tile_n = 128;
-        p->stages = 2; p->cta_group = 1;
+        p->stages = simt_bk() == 8 ? 4 : 3; p->cta_group = 1;
         p->u_acc = std::ldexp(1.0f, -24); p->lambda1 = 16.0f; p->lambda2 = 32.0f;
     } else {
         const int bk = dtype == FTGEMM_TF32 ? 32 : 64;
         const int64_t tiles256 = ((M + 124) / 125) * ((N + 251) / 252);
-        const bool small = tiles256 < 2 * kNumSMsB200 || N <= 512;
+        // skinny operands (cfg4): one check tile across the narrow dimension, so
+        // the long operand streams through each SM once -- N <= 252: one
+        // 252-column tile; M <= 250: a CTA pair (2 x 125 rows) per unit
+        const bool skinny_n = N <= 252;
+        const bool skinny_m = M <= 250 && !skinny_n;
+        const bool small = !skinny_n && !skinny_m && (tiles256 < 2 * kNumSMsB200 || N <= 512);
         const int bn = small ? 128 : 256;
         p->shape_class = small ? FTGEMM_SHAPE_SMALL_N : FTGEMM_SHAPE_SQUARE;
         p->bm = 128; p->bn = bn; p->bk = bk;
         p->check_tile_m = 125; p->check_tile_n = bn - 4;
         p->off_tile_m = 128; p->off_tile_n = bn;
         // CTA pairs (cta_group::2, M = 256 per MMA) halve the B tile each SM
-        // loads; measured on B200 (profiles/cg_sweep_r1.txt) they pay off for
-        // the large-tile class with enough K to amortise the pair handshake
-        // (BF16 K >= 2048, TF32 K >= 1024) and lose on K = 128 and M = 128
+        // loads; measured on B200 (profiles/r1_sweep.md, the CG sweep) they pay
+        // off for the large-tile class with enough K to amortise the pair
+        // handshake (BF16 K >= 2048, TF32 K >= 1024) and lose on K = 128 shapes
         const int64_t tiles_m125 = (M + 124) / 125;
-        int cg = (bn == 256 && tiles_m125 >= 4 && (K >= 2048 || (dtype == FTGEMM_TF32 && K >= 1024))) ? 2 : 1;
+        int cg = (bn == 256 && ((tiles_m125 >= 4 && (K >= 2048 || (dtype == FTGEMM_TF32 && K >= 1024))) ||
+                                (skinny_m && K >= 1024))) ? 2 : 1;
         if (const char* e = getenv("FTGEMM_CG")) cg = atoi(e) == 2 ? 2 : 1;
         p->cta_group = cg;
         const int elt = dtype == FTGEMM_TF32 ? 4 : 2;

@@ -81,9 +81,15 @@ def test_plan_table(F, dtype):
     assert p.tiles_m == -(-8192 // p.check_tile_m) and p.tiles_n == -(-8192 // p.check_tile_n)
     assert 0 < p.enc_b_offset < p.enc_bytes and p.enc_b_offset + p.enc_b_bytes == p.enc_bytes
     assert p.report_bytes > 0 and p.max_events == 4096
-    small = F.plan(dtype, 128, 16384, 16384)
     if dtype != "f32_simt":
-        assert small.bn == 128 and small.shape_class == 1
+        small = F.plan(dtype, 2048, 2048, 2048)          # too few 125 x 252 tiles for 2 waves
+        assert small.bn == 128 and small.shape_class == 1 and small.cta_group == 1
+        sm = F.plan(dtype, 128, 16384, 16384)             # skinny M: one CTA pair per unit
+        assert sm.bn == 256 and sm.cta_group == 2 and sm.tiles_m == 2
+        sn = F.plan(dtype, 16384, 128, 16384)             # skinny N: a single check-tile column
+        assert sn.bn == 256 and sn.tiles_n == 1
+        big = F.plan(dtype, 8192, 8192, 8192)
+        assert big.cta_group == 2 and big.stages >= 4
 
 
 def test_plan_errors(F):

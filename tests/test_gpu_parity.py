@@ -215,6 +215,28 @@ def test_false_positive_sweep(dtype):
         assert c.counts["tiles_checked"] == c.plan.tiles_m * c.plan.tiles_n
 
 
+# ------------------------------------------------------- skinny shapes -----
+
+@pytest.mark.parametrize("dtype", ["tf32", "bf16"])
+@pytest.mark.parametrize("shape", [(250, 3000, 1024), (3000, 200, 1024), (128, 2600, 2048)],
+                         ids=["m250", "n200", "m128"])
+def test_skinny_shapes(dtype, shape):
+    """cfg4-style skinny operands get one check tile across the narrow
+    dimension (N <= 252: a single 252-column tile; M <= 250: a CTA pair per
+    unit); faults in both CTAs of the pair / anywhere in the narrow tile."""
+    F = ftmod()
+    M, N, K = shape
+    plan = F.plan(dtype, M, N, K)
+    assert plan.bn == 256 and (plan.tiles_n == 1 if N <= 252 else plan.cta_group == 2)
+    A, B, _ = synth.problem(M, N, K, dtype=odt(dtype))
+    inj = detectable_sites(dtype, 6, M, N, K, plan, A, B, seed=41)
+    c = Case(dtype, M, N, K, injections=inj, alpha=1.0, beta=0.5)
+    assert c.counts_match() and c.events_match(), (c.counts, c.ref.counts)
+    assert c.counts["corrected"] == len(inj) and c.fro() < TOL[dtype]
+    off = Case(dtype, M, N, K, ft=F.FT_OFF, alpha=1.0, beta=0.5)
+    assert off.fro() < TOL[dtype]
+
+
 # ------------------------------------------ online verification every K_s ---
 
 @pytest.mark.parametrize("cg", [1, 2])
