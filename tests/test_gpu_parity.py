@@ -215,6 +215,56 @@ def test_false_positive_sweep(dtype):
         assert c.counts["tiles_checked"] == c.plan.tiles_m * c.plan.tiles_n
 
 
+# ------------------------------------------- multi-GPU partition invariant --
+
+@pytest.mark.parametrize("dtype,shape", [("bf16", (4000, 8192, 2048)), ("tf32", (2000, 3000, 1024)),
+                                         ("f32_simt", (1000, 1024, 512))])
+def test_partition_invariance(dtype, shape):
+    """the M-block partition of paper_2305_01024_b200.distributed
+    (whole check tiles per rank, B shared) gives, rank by rank, C and event
+    positions bit-identical to the single-GPU run.  The ranks are run one
+    after another on one GPU with the real kernels (the process-group plumbing
+    is covered by tests/test_distributed.py on gloo)."""
+    import torch
+    F = ftmod()
+    from paper_2305_01024_b200.distributed import row_partition
+    M, N, K = shape
+    A, B, Cin = synth.problem(M, N, K, dtype=odt(dtype))
+    full_plan = F.plan(dtype, M, N, K)
+    tm = full_plan.check_tile_m
+    inj = detectable_sites(dtype, 6, M, N, K, full_plan, A, B, seed=51)
+    Ad, Bd = synth.to_torch(A, odt(dtype)).cuda(), synth.to_torch(B, odt(dtype)).cuda()
+    g = F.FTGemm(dtype, M, N, K)
+    Cf = synth.to_torch(Cin, odt(dtype)).cuda()
+    g.encode(Ad, Bd)
+    g.run(Ad, Bd, Cf, alpha=1.0, beta=0.5, injections=inj)
+    torch.cuda.synchronize()
+    _, ev_full = g.report()
+    key = lambda e: (e["tile_m"], e["tile_n"], e["kind"], e["row"], e["col"], e["n_rows"], e["n_cols"])
+    for world in (2, 3):
+        parts = row_partition(M, world, tm)
+        Cp, evs = [], []
+        for row0, rows in parts:
+            gp = F.FTGemm(dtype, rows, N, K)
+            assert (gp.plan.bn, gp.plan.cta_group, gp.plan.check_tile_m, gp.plan.check_tile_n) == \
+                (full_plan.bn, full_plan.cta_group, full_plan.check_tile_m, full_plan.check_tile_n)
+            mine = [(r - row0, c, k, b, m, tg, ad) for (r, c, k, b, m, tg, ad) in inj if row0 <= r < row0 + rows]
+            Cd = synth.to_torch(Cin[row0:row0 + rows], odt(dtype)).cuda()
+            Ar = Ad[row0:row0 + rows].contiguous()
+            gp.encode(Ar, Bd)
+            gp.run(Ar, Bd, Cd, alpha=1.0, beta=0.5, injections=mine)
+            torch.cuda.synchronize()
+            _, e = gp.report()
+            for x in e:
+                x = dict(x)
+                x["row"] += row0 if x["row"] >= 0 else 0
+                x["tile_m"] += row0 // tm
+                evs.append(x)
+            Cp.append(Cd)
+        assert torch.equal(torch.cat(Cp), Cf), world
+        assert sorted(map(key, evs)) == sorted(map(key, ev_full)), world
+
+
 # ------------------------------------------------------- skinny shapes -----
 
 @pytest.mark.parametrize("dtype", ["tf32", "bf16"])
