@@ -86,6 +86,23 @@ typedef struct ftgemm_inject {
     float   addend;     /* for FTGEMM_INJ_ADD */
 } ftgemm_inject_t;      /* 40 bytes */
 
+/* ---- run with the A-side encode inside the GEMM kernel -----------------------
+ * SURVEY 8(f) row 1, the paper's threadblock-level fusion of the checksum
+ * encoding into the prefetch stage.  As ftgemm_run, but the
+ * column checksum of A (Eq. 1: e^T A per check tile, its exact split into the
+ * operand format) and the threshold's row / tile norms are computed by the
+ * kernel from the A tiles it stages anyway, so enc_ws needs only the B part
+ * (ftgemm_encode which = 2).  Runs one CTA per MMA (no CTA pairs).  Measured
+ * on B200 it is SLOWER than the separate encode pass for BF16 (the column sums
+ * on two spare warps cannot keep pace with the tensor core: 2x at 8192^2 x
+ * 1024), within 1.2x for TF32; kept as the paper's fusion for comparison.
+ * Tensor-core dtypes, ft_level DETECT, CORRECT or DETECT_ROWS; UNSUPPORTED for
+ * F32_SIMT, FT_OFF and the online-interval mode.                             */
+FTGEMM_API int ftgemm_run_fused(int dtype, int64_t M, int64_t N, int64_t K, float alpha,
+               const void* A, int64_t lda, const void* B, int64_t ldb,
+               float beta, void* C, int64_t ldc, const void* enc_ws, int ft_level,
+               const ftgemm_inject_t* inj, int32_t n_inj, void* report_ws, void* stream);
+
 /* ---- online verification every K_s (outer-product online ABFT) ----------------
  * PAPER.md:170-173 (Chen's online scheme: the checksum relation holds after
  * every outer-product step, so "the online version, which corrects a single

@@ -250,13 +250,15 @@ int ftgemm_encode(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int
 
 static int run_impl(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const void* A, int64_t lda,
                     const void* B, int64_t ldb, float beta, void* C, int64_t ldc, const void* enc_ws, int ft_level,
-                    int64_t ks, const ftgemm_inject_t* inj, int32_t n_inj, void* report_ws, void* stream) {
+                    int64_t ks, int fuse_a, const ftgemm_inject_t* inj, int32_t n_inj, void* report_ws, void* stream) {
     int e = check_dims(dtype, M, N, K);
     if (e) return e;
     if (ks < 0) return fail(FTGEMM_ERR_INVALID_VALUE, "ks must be >= 0");
     if (ks > 0 && dtype == FTGEMM_F32_SIMT) return fail(FTGEMM_ERR_UNSUPPORTED, "online-interval mode: tensor-core dtypes");
     if (ks > 0 && (ft_level == FTGEMM_FT_OFF || ft_level == FTGEMM_FT_DETECT_ROWS))
         return fail(FTGEMM_ERR_INVALID_VALUE, "online-interval mode needs ft_level DETECT or CORRECT");
+    if (fuse_a && (dtype == FTGEMM_F32_SIMT || ks > 0 || ft_level == FTGEMM_FT_OFF))
+        return fail(FTGEMM_ERR_UNSUPPORTED, "in-kernel encode: tensor-core dtypes, FT on, end-of-K verification");
     if (!A || !B || !C) return fail(FTGEMM_ERR_INVALID_VALUE, "null A, B or C");
     if (lda < K || ldb < N || ldc < N) return fail(FTGEMM_ERR_INVALID_VALUE, "leading dimension too small");
     if (ft_level < FTGEMM_FT_OFF || ft_level > FTGEMM_FT_DETECT_ROWS) return fail(FTGEMM_ERR_INVALID_VALUE, "bad ft_level");
@@ -272,6 +274,9 @@ static int run_impl(int dtype, int64_t M, int64_t N, int64_t K, float alpha, con
     ftgemm_plan_t p;
     fill_plan(dtype, M, N, K, &p);
     if (ks > 0 && ks % p.bk) return fail(FTGEMM_ERR_INVALID_VALUE, "ks must be a multiple of plan.bk (%d)", p.bk);
+    // in-kernel encode: one CTA per MMA (a CTA pair would put a cluster-scope
+    // release of the peer's split rows on every k-block's critical path)
+    if (fuse_a) p.cta_group = 1;
     const bool ft = ft_level != FTGEMM_FT_OFF;
     const Geometry g = geometry(p, K);
     const EncLayout L = enc_layout(g, M, N);
@@ -368,6 +373,7 @@ static int run_impl(int dtype, int64_t M, int64_t N, int64_t K, float alpha, con
         a.group = tc_group(a.units_m, p.cta_group);
         a.ft_level = ft_level; a.alpha = alpha; a.beta = beta; a.C = C; a.ldc = ldc;
         a.ks_kb = ks > 0 ? (int)std::min<int64_t>(ks / p.bk, num_kb) : 0;
+        a.fuse_a = fuse_a;
         if (ft) {
             a.Y = enc + L.y; a.kp = g.kp;
             a.rownorm = (const float*)(enc + L.rownorm); a.colnorm = (const float*)(enc + L.colnorm);
@@ -389,7 +395,14 @@ static int run_impl(int dtype, int64_t M, int64_t N, int64_t K, float alpha, con
 int ftgemm_run(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const void* A, int64_t lda,
                const void* B, int64_t ldb, float beta, void* C, int64_t ldc, const void* enc_ws, int ft_level,
                const ftgemm_inject_t* inj, int32_t n_inj, void* report_ws, void* stream) {
-    return run_impl(dtype, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, enc_ws, ft_level, 0, inj, n_inj, report_ws,
+    return run_impl(dtype, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, enc_ws, ft_level, 0, 0, inj, n_inj, report_ws,
+                    stream);
+}
+
+int ftgemm_run_fused(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const void* A, int64_t lda,
+                     const void* B, int64_t ldb, float beta, void* C, int64_t ldc, const void* enc_ws, int ft_level,
+                     const ftgemm_inject_t* inj, int32_t n_inj, void* report_ws, void* stream) {
+    return run_impl(dtype, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, enc_ws, ft_level, 0, 1, inj, n_inj, report_ws,
                     stream);
 }
 
@@ -397,7 +410,7 @@ int ftgemm_run_online(int dtype, int64_t M, int64_t N, int64_t K, float alpha, c
                       const void* B, int64_t ldb, float beta, void* C, int64_t ldc, const void* enc_ws, int ft_level,
                       int64_t ks, const ftgemm_inject_t* inj, int32_t n_inj, void* report_ws, void* stream) {
     if (ks < 1) return fail(FTGEMM_ERR_INVALID_VALUE, "ks must be >= 1");
-    return run_impl(dtype, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, enc_ws, ft_level, ks, inj, n_inj, report_ws,
+    return run_impl(dtype, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, enc_ws, ft_level, ks, 0, inj, n_inj, report_ws,
                     stream);
 }
 

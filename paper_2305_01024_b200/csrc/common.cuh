@@ -42,6 +42,7 @@ struct TcArgs {
     int group;            // M-units per schedule group (tile_coords)
     int ft_level;
     int ks_kb;            // > 0: verify after every ks_kb k-blocks too (online-interval mode)
+    int fuse_a;           // 1: the A-side encode (split e^T A rows, row / tile norms) runs in the kernel
     float alpha, beta;
     void* C; int64_t ldc;
     const void* Y; int kp;

@@ -62,7 +62,8 @@ struct TcCfg {
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int STG_BYTES = 4 * 2 * 4096;     // per epilogue warpgroup (see below)
     static constexpr int EPI_BYTES = kEpiWG * STG_BYTES;
-    static constexpr int STAGE_FIT = (227 * 1024 - 1280 - EPI_BYTES) / (A_BYTES + B_BYTES);
+    static constexpr int MISC_BYTES = 2048;            // barriers, TMEM address, in-kernel-encode norms
+    static constexpr int STAGE_FIT = (227 * 1024 - 1024 - MISC_BYTES - EPI_BYTES) / (A_BYTES + B_BYTES);
     static constexpr int STAGES = STAGE_FIT < 8 ? STAGE_FIT : 8;
     static constexpr int BMD = FT ? BM - 3 : BM;   // data rows of a check tile
     static constexpr int BND = FT ? BN - 4 : BN;   // data cols of a check tile
@@ -78,7 +79,7 @@ struct TcCfg {
     static constexpr int GW = kTF32 ? 32 : 64;     // output columns per 128-byte store box
     static constexpr int NG = (BND + GW - 1) / GW; // store groups per tile
     static constexpr int LAST = BND - GW;          // start of the last group (overlaps the previous one by BND % GW)
-    static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 256;
+    static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + MISC_BYTES;
 };
 
 // Tile schedule: groups of G consecutive M-tiles are swept across all N-tiles
@@ -144,7 +145,13 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     uint64_t* inj_req = tm_empty + 2;   // [2]  mid-mainloop hand-off, per accumulator buffer
     uint64_t* inj_done = inj_req + 2;   // [2]
     uint64_t* cbar = inj_done + 2;      // [4 kEpiWG]  C_in tile loads (beta != 0), one per epilogue warp
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(cbar + 4 * kEpiWG);
+    uint64_t* afull = cbar + 4 * kEpiWG;  // [S]  in-kernel encode: this CTA's A tile landed
+    uint64_t* yrdy = afull + S;           // [S]  in-kernel encode: split rows of e^T A written (leader's)
+    uint64_t* nrdy = yrdy + S;            // [2]  in-kernel encode: row / tile norms of the tile written
+    uint64_t* nfree = nrdy + 2;           // [2]  ... and read by the epilogue (slot reusable)
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(nfree + 2);
+    float* nsq = reinterpret_cast<float*>(tmem_holder + 4);   // [2 acc][2 half][128] row sums of squares
+    float* acsq = nsq + 2 * 2 * 128;                          // [2 acc][2 half] sum of (e^T A)^2
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
@@ -173,6 +180,14 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             mbar_init(&inj_done[b], CG);
         }
         for (int w = 0; w < 4 * kEpiWG; ++w) mbar_init(&cbar[w], 1);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&afull[s], 1);
+            mbar_init(&yrdy[s], 2 * CG);         // both encoder warps of both CTAs
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&nrdy[b], 2);
+            mbar_init(&nfree[b], 4);
+        }
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc<Cfg::TMEM_COLS, CG>(tmem_holder);
@@ -190,7 +205,12 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             // row-major B.  B is N-major in BOXN-column boxes; with a CTA pair each
             // CTA loads half of the tile's columns.  All bytes of a stage (both CTAs)
             // are counted on the leader's full barrier.
-            constexpr uint32_t bytes_cta = FT ? (Cfg::BMD * 128 + Cfg::Y_BYTES + Cfg::B_BYTES) : (Cfg::A_BYTES + Cfg::B_BYTES);
+            // in-kernel encode (a.fuse_a): the A box lands on this CTA's own afull
+            // barrier (the encoder warps read it); rows 125..127 are written by
+            // the encoder warps instead of loaded
+            const bool fa = FT && a.fuse_a;
+            const uint32_t bytes_cta = !FT ? (Cfg::A_BYTES + Cfg::B_BYTES)
+                                     : fa ? Cfg::B_BYTES : (Cfg::BMD * 128 + Cfg::Y_BYTES + Cfg::B_BYTES);
             for (int u = cluster_id; u < a.num_units; u += num_clusters) {
                 int tmu, tj;
                 tile_coords(u, a.units_m, a.tiles_n, a.group, tmu, tj);
@@ -202,16 +222,20 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     if (leader) mbar_arrive_expect_tx(&full[s], CG * bytes_cta);
                     uint8_t* sa = stage_base + s * Cfg::STAGE_BYTES;
                     uint8_t* sb = sa + Cfg::A_BYTES;
+                    if (fa) {
+                        mbar_arrive_expect_tx(&afull[s], Cfg::BMD * 128);
+                        tma_load_2d(sa, &tmA, &afull[s], kb * Cfg::BK, row0);
+                    }
                     if constexpr (CG == 1) {
-                        tma_load_2d(sa, &tmA, &full[s], kb * Cfg::BK, row0);
-                        if constexpr (FT) tma_load_2d(sa + Cfg::BMD * 128, &tmY, &full[s], 0, ti * a.num_kb + kb);
+                        if (!fa) tma_load_2d(sa, &tmA, &full[s], kb * Cfg::BK, row0);
+                        if (FT && !fa) tma_load_2d(sa + Cfg::BMD * 128, &tmY, &full[s], 0, ti * a.num_kb + kb);
 #pragma unroll
                         for (int b = 0; b < Cfg::NBOX; ++b)
                             tma_load_2d(sb + b * Cfg::B_BOX_BYTES, &tmB, &full[s], colb + b * Cfg::BOXN, kb * Cfg::BK);
                     } else {
                         const uint32_t mb = smem_u32(&full[s]) & kPeerBitMask;
-                        tma_load_2d_pair(sa, &tmA, mb, kb * Cfg::BK, row0);
-                        if constexpr (FT) tma_load_2d_pair(sa + Cfg::BMD * 128, &tmY, mb, 0, ti * a.num_kb + kb);
+                        if (!fa) tma_load_2d_pair(sa, &tmA, mb, kb * Cfg::BK, row0);
+                        if (FT && !fa) tma_load_2d_pair(sa + Cfg::BMD * 128, &tmY, mb, 0, ti * a.num_kb + kb);
 #pragma unroll
                         for (int b = 0; b < Cfg::NBOX / CG; ++b)
                             tma_load_2d_pair(sb + b * Cfg::B_BOX_BYTES, &tmB, mb, colb + b * Cfg::BOXN, kb * Cfg::BK);
@@ -243,6 +267,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 }
                 for (int kb = 0; kb < a.num_kb; ++kb) {
                     mbar_wait(&full[s], ph);
+                    if (FT && a.fuse_a) mbar_wait(&yrdy[s], ph);    // both CTAs' A tiles + split rows ready
                     tc_fence_after();
                     const uint32_t sa = smem_u32(stage_base + s * Cfg::STAGE_BYTES);
                     const uint32_t sb = sa + Cfg::A_BYTES;
@@ -271,6 +296,118 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             }
         }
         __syncwarp();
+    } else if (warp == 2 || warp == 3) {
+        // ------------------------------------- in-kernel encode of A -------
+        // (the paper's threadblock-level fusion of the
+        // checksum encoding into the prefetch stage.)  Per k-block,
+        // from the A tile in shared memory: e^T A_i over the 125 data rows, its
+        // exact 3-term split written as MMA rows 125..127 (SWIZZLE_128B), and the
+        // running row sums of squares / sum of (e^T A)^2 of the threshold
+        // (R1).  Warp 2 covers 16-byte chunks 0..3 of each 128-byte
+        // row, warp 3 chunks 4..7; lane = (row group rg, chunk cq).
+        if (FT && a.fuse_a) {
+            constexpr int EPC = kTF32 ? 4 : 8;            // elements per 16-byte chunk
+            const int half = warp - 2;
+            const int cq = lane & 3, rg = lane >> 2;
+            const int c = 4 * half + cq;                  // 16-byte chunk of the row
+            auto arrive_yrdy = [&](uint64_t* bar) {
+                if (CG == 1 || leader) mbar_arrive(bar);
+                else mbar_arrive_cluster(mapa_shared(smem_u32(bar), 0));
+            };
+            int s = 0; uint32_t ph = 0; int lt = 0;
+            for (int u = cluster_id; u < a.num_units; u += num_clusters, ++lt) {
+                float rsq[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) rsq[i] = 0.0f;
+                float asq = 0.0f;
+                for (int kb = 0; kb < a.num_kb; ++kb) {
+                    mbar_wait(&afull[s], ph);
+                    uint8_t* sa = stage_base + s * Cfg::STAGE_BYTES;
+                    // column sums and squares with paired FP32 ops (FADD2 / FFMA2)
+                    float2 cs2[EPC / 2];
+#pragma unroll
+                    for (int j = 0; j < EPC / 2; ++j) cs2[j] = make_float2(0.0f, 0.0f);
+                    uint4 v[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int r = rg + 8 * i;
+                        v[i] = r < Cfg::BMD ? ld_shared_v4(sa + r * 128 + ((c ^ (r & 7)) << 4)) : make_uint4(0u, 0u, 0u, 0u);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const uint32_t wd[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+                        float2 q2 = make_float2(0.0f, 0.0f);
+#pragma unroll
+                        for (int j = 0; j < EPC / 2; ++j) {
+                            float2 x;
+                            if constexpr (kTF32) {
+                                x = make_float2(tf32_trunc(__uint_as_float(wd[2 * j])), tf32_trunc(__uint_as_float(wd[2 * j + 1])));
+                            } else {
+                                x = make_float2(__uint_as_float(wd[j] << 16), __uint_as_float(wd[j] & 0xFFFF0000u));
+                            }
+                            cs2[j] = __fadd2_rn(cs2[j], x);
+                            q2 = __ffma2_rn(x, x, q2);
+                        }
+                        rsq[i] += q2.x + q2.y;
+                    }
+                    float cs[EPC];
+#pragma unroll
+                    for (int j = 0; j < EPC / 2; ++j) { cs[2 * j] = cs2[j].x; cs[2 * j + 1] = cs2[j].y; }
+#pragma unroll
+                    for (int j = 0; j < EPC; ++j) {
+                        cs[j] += __shfl_xor_sync(0xffffffffu, cs[j], 4);
+                        cs[j] += __shfl_xor_sync(0xffffffffu, cs[j], 8);
+                        cs[j] += __shfl_xor_sync(0xffffffffu, cs[j], 16);
+                    }
+                    if (rg == 0) {
+                        // columns of this chunk: split rows 125..127 (operand format)
+                        uint32_t pk[3][4];
+#pragma unroll
+                        for (int j = 0; j < EPC; ++j) {
+                            const int k = kb * Cfg::BK + c * EPC + j;
+                            const float sv = k < a.K ? cs[j] : 0.0f;
+                            asq = fmaf(sv, sv, asq);
+                            float hi, mid, lo;
+                            split3<kTF32 ? 1 : 0>(sv, hi, mid, lo);
+                            const float parts[3] = {hi, mid, lo};
+#pragma unroll
+                            for (int r3 = 0; r3 < 3; ++r3) {
+                                if constexpr (kTF32) pk[r3][j] = __float_as_uint(parts[r3]);
+                                else if (j & 1) pk[r3][j >> 1] |= (uint32_t)f32_to_bf16_rn(parts[r3]) << 16;
+                                else pk[r3][j >> 1] = (uint32_t)f32_to_bf16_rn(parts[r3]);
+                            }
+                        }
+#pragma unroll
+                        for (int r3 = 0; r3 < 3; ++r3) {
+                            const int row = Cfg::BMD + r3;
+                            st_shared_v4(sa + row * 128 + ((c ^ (row & 7)) << 4), pk[r3][0], pk[r3][1], pk[r3][2], pk[r3][3]);
+                        }
+                    }
+                    fence_proxy_async_smem();               // generic writes -> tensor-core reads
+                    __syncwarp();
+                    if (lane == 0) arrive_yrdy(&yrdy[s]);
+                    if (++s == S) { s = 0; ph ^= 1; }
+                }
+                // tile end: row sums of squares (4 lanes per row group) and sum of (e^T A)^2
+                const int acc = lt & 1;
+                if (lt >= 2) mbar_wait(&nfree[acc], ((lt >> 1) & 1) ^ 1);   // tile lt-2 read its norms
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    rsq[i] += __shfl_xor_sync(0xffffffffu, rsq[i], 1);
+                    rsq[i] += __shfl_xor_sync(0xffffffffu, rsq[i], 2);
+                }
+                asq += __shfl_xor_sync(0xffffffffu, asq, 1);
+                asq += __shfl_xor_sync(0xffffffffu, asq, 2);
+                if (cq == 0) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        if (rg + 8 * i < 128) nsq[(acc * 2 + half) * 128 + rg + 8 * i] = rsq[i];
+                }
+                if (lane == 0) acsq[acc * 2 + half] = asq;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&nrdy[acc]);     // release: the epilogue of this tile may read them
+            }
+        }
     } else if (warp >= 4) {
         // ----------------------------------------------------- epilogue -----
         const int wg = (warp - 4) >> 2;          // epilogue warpgroup (owns accumulator buffer wg when kEpiWG == 2)
@@ -313,9 +450,11 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             // norms for this tile's thresholds, fetched before the accumulator is ready
             float nrow = 0.f, nbr = 0.f, nac = 0.f, ncol[2] = {0.f, 0.f};
             if (FT && has_rows) {
-                if (rloc < bm) nrow = __ldg(a.rownorm + r0 + rloc);
+                if (!a.fuse_a) {
+                    if (rloc < bm) nrow = __ldg(a.rownorm + r0 + rloc);
+                    nac = __ldg(a.acnorm + ti);
+                }
                 nbr = __ldg(a.brnorm + tj);
-                nac = __ldg(a.acnorm + ti);
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
                     if (et + 128 * h < bn) ncol[h] = __ldg(a.colnorm + c0 + et + 128 * h);
@@ -535,6 +674,14 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 
             mbar_wait(&tm_full[acc], accph);
             tc_fence_after();
+            if (FT && a.fuse_a) {
+                // norms of the in-kernel encode (the tile's own rows)
+                mbar_wait(&nrdy[acc], accph);
+                nrow = sqrtf(nsq[acc * 256 + rloc] + nsq[acc * 256 + 128 + rloc]);
+                nac = sqrtf(acsq[acc * 2] + acsq[acc * 2 + 1]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&nfree[acc]);
+            }
             if (!has_rows) {                                   // padding half of the last pair row
                 __syncwarp();
                 if (lane == 0) arrive_leader(&tm_empty[acc]);

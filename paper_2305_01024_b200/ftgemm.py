@@ -59,7 +59,7 @@ class Cost(C.Structure):
                 ("online_expected_runs", C.c_double), ("offline_expected_runs", C.c_double)]
 
 
-SYMBOLS = ("ftgemm_plan", "ftgemm_encode", "ftgemm_run", "ftgemm_run_online", "ftgemm_run_offline", "ftgemm_cost_model",
+SYMBOLS = ("ftgemm_plan", "ftgemm_encode", "ftgemm_run", "ftgemm_run_fused", "ftgemm_run_online", "ftgemm_run_offline", "ftgemm_cost_model",
            "ftgemm_nonfused_workspace", "ftgemm_run_nonfused",
            "ftgemm_report", "ftgemm_report_reset", "ftgemm_last_error", "ftgemm_version", "ftgemm_device_arch")
 
@@ -79,6 +79,7 @@ def lib():
         L.ftgemm_encode.argtypes = [C.c_int, i64, i64, i64, vp, i64, vp, i64, vp, C.c_int, vp]
         L.ftgemm_run.argtypes = [C.c_int, i64, i64, i64, C.c_float, vp, i64, vp, i64, C.c_float, vp, i64,
                                  vp, C.c_int, vp, i32, vp, vp]
+        L.ftgemm_run_fused.argtypes = L.ftgemm_run.argtypes
         L.ftgemm_run_online.argtypes = [C.c_int, i64, i64, i64, C.c_float, vp, i64, vp, i64, C.c_float, vp, i64,
                                         vp, C.c_int, i64, vp, i32, vp, vp]
         L.ftgemm_run_offline.argtypes = [C.c_int, i64, i64, i64, C.c_float, vp, i64, vp, i64, C.c_float, vp, i64,
@@ -181,16 +182,19 @@ def _inj_array(injections):
 
 def run(dtype, A: torch.Tensor, B: torch.Tensor, C_: torch.Tensor, *, alpha: float = 1.0, beta: float = 0.0,
         enc_ws: torch.Tensor | None = None, ft_level: int = FT_CORRECT, injections=(),
-        report_ws: torch.Tensor | None = None, stream=None):
+        report_ws: torch.Tensor | None = None, stream=None, fuse_a: bool = False):
+    """fuse_a: the A-side encode runs inside the GEMM kernel (ftgemm_run_fused);
+    enc_ws then needs only the B part."""
     M, K = A.shape
     N = B.shape[1]
     arr, n = _inj_array(injections)
-    _check(lib().ftgemm_run(_dt(dtype), M, N, K, alpha, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0),
+    fn = lib().ftgemm_run_fused if fuse_a else lib().ftgemm_run
+    _check(fn(_dt(dtype), M, N, K, alpha, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0),
                             beta, C_.data_ptr(), C_.stride(0),
                             enc_ws.data_ptr() if enc_ws is not None else None, ft_level,
                             C.cast(arr, C.c_void_p) if arr is not None else None, n,
                             report_ws.data_ptr() if report_ws is not None else None, _stream(stream)),
-           "ftgemm_run")
+           "ftgemm_run_fused" if fuse_a else "ftgemm_run")
 
 
 def run_offline(dtype, A: torch.Tensor, B: torch.Tensor, C_: torch.Tensor, *, alpha: float = 1.0,
@@ -294,9 +298,9 @@ class FTGemm:
     def encode(self, A=None, B=None, which: int = 3, stream=None):
         encode(self.dtype, A, B, self.enc_ws, M=self.M, N=self.N, K=self.K, which=which, stream=stream)
 
-    def run(self, A, B, C_, *, alpha=1.0, beta=0.0, ft_level=FT_CORRECT, injections=(), stream=None):
+    def run(self, A, B, C_, *, alpha=1.0, beta=0.0, ft_level=FT_CORRECT, injections=(), stream=None, fuse_a=False):
         run(self.dtype, A, B, C_, alpha=alpha, beta=beta, enc_ws=self.enc_ws, ft_level=ft_level,
-            injections=injections, report_ws=self.report_ws, stream=stream)
+            injections=injections, report_ws=self.report_ws, stream=stream, fuse_a=fuse_a)
 
     def run_online(self, A, B, C_, *, ks, alpha=1.0, beta=0.0, ft_level=FT_CORRECT, injections=(), stream=None):
         run_online(self.dtype, A, B, C_, ks=ks, alpha=alpha, beta=beta, enc_ws=self.enc_ws, ft_level=ft_level,

@@ -215,6 +215,59 @@ def test_false_positive_sweep(dtype):
         assert c.counts["tiles_checked"] == c.plan.tiles_m * c.plan.tiles_n
 
 
+# ------------------------------------------------ in-kernel encode of A ----
+
+@pytest.mark.parametrize("cg", [1, 2])
+@pytest.mark.parametrize("dtype", ["tf32", "bf16"])
+@pytest.mark.parametrize("shape", [(845, 600, 1000), (1000, 10896, 2048)], ids=["bn128", "bn256"])
+def test_fused_encode_parity(dtype, cg, shape, monkeypatch):
+    """ftgemm_run_fused: with only B encoded,
+    the kernel derives e^T A, its split rows and the row / tile norms itself;
+    events, counts and C as the oracle; C bit-identical to the separately
+    encoded run except at corrected elements (same tiles, same k order)."""
+    import torch
+    monkeypatch.setenv("FTGEMM_CG", str(cg))
+    F = ftmod()
+    M, N, K = shape
+    A, B, Cin = synth.problem(M, N, K, dtype=odt(dtype))
+    plan = F.plan(dtype, M, N, K)
+    assert plan.cta_group == cg
+    tm, tn = plan.check_tile_m, plan.check_tile_n
+    inj = detectable_sites(dtype, 8, M, N, K, plan, A, B, seed=61)
+    inj.append((plan.tiles_m * tm - tm + 2, 3, 40, 0, oracle.INJ_ADD, 0, 800.0))          # last (ragged) tile row
+    Ad, Bd = synth.to_torch(A, odt(dtype)).cuda(), synth.to_torch(B, odt(dtype)).cuda()
+    g = F.FTGemm(dtype, M, N, K)
+    g.enc_ws.fill_(0xFF)                          # the A part must not be read
+    g.encode(None, Bd, which=2)
+    Cf = synth.to_torch(Cin, odt(dtype)).cuda()
+    g.run(Ad, Bd, Cf, alpha=1.5, beta=-0.5, injections=inj, fuse_a=True)
+    torch.cuda.synchronize()
+    counts, events = g.report()
+    ref = oracle.ftgemm(A, B, Cin, alpha=1.5, beta=-0.5, out=odt(dtype), tile_m=tm, tile_n=tn, bk=plan.bk,
+                        u_acc=plan.u_acc, lambda1=plan.lambda1, lambda2=plan.lambda2, injections=inj)
+    keys = ("tiles_checked", "tiles_detected", "corrected", "checksum_only", "uncorrectable", "located", "events")
+    assert all(int(counts[k]) == int(ref.counts[k]) for k in keys), (counts, ref.counts)
+    ek = lambda evs: sorted((e["tile_m"], e["tile_n"], e["kind"], e["row"], e["col"], e["n_rows"], e["n_cols"])
+                            for e in evs)
+    assert ek(events) == ek(ref.events)
+    assert frob(Cf.float().cpu().numpy(), ref.C) < TOL[dtype]
+    # against the separately encoded run: identical away from the corrected elements
+    g2 = F.FTGemm(dtype, M, N, K)
+    g2.encode(Ad, Bd)
+    C2 = synth.to_torch(Cin, odt(dtype)).cuda()
+    g2.run(Ad, Bd, C2, alpha=1.5, beta=-0.5, injections=inj)
+    torch.cuda.synchronize()
+    same = (Cf == C2)
+    for e in events:
+        same[e["row"], e["col"]] = True
+    assert bool(same.all())
+    # fault-free: no detections (threshold margins hold with the in-kernel norms)
+    g.reset()
+    g.run(Ad, Bd, Cf, injections=(), fuse_a=True)
+    c0, _ = g.report()
+    assert c0["tiles_detected"] == 0 and c0["tiles_checked"] == plan.tiles_m * plan.tiles_n
+
+
 # ------------------------------------------- multi-GPU partition invariant --
 
 @pytest.mark.parametrize("dtype,shape", [("bf16", (4000, 8192, 2048)), ("tf32", (2000, 3000, 1024)),
