@@ -349,7 +349,11 @@ static int run_impl(int dtype, int64_t M, int64_t N, int64_t K, float alpha, con
 #else
         if ((e = make_map(&mA, dt, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * elt, (uint32_t)p.bk, (uint32_t)bmd))) return e;
 #endif
+#if defined(FTGEMM_EXP_B_DIRECT)
+        if (false) {
+#else
         if (ft) {
+#endif
             // the encoded operand B^r (N-major, kp rows of tiles_n * bn) from the encode workspace
             const uint64_t ldt = (uint64_t)g.tiles_n * p.bn;
             if ((e = make_map(&mB, dt, enc + L.bt, ldt, (uint64_t)g.kp, ldt * elt, boxn, (uint32_t)p.bk,

@@ -209,8 +209,13 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             // barrier (the encoder warps read it); rows 125..127 are written by
             // the encoder warps instead of loaded
             const bool fa = FT && a.fuse_a;
+#if defined(FTGEMM_EXP_A128)
+            // timing experiment: FT kernel fed like FT off (one 128-row A box, no split rows)
+            const uint32_t bytes_cta = Cfg::A_BYTES + Cfg::B_BYTES;
+#else
             const uint32_t bytes_cta = !FT ? (Cfg::A_BYTES + Cfg::B_BYTES)
                                      : fa ? Cfg::B_BYTES : (Cfg::BMD * 128 + Cfg::Y_BYTES + Cfg::B_BYTES);
+#endif
             for (int u = cluster_id; u < a.num_units; u += num_clusters) {
                 int tmu, tj;
                 tile_coords(u, a.units_m, a.tiles_n, a.group, tmu, tj);
@@ -228,14 +233,18 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     }
                     if constexpr (CG == 1) {
                         if (!fa) tma_load_2d(sa, &tmA, &full[s], kb * Cfg::BK, row0);
+#if !defined(FTGEMM_EXP_A128)
                         if (FT && !fa) tma_load_2d(sa + Cfg::BMD * 128, &tmY, &full[s], 0, ti * a.num_kb + kb);
+#endif
 #pragma unroll
                         for (int b = 0; b < Cfg::NBOX; ++b)
                             tma_load_2d(sb + b * Cfg::B_BOX_BYTES, &tmB, &full[s], colb + b * Cfg::BOXN, kb * Cfg::BK);
                     } else {
                         const uint32_t mb = smem_u32(&full[s]) & kPeerBitMask;
                         if (!fa) tma_load_2d_pair(sa, &tmA, mb, kb * Cfg::BK, row0);
+#if !defined(FTGEMM_EXP_A128)
                         if (FT && !fa) tma_load_2d_pair(sa + Cfg::BMD * 128, &tmY, mb, 0, ti * a.num_kb + kb);
+#endif
 #pragma unroll
                         for (int b = 0; b < Cfg::NBOX / CG; ++b)
                             tma_load_2d_pair(sb + b * Cfg::B_BOX_BYTES, &tmB, mb, colb + b * Cfg::BOXN, kb * Cfg::BK);
@@ -252,7 +261,10 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             auto commit = [&](uint64_t* bar) {
                 if constexpr (CG == 2) umma_commit_pair(bar, pair); else umma_commit(bar);
             };
-            int s = 0; uint32_t ph = 0; uint32_t injph[2] = {0, 0};
+            int s = 0; uint32_t ph = 0;
+            uint32_t injph0 = 0, injph1 = 0;            // hand-off phases per accumulator buffer
+            const bool fuse = FT && a.fuse_a;
+            const int ks_kb = a.ks_kb, nkb = a.num_kb;
             int lt = 0;
             for (int t = cluster_id; t < a.num_units; t += num_clusters, ++lt) {
                 const int acc = lt & 1;
@@ -265,33 +277,57 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     ii = inj_lower(a.inj, a.n_inj, t);
                     ie = inj_lower(a.inj, a.n_inj, t + 1);
                 }
-                for (int kb = 0; kb < a.num_kb; ++kb) {
-                    mbar_wait(&full[s], ph);
-                    if (FT && a.fuse_a) mbar_wait(&yrdy[s], ph);    // both CTAs' A tiles + split rows ready
-                    tc_fence_after();
-                    const uint32_t sa = smem_u32(stage_base + s * Cfg::STAGE_BYTES);
-                    const uint32_t sb = sa + Cfg::A_BYTES;
-#pragma unroll
-                    for (int kk = 0; kk < Cfg::BK / Cfg::UK; ++kk) {
-                        const uint64_t ad = smem_desc_sw128(sa + kk * 32, 16, 1024);
-                        // B is N-major: bf16 -> SW128 (8-row atoms), tf32 -> SW128_BASE32B (4-row atoms)
-                        const uint64_t bd = kTF32 ? smem_desc_sw128<1>(sb + kk * Cfg::UK * 128, Cfg::B_BOX_BYTES, 512)
-                                                  : smem_desc_sw128<2>(sb + kk * Cfg::UK * 128, Cfg::B_BOX_BYTES, 1024);
-                        umma<kTF32, CG>(d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                // next k-block that needs a mid-mainloop hand-off (a fault, or the
+                // end of a K_s step); the hot loop tests only kb == evt -- the MMA
+                // issue loop is latency-critical (measured: per-k-block flag and
+                // modulo tests here cost 9 % of the tensor pipe at 8192^3)
+                auto next_event = [&](int after) -> int {
+                    int e = ii < ie ? a.inj[ii].kb : 0x7fffffff;
+                    if (ks_kb > 0) {
+                        const int c = ((after + 1) / ks_kb + 1) * ks_kb - 1;
+                        if (c < nkb - 1 && c < e) e = c;
                     }
-                    commit(&empty[s]);
-                    const bool chk = a.ks_kb > 0 && (kb + 1) % a.ks_kb == 0 && kb + 1 < a.num_kb;
-                    if (FT && ((ii < ie && a.inj[ii].kb == kb) || chk)) {
-                        // hand the accumulator to the epilogue warps (of both CTAs) for the
-                        // fault(s) of this k-block and / or the check closing a K_s step
-                        commit(&inj_req[acc]);
-                        mbar_wait(&inj_done[acc], injph[acc]);
-                        injph[acc] ^= 1;
+                    return e;
+                };
+                int evt = FT ? next_event(-1) : 0x7fffffff;
+                // two instantiations of the k-loop: the lean one (no hand-off, no
+                // in-kernel encode -- the common case) carries no per-k-block tests
+                auto kloop = [&](auto general_c) {
+                    constexpr bool kGeneral = decltype(general_c)::value;
+                    for (int kb = 0; kb < nkb; ++kb) {
+                        mbar_wait(&full[s], ph);
+                        if constexpr (kGeneral) {
+                            if (fuse) mbar_wait(&yrdy[s], ph);     // both CTAs' A tiles + split rows ready
+                        }
                         tc_fence_after();
-                        while (ii < ie && a.inj[ii].kb == kb) ++ii;
+                        const uint32_t sa = smem_u32(stage_base + s * Cfg::STAGE_BYTES);
+                        const uint32_t sb = sa + Cfg::A_BYTES;
+#pragma unroll
+                        for (int kk = 0; kk < Cfg::BK / Cfg::UK; ++kk) {
+                            const uint64_t ad = smem_desc_sw128(sa + kk * 32, 16, 1024);
+                            // B is N-major: bf16 -> SW128 (8-row atoms), tf32 -> SW128_BASE32B (4-row atoms)
+                            const uint64_t bd = kTF32 ? smem_desc_sw128<1>(sb + kk * Cfg::UK * 128, Cfg::B_BOX_BYTES, 512)
+                                                      : smem_desc_sw128<2>(sb + kk * Cfg::UK * 128, Cfg::B_BOX_BYTES, 1024);
+                            umma<kTF32, CG>(d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                        }
+                        commit(&empty[s]);
+                        if constexpr (kGeneral) {
+                            if (FT && kb == evt) {
+                                // hand the accumulator to the epilogue warps (of both CTAs) for the
+                                // fault(s) of this k-block and / or the check closing a K_s step
+                                commit(&inj_req[acc]);
+                                mbar_wait(&inj_done[acc], acc ? injph1 : injph0);
+                                if (acc) injph1 ^= 1; else injph0 ^= 1;
+                                tc_fence_after();
+                                while (ii < ie && a.inj[ii].kb == kb) ++ii;
+                                evt = next_event(kb);
+                            }
+                        }
+                        if (++s == S) { s = 0; ph ^= 1; }
                     }
-                    if (++s == S) { s = 0; ph ^= 1; }
-                }
+                };
+                if (FT && (fuse || evt != 0x7fffffff)) kloop(std::true_type{});
+                else kloop(std::false_type{});
                 commit(&tm_full[acc]);
             }
         }
@@ -416,7 +452,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
         const int et = threadIdx.x - 128 - 128 * wg;   // 0..127
         const uint32_t ebar = 1 + wg;            // named barrier of this warpgroup
-        uint32_t injph[2] = {0, 0}, cph = 0, gcount = 0;   // gcount: store groups issued by this warp
+        uint32_t injph0 = 0, injph1 = 0, cph = 0, gcount = 0;   // gcount: store groups issued by this warp
         uint64_t* cbw = &cbar[4 * wg + ew];
         uint8_t* stg = stg0 + wg * Cfg::STG_BYTES;
         float* colsum = reinterpret_cast<float*>(stg);                            // [4][BN] (aliases staging)
@@ -630,8 +666,8 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     const int kb_c = next_chk < a.num_kb - 1 ? next_chk : 0x7fffffff;
                     const int kb = min(kb_f, kb_c);
                     if (kb == 0x7fffffff) break;
-                    mbar_wait(&inj_req[acc], injph[acc]);
-                    injph[acc] ^= 1;
+                    mbar_wait(&inj_req[acc], acc ? injph1 : injph0);
+                    if (acc) injph1 ^= 1; else injph0 ^= 1;
                     tc_fence_after();
                     for (; ii < ie && a.inj[ii].kb == kb; ++ii) {
                         const DevInject f = a.inj[ii];
@@ -716,6 +752,13 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             };
             const int trow = ew * 32 + (int)lane;            // row of this thread inside the tile
             const bool row_ok = trow < bm;
+#if defined(FTGEMM_EXP_NO_PASS2)
+            // timing experiment: no TMEM reads / stores after the verification
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) arrive_leader(&tm_empty[acc]);
+            if (true) continue;
+#endif
             if constexpr (FT && !kTF32) {
                 // leftover 4 columns (tile cols 0..3 for odd tiles, BND-4..BND-1 for even ones)
                 const int lo = par ? 0 : Cfg::BND - 4;
@@ -738,7 +781,9 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         uint2 pk;
                         pk.x = (uint32_t)f32_to_bf16_rn(o4[0]) | ((uint32_t)f32_to_bf16_rn(o4[1]) << 16);
                         pk.y = (uint32_t)f32_to_bf16_rn(o4[2]) | ((uint32_t)f32_to_bf16_rn(o4[3]) << 16);
+#if !defined(FTGEMM_EXP_NO_STORE)
                         *reinterpret_cast<uint2*>(Cp) = pk;
+#endif
                     } else {
 #pragma unroll
                         for (int i = 0; i < 4; ++i) if (lo + i < bn) Cp[i] = f32_to_bf16_rn(o4[i]);
@@ -842,7 +887,9 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
+#if !defined(FTGEMM_EXP_NO_STORE)
                     tma_store_2d(cmap, sbuf, gcol, grow);
+#endif
                     bulk_commit();
                 }
             }

@@ -1,0 +1,8 @@
+#!/bin/bash
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+for rep in 1 2; do
+python tools/one_probe.py bf16 8192 8192 8192 2 ft
+python tools/one_probe.py bf16 8192 8192 8192 0 off
+python tools/one_probe.py tf32 8192 8192 8192 2 ft
+python tools/one_probe.py tf32 8192 8192 8192 0 off
+done
