@@ -171,6 +171,25 @@ int make_map(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t 
     return FTGEMM_OK;
 }
 
+// 3-D view of a row-major [rows][cols] operand as (128-byte column slice,
+// row, column block): one box covers nblk consecutive column blocks of bk rows,
+// landing as nblk stacked [bk][128 B] SWIZZLE_128B atoms -- the smem layout of
+// the N-major B tile (cols must be a multiple of the slice width)
+int make_map_3d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t slice, uint64_t rows,
+                uint64_t nblocks, uint64_t row_bytes, uint32_t box_rows, uint32_t box_blocks, CUtensorMapSwizzle sw) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return fail(FTGEMM_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+    const uint64_t elt = (dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) ? 2 : 4;
+    cuuint64_t dims[3] = {slice, rows, nblocks};
+    cuuint64_t strides[2] = {row_bytes, slice * elt};
+    cuuint32_t box[3] = {(cuuint32_t)slice, box_rows, box_blocks};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(m, dt, 3, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(FTGEMM_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled (3-D) failed (%d)", (int)r);
+    return FTGEMM_OK;
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 int check_dims(int dtype, int64_t M, int64_t N, int64_t K) {
@@ -349,6 +368,12 @@ static int run_impl(int dtype, int64_t M, int64_t N, int64_t K, float alpha, con
 #else
         if ((e = make_map(&mA, dt, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * elt, (uint32_t)p.bk, (uint32_t)bmd))) return e;
 #endif
+        // B (N-major, 128-byte column slices): one 3-D request per stage when the
+        // column count is a whole number of slices (B^r always is), else one
+        // 2-D box per slice
+        const CUtensorMapSwizzle bsw = tf32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
+        const uint32_t nbox_cta = (uint32_t)(p.bn / boxn / p.cta_group);
+        bool b3d = !(getenv("FTGEMM_B3D") && atoi(getenv("FTGEMM_B3D")) == 0);
 #if defined(FTGEMM_EXP_B_DIRECT)
         if (false) {
 #else
@@ -356,11 +381,16 @@ static int run_impl(int dtype, int64_t M, int64_t N, int64_t K, float alpha, con
 #endif
             // the encoded operand B^r (N-major, kp rows of tiles_n * bn) from the encode workspace
             const uint64_t ldt = (uint64_t)g.tiles_n * p.bn;
-            if ((e = make_map(&mB, dt, enc + L.bt, ldt, (uint64_t)g.kp, ldt * elt, boxn, (uint32_t)p.bk,
-                              tf32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B))) return e;
+            if (b3d) e = make_map_3d(&mB, dt, enc + L.bt, boxn, (uint64_t)g.kp, ldt / boxn, ldt * elt, (uint32_t)p.bk,
+                                     nbox_cta, bsw);
+            else e = make_map(&mB, dt, enc + L.bt, ldt, (uint64_t)g.kp, ldt * elt, boxn, (uint32_t)p.bk, bsw);
+            if (e) return e;
         } else {
-            if ((e = make_map(&mB, dt, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb * elt, boxn, (uint32_t)p.bk,
-                              tf32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B))) return e;
+            b3d = b3d && (N % boxn) == 0;
+            if (b3d) e = make_map_3d(&mB, dt, B, boxn, (uint64_t)K, (uint64_t)N / boxn, (uint64_t)ldb * elt,
+                                     (uint32_t)p.bk, nbox_cta, bsw);
+            else e = make_map(&mB, dt, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb * elt, boxn, (uint32_t)p.bk, bsw);
+            if (e) return e;
         }
         // C: 128-byte rows of output per thread, 32-row boxes (29 rows for the
         // last epilogue warp of a 125-row check tile)
@@ -378,6 +408,7 @@ static int run_impl(int dtype, int64_t M, int64_t N, int64_t K, float alpha, con
         a.ft_level = ft_level; a.alpha = alpha; a.beta = beta; a.C = C; a.ldc = ldc;
         a.ks_kb = ks > 0 ? (int)std::min<int64_t>(ks / p.bk, num_kb) : 0;
         a.fuse_a = fuse_a;
+        a.b3d = b3d ? 1 : 0;
         if (ft) {
             a.Y = enc + L.y; a.kp = g.kp;
             a.rownorm = (const float*)(enc + L.rownorm); a.colnorm = (const float*)(enc + L.colnorm);

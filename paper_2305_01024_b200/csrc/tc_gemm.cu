@@ -209,6 +209,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             // barrier (the encoder warps read it); rows 125..127 are written by
             // the encoder warps instead of loaded
             const bool fa = FT && a.fuse_a;
+            const bool b3d = a.b3d != 0;                 // B tile in one 3-D TMA request
 #if defined(FTGEMM_EXP_A128)
             // timing experiment: FT kernel fed like FT off (one 128-row A box, no split rows)
             const uint32_t bytes_cta = Cfg::A_BYTES + Cfg::B_BYTES;
@@ -236,18 +237,26 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #if !defined(FTGEMM_EXP_A128)
                         if (FT && !fa) tma_load_2d(sa + Cfg::BMD * 128, &tmY, &full[s], 0, ti * a.num_kb + kb);
 #endif
+                        if (b3d) {
+                            tma_load_3d(sb, &tmB, &full[s], 0, kb * Cfg::BK, colb / Cfg::BOXN);
+                        } else {
 #pragma unroll
-                        for (int b = 0; b < Cfg::NBOX; ++b)
-                            tma_load_2d(sb + b * Cfg::B_BOX_BYTES, &tmB, &full[s], colb + b * Cfg::BOXN, kb * Cfg::BK);
+                            for (int b = 0; b < Cfg::NBOX; ++b)
+                                tma_load_2d(sb + b * Cfg::B_BOX_BYTES, &tmB, &full[s], colb + b * Cfg::BOXN, kb * Cfg::BK);
+                        }
                     } else {
                         const uint32_t mb = smem_u32(&full[s]) & kPeerBitMask;
                         if (!fa) tma_load_2d_pair(sa, &tmA, mb, kb * Cfg::BK, row0);
 #if !defined(FTGEMM_EXP_A128)
                         if (FT && !fa) tma_load_2d_pair(sa + Cfg::BMD * 128, &tmY, mb, 0, ti * a.num_kb + kb);
 #endif
+                        if (b3d) {
+                            tma_load_3d_pair(sb, &tmB, mb, 0, kb * Cfg::BK, colb / Cfg::BOXN);
+                        } else {
 #pragma unroll
-                        for (int b = 0; b < Cfg::NBOX / CG; ++b)
-                            tma_load_2d_pair(sb + b * Cfg::B_BOX_BYTES, &tmB, mb, colb + b * Cfg::BOXN, kb * Cfg::BK);
+                            for (int b = 0; b < Cfg::NBOX / CG; ++b)
+                                tma_load_2d_pair(sb + b * Cfg::B_BOX_BYTES, &tmB, mb, colb + b * Cfg::BOXN, kb * Cfg::BK);
+                        }
                     }
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
