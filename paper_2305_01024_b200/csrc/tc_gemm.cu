@@ -39,11 +39,10 @@ namespace ftg {
 
 // epilogue warpgroups: 2 = one warpgroup per TMEM accumulator buffer, so the
 // epilogues (verification included) of two consecutive tiles run concurrently
+// (FT on); FT off keeps one and spends the staging memory on a deeper ring
 #ifndef FTGEMM_EPI_WG
 #define FTGEMM_EPI_WG 2
 #endif
-constexpr int kEpiWG = FTGEMM_EPI_WG;
-constexpr int kThreads = 128 + 128 * kEpiWG;
 
 template <bool kTF32, int BN_, bool FT, int CG_ = 1>
 struct TcCfg {
@@ -60,8 +59,10 @@ struct TcCfg {
     static constexpr int B_BYTES = (NBOX / CG) * B_BOX_BYTES;   // this CTA's share of the B tile
     static constexpr int Y_BYTES = 384;            // 3 split rows x 128 bytes
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int EPI_WG = FT ? FTGEMM_EPI_WG : 1;
+    static constexpr int THREADS = 128 + 128 * EPI_WG;
     static constexpr int STG_BYTES = 4 * 2 * 4096;     // per epilogue warpgroup (see below)
-    static constexpr int EPI_BYTES = kEpiWG * STG_BYTES;
+    static constexpr int EPI_BYTES = EPI_WG * STG_BYTES;
     static constexpr int MISC_BYTES = 2048;            // barriers, TMEM address, in-kernel-encode norms
     static constexpr int STAGE_FIT = (227 * 1024 - 1024 - MISC_BYTES - EPI_BYTES) / (A_BYTES + B_BYTES);
     static constexpr int STAGES = STAGE_FIT < 8 ? STAGE_FIT : 8;
@@ -125,12 +126,13 @@ __device__ __forceinline__ uint32_t apply_fault(uint32_t bits, const DevInject& 
 }
 
 template <bool kTF32, int BN, bool FT, int CG>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(TcCfg<kTF32, BN, FT, CG>::THREADS, 1)
 tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC29,
                  const __grid_constant__ CUtensorMap tmY, const TcArgs a) {
     using Cfg = TcCfg<kTF32, BN, FT, CG>;
     constexpr int S = Cfg::STAGES;
+    constexpr int kEpiWG = Cfg::EPI_WG;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte aligned base (SWIZZLE_128B atoms); pointer arithmetic on the
     // __shared__ array keeps the shared address space visible to the compiler
@@ -932,7 +934,7 @@ cudaError_t launch_tc_t(const CUtensorMap& mA, const CUtensorMap& mB, const CUte
     const int clusters = a.num_units < kNumSMsB200 / CG ? a.num_units : kNumSMsB200 / CG;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(clusters * CG, 1, 1);
-    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.blockDim = dim3(Cfg::THREADS, 1, 1);
     cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
