@@ -587,6 +587,46 @@ def test_cfg3_full_size_sampled():
         assert mine == sorted((e["row"], e["col"]) for e in ref.events)
 
 
+def test_large_indexing_sampled():
+    """C with more than 2^31 elements (65539 x 32768 BF16, 4.3 GB; ragged last
+    check-tile row): 64-bit offsets in the encode, fused kernel and epilogue
+    stores.  Faults in the first, an interior and the very last tile; whole
+    tiles checked against the tile-local oracle."""
+    import torch
+    F = ftmod()
+    M, N, K = 65539, 32768, 256
+    plan = F.plan("bf16", M, N, K)
+    tm, tn = plan.check_tile_m, plan.check_tile_n
+    assert M * N > 2 ** 31
+    seedA, seedB = synth.BASE_SEED + 7, synth.BASE_SEED + 8
+    A = synth.to_torch(synth.matrix(seedA, M, K, dtype="bf16"), "bf16").cuda()
+    B = synth.to_torch(synth.matrix(seedB, K, N, dtype="bf16"), "bf16").cuda()
+    C = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    last = (plan.tiles_m - 1, plan.tiles_n - 1)
+    tiles = [(0, 0), (300, 70), last, (plan.tiles_m - 1, 0)]
+    inj = [(ti * tm + (ti * 7) % min(tm, M - ti * tm), tj * tn + 5, 200, 0, oracle.INJ_ADD, 0, 3000.0)
+           for ti, tj in tiles[:3]]
+    g = F.FTGemm("bf16", M, N, K)
+    g.encode(A, B)
+    g.run(A, B, C, injections=inj)
+    counts, events = g.report()
+    assert counts["corrected"] == 3 and counts["tiles_detected"] == 3
+    assert counts["tiles_checked"] == plan.tiles_m * plan.tiles_n
+    for (ti, tj) in tiles:
+        r0, c0 = ti * tm, tj * tn
+        r1, c1 = min(M, r0 + tm), min(N, c0 + tn)
+        Ab = synth.matrix(seedA, M, K, dtype="bf16", r0=r0, r1=r1)
+        Bb = synth.matrix(seedB, K, N, dtype="bf16", c0=c0, c1=c1)
+        loc = [(r - r0, c - c0, k, b, m, tg, ad) for (r, c, k, b, m, tg, ad) in inj if r0 <= r < r1 and c0 <= c < c1]
+        ref = oracle.ftgemm(Ab, Bb, out="bf16", tile_m=tm, tile_n=tn, bk=plan.bk, u_acc=plan.u_acc,
+                            lambda1=plan.lambda1, lambda2=plan.lambda2, injections=loc)
+        blk = C[r0:r1, c0:c1].float().cpu().numpy().astype(np.float64)
+        assert np.linalg.norm(blk - ref.C) / np.linalg.norm(ref.C) < TOL["bf16"], (ti, tj)
+        mine = sorted((e["row"] - r0, e["col"] - c0) for e in events if e["tile_m"] == ti and e["tile_n"] == tj)
+        assert mine == sorted((e["row"], e["col"]) for e in ref.events)
+    del C
+
+
 # --------------------------------------------------------------- API errors --
 
 def test_device_argument_errors():
