@@ -253,6 +253,28 @@ FTGEMM_API int ftgemm_encode(int dtype, int64_t M, int64_t N, int64_t K,
                   const void* A, int64_t lda, const void* B, int64_t ldb,
                   void* enc_ws, int which, void* stream);
 
+/* Where ftgemm_encode puts its results inside enc_ws (byte offsets from the
+ * workspace base), for inspection and tests; pure host function.  FP32 arrays:
+ *   ac      [tiles_m][kp]  Ac_i[k]  (Eq. 1), k >= K zero
+ *   br      [tiles_n][kp]  Br_j[k]  (Eq. 2)
+ *   rownorm [M] ||A[p,:]||_2,  acnorm [tiles_m] ||Ac_i||_2
+ *   colnorm [N] ||B[:,q]||_2,  brnorm [tiles_n] ||Br_j||_2
+ * and, for the tensor-core dtypes, the encoded operand B^r in the operand type:
+ *   bt      [kp][bt_ld], bt_ld = tiles_n * bn: slot j = columns j*bn .. j*bn+bn-1
+ *           holds B[k, j*check_tile_n + c] for c < check_tile_n, then the exact
+ *           three-term split hi, mid, lo of Br_j[k] (hi + mid + lo == Br_j[k]),
+ *           then zero (bt = -1 for F32_SIMT);
+ *   y       [tiles_m][kp / bk][3][128 bytes]: row r = split term r (hi, mid, lo)
+ *           of Ac_i[kb*bk .. kb*bk+bk) in the operand type, its 16-byte chunks
+ *           permuted c -> c ^ ((125 + r) & 7) (the SWIZZLE_128B order of MMA
+ *           rows 125..127; y = -1 for F32_SIMT).
+ * Errors: INVALID_VALUE (dims < 1, bad dtype, null out).                      */
+typedef struct ftgemm_enc_layout {
+    int64_t ac, br, bt, rownorm, colnorm, acnorm, brnorm;
+    int64_t kp, bt_ld, y;
+} ftgemm_enc_layout_t;
+FTGEMM_API int ftgemm_encode_layout(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_enc_layout_t* out);
+
 /* ---- run --------------------------------------------------------------------
  * C = alpha A B + beta C with online ABFT at ft_level.  A, B, C are device
  * row-major matrices of the dtype's operand type (float for F32_SIMT/TF32,

@@ -23,7 +23,7 @@
 namespace ftg {
 cudaError_t launch_encode(const Geometry& g, const EncLayout& L, int64_t M, int64_t N, int64_t K,
                           const void* A, int64_t lda, const void* B, int64_t ldb, void* enc, int which,
-                          const CUtensorMap* mapA, int nkc_tma, cudaStream_t st);
+                          cudaStream_t st);
 }  // namespace ftg
 
 namespace ftg {
@@ -123,7 +123,16 @@ Geometry geometry(const ftgemm_plan_t& p, int64_t K) {
     g.elt = p.dtype == FTGEMM_BF16 ? 2 : 4;
     g.tc = p.dtype != FTGEMM_F32_SIMT;
     g.nkc_a = (g.kp + 512 / g.elt - 1) / (512 / g.elt);   // encode-A k chunks (512-byte rows)
-    g.nkc_b = (g.kp + kEncBRows - 1) / kEncBRows;
+    // encode B: 256 k-rows per block (measured best or equal against 64 / 128
+    // for every profiled shape, profiles/r1_encode.md)
+    g.enc_b_rows = kEncBRows;
+    {
+        if (const char* e = getenv("FTGEMM_ENC_B_ROWS")) {       // tuning override (32 .. 256)
+            const int r = atoi(e);
+            if (r >= 32 && r <= 256 && r % 32 == 0) g.enc_b_rows = r;
+        }
+    }
+    g.nkc_b = (g.kp + g.enc_b_rows - 1) / g.enc_b_rows;
     return g;
 }
 
@@ -236,6 +245,23 @@ int ftgemm_plan(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* out) 
     return FTGEMM_OK;
 }
 
+int ftgemm_encode_layout(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_enc_layout_t* out) {
+    if (!out) return fail(FTGEMM_ERR_INVALID_VALUE, "null layout pointer");
+    int e = check_dims(dtype, M, N, K);
+    if (e) return e;
+    ftgemm_plan_t p;
+    fill_plan(dtype, M, N, K, &p);
+    const Geometry g = geometry(p, K);
+    const EncLayout L = enc_layout(g, M, N);
+    out->ac = (int64_t)L.ac; out->br = (int64_t)L.br; out->bt = g.tc ? (int64_t)L.bt : -1;
+    out->rownorm = (int64_t)L.rownorm; out->colnorm = (int64_t)L.colnorm;
+    out->acnorm = (int64_t)L.acnorm; out->brnorm = (int64_t)L.brnorm;
+    out->kp = g.kp; out->bt_ld = (int64_t)g.tiles_n * g.bn;
+    out->y = g.tc ? (int64_t)L.y : -1;
+    g_err.clear();
+    return FTGEMM_OK;
+}
+
 int ftgemm_encode(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B,
                   int64_t ldb, void* enc_ws, int which, void* stream) {
     int e = check_dims(dtype, M, N, K);
@@ -253,15 +279,7 @@ int ftgemm_encode(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int
     fill_plan(dtype, M, N, K, &p);
     const Geometry g = geometry(p, K);
     const EncLayout L = enc_layout(g, M, N);
-    // encode A streams the operand through TMA: one (check-tile rows x 512 bytes) box per block
-    CUtensorMap mA{};
-    if (which & 1) {
-        const CUtensorMapDataType dt = dtype == FTGEMM_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-        if ((e = make_map(&mA, dt, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * elt, (uint32_t)(512 / elt),
-                          (uint32_t)g.bmd, CU_TENSOR_MAP_SWIZZLE_NONE))) return e;
-    }
-    cudaError_t ce = launch_encode(g, L, M, N, K, A, lda, B, ldb, enc_ws, which, (which & 1) ? &mA : nullptr,
-                                   g.nkc_a, (cudaStream_t)stream);
+    cudaError_t ce = launch_encode(g, L, M, N, K, A, lda, B, ldb, enc_ws, which, (cudaStream_t)stream);
     if (ce != cudaSuccess) return fail_cuda(ce, "encode launch");
     g_err.clear();
     return FTGEMM_OK;

@@ -86,6 +86,7 @@ struct Geometry {
     int nkb;              // kp / bk (MMA k-blocks)
     int nkc_a;            // K chunks of the A-encode partial row norms (256 wide)
     int nkc_b;            // K chunks of the B-encode partial column norms
+    int enc_b_rows;       // k-rows per encode-B block (nkc_b = ceil(kp / enc_b_rows))
     int elt;              // operand element bytes
     int tc;               // 1 for the tensor-core paths (split operands, B^r)
 };
@@ -158,6 +159,11 @@ __device__ __forceinline__ void split3(float s, float& hi, float& mid, float& lo
         mid = tf32_trunc(r1);
         lo = r1 - mid;
     }
+}
+
+// packed bf16x2 word -> (low, high) as FP32 (exact)
+__device__ __forceinline__ float2 bf16x2_to_f2(uint32_t w) {
+    return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
 }
 
 // two floats -> packed bf16x2 (RNE), low half = a (one cvt.rn.bf16x2.f32)

@@ -11,16 +11,23 @@
 //       Bt_j    = B^r_j = [B_j, split(B_j e), 0], K-major (tensor-core paths)
 //       ||B[:,q]||_2 per column, ||Br_j||_2 per tile.
 //
-// Single streaming passes over each operand (HBM bound).  Encode A is fed by
-// one TMA box per block (check-tile rows x 512 bytes); encode B streams 8- or
-// 16-byte vectors in unrolled batches; reductions go through warp shuffles
-// and shared memory; with both operands, encode B runs on a side stream
-// beside encode A (launch_encode).  The
+// Single streaming passes over each operand (HBM bound), every global access a
+// 16-byte (A; TF32 / FP32 B) or 8-byte (BF16 B: 252-column tiles start on
+// 8-byte boundaries) vector with several rows in flight per lane; reductions go
+// through registers, warp shuffles and shared memory; with both operands,
+// encode B runs on a side stream beside encode A (launch_encode).  The
 // per-row / per-column norms are reduced across K-chunk blocks by the LAST
 // block of each tile (atomic ticket, self-resetting), so no extra launch is
 // needed.  TF32 mode sums the values exactly as the tensor core will see them
 // (low 13 mantissa bits dropped), so the carried references and the main
 // product are built from the same operands.
+//
+// Measured alternatives (profiles/r1_encode.md): a TMA-fed encode A (one
+// 64 KB box per block, column sums from shared memory) ran at 3.2 TB/s against
+// 4.0 TB/s for the register-streaming kernel below; for BF16 encode B, a
+// shared-memory-staged tile-pair kernel (16-byte cp.async or per-row bulk TMA
+// copies, shifted re-reads for the 4-column slot offset) and a shuffle-based
+// tile-pair kernel were 2-40 % slower than the 8-byte register kernel.
 #include <cstdint>
 #include <mutex>
 #include <type_traits>
@@ -67,72 +74,131 @@ __device__ __forceinline__ bool last_block(int* ticket, int idx, int nblocks, in
     return last;
 }
 
-// ------------------------------------------------ encode A (TMA-fed) -------
-// grid (nkc = ceil(kp/KC), tiles_m); block 256.  One TMA load brings the tile's
-// bmd rows x KC k (512-byte rows, 64 KB) into shared memory -- a single bulk
-// request per block, so every SM keeps ~3 x 64 KB in flight with no registers
-// tied up -- then (a) thread pairs sum columns over the rows, (b) warps reduce
-// the row sums of squares.  KC = 256 (BF16) / 128 (FP32 storage).
+// ------------------------------------------ encode A (register streaming) --
+// grid (nkc = ceil(kp/KC), tiles_m); block 256.  Same outputs as the TMA-fed
+// kernel above, without the shared-memory round trip: warp w streams rows
+// w, w+8, ... of check tile ti, every lane one 16-byte vector of the row's
+// 512-byte k-chunk (a warp reads one full row per instruction, coalesced), ENC_U
+// rows in flight per lane.  Column sums stay in registers (8 BF16 / 4 FP32
+// columns per lane) and are reduced across the 8 warps once per block; row sums
+// of squares are warp-shuffle reductions.
+constexpr int ENC_U = 8;
 template <int MODE>
-__global__ void __launch_bounds__(256) encode_a_tma_kernel(const __grid_constant__ CUtensorMap tmA, int M, int K,
-                                                           int bmd, int kp, int bk, int nkc, float* __restrict__ Ac,
-                                                           uint8_t* __restrict__ Y, float* rn2, float* acn2, int* ticket,
-                                                           float* __restrict__ rownorm, float* __restrict__ acnorm) {
+__global__ void __launch_bounds__(256) encode_a_kernel(const void* __restrict__ A_, int64_t lda, int M, int K, int bmd,
+                                                       int kp, int bk, int nkc, float* __restrict__ Ac,
+                                                       uint8_t* __restrict__ Y, float* rn2, float* acn2, int* ticket,
+                                                       float* __restrict__ rownorm, float* __restrict__ acnorm) {
     constexpr int ELT = MODE == 0 ? 2 : 4;
     constexpr int KC = 512 / ELT;                       // k per block (512-byte rows)
-    extern __shared__ __align__(128) uint8_t enc_smem[];
-    uint8_t* tile = enc_smem;                           // [bmd][512 B]
-    float* colp = reinterpret_cast<float*>(enc_smem + 128 * 512);   // [2][KC] half-tile column sums
-    __shared__ __align__(8) uint64_t bar;
+    constexpr int VPL = 16 / ELT;                       // values per lane
+    __shared__ __align__(16) float colp[8][KC];
     __shared__ float red8[8];
     __shared__ int s_flag;
     const int kc = blockIdx.x, ti = blockIdx.y;
     const int t = threadIdx.x, w = t >> 5, lane = t & 31;
     const int rbeg = ti * bmd, rows = min(bmd, M - rbeg);
-    if (t == 0) {
-        mbar_init(&bar, 1);
-        fence_barrier_init();
-        mbar_arrive_expect_tx(&bar, (uint32_t)(bmd * 512));
-        tma_load_2d(tile, &tmA, &bar, kc * KC, rbeg);
-    }
-    __syncthreads();
-    mbar_wait(&bar, 0);
-    auto val = [&](int r, int c) -> float {             // element (row r, k-col c) as the MMA sees it
-        if constexpr (MODE == 0) return bf16_to_f32(reinterpret_cast<const uint16_t*>(tile + r * 512)[c]);
-        else if constexpr (MODE == 1) return tf32_trunc(reinterpret_cast<const float*>(tile + r * 512)[c]);
-        else return reinterpret_cast<const float*>(tile + r * 512)[c];
-    };
-    // (a) column sums: thread t: column c = t % KC over one half of the rows (BF16:
-    // 256 columns x 1 half; FP32: 128 columns x 2 halves)
-    {
-        constexpr int HALVES = 256 / KC;
-        const int c = t % KC, h = t / KC;
-        const int r_lo = h * ((rows + HALVES - 1) / HALVES), r_hi = min(rows, r_lo + (rows + HALVES - 1) / HALVES);
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-        int r = r_lo;
-        for (; r + 4 <= r_hi; r += 4) { s0 += val(r, c); s1 += val(r + 1, c); s2 += val(r + 2, c); s3 += val(r + 3, c); }
-        for (; r < r_hi; ++r) s0 += val(r, c);
-        colp[h * KC + c] = (s0 + s1) + (s2 + s3);
-    }
-    // (b) row sums of squares: warp w, rows w, w + 8, ...; lane reads 16 bytes
-    for (int r = w; r < rows; r += 8) {
-        const uint4 u = *reinterpret_cast<const uint4*>(tile + r * 512 + lane * 16);
-        const uint32_t wd[4] = {u.x, u.y, u.z, u.w};
-        float q = 0.0f;
+    const int k0 = kc * KC + lane * VPL;
+    const bool full = k0 + VPL <= K;
+    const bool blk_full = (kc + 1) * KC <= K;
+    const int64_t ldb_ = lda * ELT;                     // row pitch (bytes)
+    const uint8_t* base = reinterpret_cast<const uint8_t*>(A_) + (int64_t)rbeg * ldb_ + (int64_t)k0 * ELT;
+    // ragged K: the lane's elements below K, zeros above (no local arrays)
+    auto load_partial = [&](const uint8_t* p) -> uint4 {
+        uint32_t wd[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            if constexpr (MODE == 0) {
-                const float lo = __uint_as_float(wd[i] << 16), hi = __uint_as_float(wd[i] & 0xFFFF0000u);
-                q = fmaf(lo, lo, q); q = fmaf(hi, hi, q);
-            } else {
-                const float x = MODE == 1 ? tf32_trunc(__uint_as_float(wd[i])) : __uint_as_float(wd[i]);
-                q = fmaf(x, x, q);
+        for (int i = 0; i < VPL; ++i) {
+            if (k0 + i < K) {
+                if constexpr (ELT == 2) wd[i >> 1] |= (uint32_t)reinterpret_cast<const uint16_t*>(p)[i] << (16 * (i & 1));
+                else wd[i] = reinterpret_cast<const uint32_t*>(p)[i];
             }
         }
+        return make_uint4(wd[0], wd[1], wd[2], wd[3]);
+    };
+    // value pair j of a 16-byte vector as the MMA sees it
+    auto pair = [](const uint4& u, int j) -> float2 {
+        const uint32_t wd[4] = {u.x, u.y, u.z, u.w};
+        if constexpr (MODE == 0) return make_float2(__uint_as_float(wd[j] << 16), __uint_as_float(wd[j] & 0xFFFF0000u));
+        else if constexpr (MODE == 1)
+            return make_float2(tf32_trunc(__uint_as_float(wd[2 * j])), tf32_trunc(__uint_as_float(wd[2 * j + 1])));
+        else return make_float2(__uint_as_float(wd[2 * j]), __uint_as_float(wd[2 * j + 1]));
+    };
+    float2 col2[VPL / 2];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-        if (lane == 0) rn2[(int64_t)kc * M + rbeg + r] = q;
+    for (int j = 0; j < VPL / 2; ++j) col2[j] = make_float2(0.0f, 0.0f);
+    // the lane that ends up holding row u's sum of squares after the transposed
+    // reduction below: bits 4, 3, 2 of the lane index encode u
+    const int my_u = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+    for (int r0 = w; r0 < rows; r0 += 8 * ENC_U) {
+        uint4 raw[ENC_U];
+        if (blk_full) {                                 // block-uniform: the common case, 8 plain loads
+#pragma unroll
+            for (int u = 0; u < ENC_U; ++u) {
+                const int r = r0 + 8 * u;
+                raw[u] = r < rows ? ldg_stream_v4(base + (int64_t)r * ldb_) : make_uint4(0u, 0u, 0u, 0u);
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < ENC_U; ++u) {
+                const int r = r0 + 8 * u;
+                const uint8_t* p = base + (int64_t)r * ldb_;
+                raw[u] = make_uint4(0u, 0u, 0u, 0u);
+                if (r < rows) {
+                    if (full) raw[u] = ldg_stream_v4(p);
+                    else if (k0 < K) raw[u] = load_partial(p);
+                }
+            }
+        }
+        float q[ENC_U];
+#pragma unroll
+        for (int u = 0; u < ENC_U; ++u) {
+            float2 q2 = make_float2(0.0f, 0.0f);
+#pragma unroll
+            for (int j = 0; j < VPL / 2; ++j) {
+                const float2 x = pair(raw[u], j);
+                col2[j] = __fadd2_rn(col2[j], x);
+                q2 = __ffma2_rn(x, x, q2);
+            }
+            q[u] = q2.x + q2.y;
+        }
+        // transposed reduction of the 8 rows' squares: 4 + 2 + 1 exchanges halve
+        // the set each lane carries, then two plain butterfly steps (9 shuffles
+        // for 8 rows instead of 40)
+        static_assert(ENC_U == 8, "transposed reduction assumes 8 rows per batch");
+        float h4[4], h2[2], h1;
+        {
+            const bool up = lane & 16;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float send = up ? q[i] : q[i + 4];
+                const float keep = up ? q[i + 4] : q[i];
+                h4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+            }
+        }
+        {
+            const bool up = lane & 8;
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const float send = up ? h4[i] : h4[i + 2];
+                const float keep = up ? h4[i + 2] : h4[i];
+                h2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+            }
+        }
+        {
+            const bool up = lane & 4;
+            const float send = up ? h2[0] : h2[1];
+            const float keep = up ? h2[1] : h2[0];
+            h1 = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
+        h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+        if ((lane & 3) == 0 && r0 + 8 * my_u < rows) rn2[(int64_t)kc * M + rbeg + r0 + 8 * my_u] = h1;
     }
+    float col[VPL];
+#pragma unroll
+    for (int j = 0; j < VPL / 2; ++j) { col[2 * j] = col2[j].x; col[2 * j + 1] = col2[j].y; }
+#pragma unroll
+    for (int i = 0; i < VPL; i += 4)
+        *reinterpret_cast<float4*>(&colp[w][lane * VPL + i]) = make_float4(col[i], col[i + 1], col[i + 2], col[i + 3]);
     __syncthreads();
     // Ac, its split rows (pre-swizzled Ypack) and the partial ||Ac||^2
     float s2 = 0.0f;
@@ -140,7 +206,8 @@ __global__ void __launch_bounds__(256) encode_a_tma_kernel(const __grid_constant
         const int k = kc * KC + c;
         if (k >= kp) break;
         float s = 0.0f;
-        for (int h = 0; h < 256 / KC; ++h) s += colp[h * KC + c];
+#pragma unroll
+        for (int ww = 0; ww < 8; ++ww) s += colp[ww][c];
         if (k >= K) s = 0.0f;
         Ac[(int64_t)ti * kp + k] = s;
         s2 = fmaf(s, s, s2);
@@ -175,12 +242,10 @@ __global__ void __launch_bounds__(256) encode_a_tma_kernel(const __grid_constant
     }
 }
 
-size_t encode_a_tma_smem() { return 128 * 512 + 2 * 256 * sizeof(float); }
-
 // ----------------------------------------------------- encode B (FP32 SIMT) --
-// grid (nkc = ceil(kp/kEncBRows), tiles_n): Br_j (warp per k-row) and column squares.
+// grid (nkc = ceil(kp/rpb), tiles_n): Br_j (warp per k-row) and column squares.
 __global__ void __launch_bounds__(256) encode_b_simt_kernel(const float* __restrict__ B, int64_t ldb, int N, int K,
-                                                            int bnd, int kp, int nkc, float* __restrict__ Br,
+                                                            int bnd, int kp, int nkc, int rpb, float* __restrict__ Br,
                                                             float* cn2, float* brn2, int* ticket,
                                                             float* __restrict__ colnorm, float* __restrict__ brnorm) {
     __shared__ float red[8][257];
@@ -194,8 +259,8 @@ __global__ void __launch_bounds__(256) encode_b_simt_kernel(const float* __restr
 #pragma unroll
     for (int i = 0; i < 8; ++i) csq[i] = 0.0f;
     float bq = 0.0f;
-    for (int r = w; r < kEncBRows; r += 8) {
-        const int k = kc * kEncBRows + r;
+    for (int r = w; r < rpb; r += 8) {
+        const int k = kc * rpb + r;
         if (k >= kp) break;
         float s = 0.0f;
         if (k < K) {
@@ -258,7 +323,7 @@ __global__ void __launch_bounds__(256) encode_b_simt_kernel(const float* __restr
 }
 
 // -------------------------------------------- encode B (tensor-core paths) --
-// grid (nkc = ceil(kp/kEncBRows), tiles_n); warp w handles k-rows kc*kEncBRows + w + 8i.
+// grid (nkc = ceil(kp/rpb), tiles_n); warp w handles k-rows kc*rpb + w + 8i (rpb: a multiple of 32).
 // Per k-row of check tile j the warp streams the bnd data columns (4-element
 // chunks: lane l owns chunks l and l+32), reduces B_j e with warp shuffles,
 // accumulates column squares in registers, and writes the encoded operand row
@@ -267,7 +332,7 @@ __global__ void __launch_bounds__(256) encode_b_simt_kernel(const float* __restr
 // fused kernel's TMA boxes start on cache-line boundaries).
 template <int MODE>
 __global__ void __launch_bounds__(256) encode_b_tc_kernel(const void* __restrict__ B_, int64_t ldb, int N, int K,
-                                                          int bnd, int bn, int kp, int ldt, int nkc,
+                                                          int bnd, int bn, int kp, int ldt, int nkc, int rpb,
                                                           float* __restrict__ Br, uint8_t* __restrict__ Bt,
                                                           float* cn2, float* brn2, int* ticket,
                                                           float* __restrict__ colnorm, float* __restrict__ brnorm) {
@@ -290,12 +355,12 @@ __global__ void __launch_bounds__(256) encode_b_tc_kernel(const void* __restrict
         if constexpr (MODE == 0) return bf16_to_f32(x);
         else return tf32_trunc(x);
     };
-    for (int r = w; r < kEncBRows; r += 8 * RB) {
+    for (int r = w; r < rpb; r += 8 * RB) {
         V raw[RB][2];
         float s[RB];
 #pragma unroll
         for (int u = 0; u < RB; ++u) {
-            const int k = kc * kEncBRows + r + 8 * u;
+            const int k = kc * rpb + r + 8 * u;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int ch = lane + 32 * h;
@@ -337,7 +402,7 @@ __global__ void __launch_bounds__(256) encode_b_tc_kernel(const void* __restrict
             for (int u = 0; u < RB; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
 #pragma unroll
         for (int u = 0; u < RB; ++u) {
-            const int k = kc * kEncBRows + r + 8 * u;
+            const int k = kc * rpb + r + 8 * u;
             if (k >= kp) continue;
             uint8_t* row = Bt + ((int64_t)k * ldt + (int64_t)tj * bn) * ELT;
 #pragma unroll
@@ -407,7 +472,7 @@ EncodeFork g_fork[64];
 
 cudaError_t launch_encode(const Geometry& g, const EncLayout& L, int64_t M, int64_t N, int64_t K,
                           const void* A, int64_t lda, const void* B, int64_t ldb, void* enc, int which,
-                          const CUtensorMap* mapA, int nkc_tma, cudaStream_t st) {
+                          cudaStream_t st) {
     char* base = reinterpret_cast<char*>(enc);
     const int mode = g.dtype == FTGEMM_BF16 ? 0 : (g.dtype == FTGEMM_TF32 ? 1 : 2);
     auto F = [&](size_t off) { return reinterpret_cast<float*>(base + off); };
@@ -439,35 +504,26 @@ cudaError_t launch_encode(const Geometry& g, const EncLayout& L, int64_t M, int6
         dim3 grid(g.nkc_b, g.tiles_n);
         if (mode == 2) {
             encode_b_simt_kernel<<<grid, 256, 0, sb>>>(reinterpret_cast<const float*>(B), ldb, (int)N, (int)K, g.bnd,
-                                                       g.kp, g.nkc_b, F(L.br), F(L.cn2), F(L.brn2), tk,
+                                                       g.kp, g.nkc_b, g.enc_b_rows, F(L.br), F(L.cn2), F(L.brn2), tk,
                                                        F(L.colnorm), F(L.brnorm));
         } else {
             uint8_t* Bt = (which & 4) ? nullptr : reinterpret_cast<uint8_t*>(base + L.bt);   // 4: no encoded operand
 #define ENC_B(MD) encode_b_tc_kernel<MD><<<grid, 256, 0, sb>>>(B, ldb, (int)N, (int)K, g.bnd, g.bn, g.kp, \
-            g.tiles_n * g.bn, g.nkc_b, F(L.br), Bt, F(L.cn2), F(L.brn2), tk, F(L.colnorm), F(L.brnorm))
+            g.tiles_n * g.bn, g.nkc_b, g.enc_b_rows, F(L.br), Bt, F(L.cn2), F(L.brn2), tk, F(L.colnorm), F(L.brnorm))
             if (mode == 0) ENC_B(0); else ENC_B(1);
 #undef ENC_B
         }
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (which & 1) {
-        if (!mapA) return cudaErrorInvalidValue;
         if ((e = cudaMemsetAsync(base + L.cnt_a, 0, sizeof(int) * (size_t)g.tiles_m, st)) != cudaSuccess) return e;
         uint8_t* Y = reinterpret_cast<uint8_t*>(base + L.y);
         int* tk = reinterpret_cast<int*>(base + L.cnt_a);
-        static bool attr[3] = {false, false, false};
-        const int smem = (int)encode_a_tma_smem();
-        dim3 grid(nkc_tma, g.tiles_m);
-#define ENC_AT(MD) do { \
-            if (!attr[MD]) { \
-                cudaError_t ea = cudaFuncSetAttribute(encode_a_tma_kernel<MD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
-                if (ea != cudaSuccess) return ea; \
-                attr[MD] = true; \
-            } \
-            encode_a_tma_kernel<MD><<<grid, 256, smem, st>>>(*mapA, (int)M, (int)K, g.bmd, g.kp, g.bk, nkc_tma, \
-                F(L.ac), Y, F(L.rn2), F(L.acn2), tk, F(L.rownorm), F(L.acnorm)); } while (0)
-        if (mode == 0) ENC_AT(0); else if (mode == 1) ENC_AT(1); else ENC_AT(2);
-#undef ENC_AT
+        dim3 grid(g.nkc_a, g.tiles_m);
+#define ENC_A(MD) encode_a_kernel<MD><<<grid, 256, 0, st>>>(A, lda, (int)M, (int)K, g.bmd, g.kp, g.bk, g.nkc_a, \
+            F(L.ac), Y, F(L.rn2), F(L.acn2), tk, F(L.rownorm), F(L.acnorm))
+        if (mode == 0) ENC_A(0); else if (mode == 1) ENC_A(1); else ENC_A(2);
+#undef ENC_A
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (sb != st) {

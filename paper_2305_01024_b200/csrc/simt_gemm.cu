@@ -20,6 +20,7 @@
 #include <cstdint>
 
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace ftg {
 
@@ -30,19 +31,6 @@ constexpr int SB = 128, SK = FTGEMM_SIMT_SK;       // tile, k-block (plan.bk)
 constexpr int NST = SK == 8 ? 4 : 3;                // smem pipeline stages
 constexpr int STAGE_FLOATS = SB * SK + SK * SB + 2 * SK;
 constexpr int SIMT_DSMEM = NST * STAGE_FLOATS * 4;  // dynamic smem: the stage ring
-
-// cp.async with zero fill: src_bytes < cp bytes fills the rest of dst with 0
-__device__ __forceinline__ void cp_async4(void* dst, const void* src, int src_bytes) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;"
-                 :: "r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src), "r"(src_bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
-                 :: "r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src), "r"(src_bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
 
 __device__ __forceinline__ int simt_inj_lower(const DevInject* inj, int n, int t) {
     int lo = 0, hi = n;

@@ -54,12 +54,16 @@ class PlanStruct(C.Structure):
                 ("u_acc", C.c_float), ("lambda1", C.c_float), ("lambda2", C.c_float), ("pad1", C.c_int32)]
 
 
+class EncLayoutStruct(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("ac", "br", "bt", "rownorm", "colnorm", "acnorm", "brnorm", "kp", "bt_ld", "y")]
+
+
 class Cost(C.Structure):
     _fields_ = [("gamma0", C.c_double), ("tiles", C.c_int64), ("gamma", C.c_double),
                 ("online_expected_runs", C.c_double), ("offline_expected_runs", C.c_double)]
 
 
-SYMBOLS = ("ftgemm_plan", "ftgemm_encode", "ftgemm_run", "ftgemm_run_fused", "ftgemm_run_online", "ftgemm_run_offline", "ftgemm_cost_model",
+SYMBOLS = ("ftgemm_plan", "ftgemm_encode", "ftgemm_encode_layout", "ftgemm_run", "ftgemm_run_fused", "ftgemm_run_online", "ftgemm_run_offline", "ftgemm_cost_model",
            "ftgemm_nonfused_workspace", "ftgemm_run_nonfused",
            "ftgemm_report", "ftgemm_report_reset", "ftgemm_last_error", "ftgemm_version", "ftgemm_device_arch")
 
@@ -77,6 +81,7 @@ def lib():
         i64, i32, vp = C.c_int64, C.c_int32, C.c_void_p
         L.ftgemm_plan.argtypes = [C.c_int, i64, i64, i64, C.POINTER(PlanStruct)]
         L.ftgemm_encode.argtypes = [C.c_int, i64, i64, i64, vp, i64, vp, i64, vp, C.c_int, vp]
+        L.ftgemm_encode_layout.argtypes = [C.c_int, i64, i64, i64, C.POINTER(EncLayoutStruct)]
         L.ftgemm_run.argtypes = [C.c_int, i64, i64, i64, C.c_float, vp, i64, vp, i64, C.c_float, vp, i64,
                                  vp, C.c_int, vp, i32, vp, vp]
         L.ftgemm_run_fused.argtypes = L.ftgemm_run.argtypes
@@ -150,6 +155,13 @@ def plan(dtype, M: int, N: int, K: int) -> Plan:
     p = PlanStruct()
     _check(lib().ftgemm_plan(_dt(dtype), M, N, K, C.byref(p)), "ftgemm_plan")
     return Plan(**{f: getattr(p, f) for f in Plan.__dataclass_fields__})
+
+
+def encode_layout(dtype, M: int, N: int, K: int) -> dict:
+    """Byte offsets of the encode results inside enc_ws (ftgemm_encode_layout)."""
+    e = EncLayoutStruct()
+    _check(lib().ftgemm_encode_layout(_dt(dtype), M, N, K, C.byref(e)), "ftgemm_encode_layout")
+    return {f: getattr(e, f) for f, _ in EncLayoutStruct._fields_}
 
 
 def alloc_workspaces(pl: Plan, device="cuda"):
