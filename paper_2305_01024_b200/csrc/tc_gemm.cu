@@ -526,8 +526,10 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 float* tbuf = reinterpret_cast<float*>(stg + 12288) + ew * (32 * 36);   // 32 x 36 transpose buffer
                 float srow = 0.0f, rref = 0.0f;
                 {
-                    // 64 columns per TMEM load; row sums in 4 independent chains
-                    float rs[4] = {0.f, 0.f, 0.f, 0.f};
+                    // 64 columns per TMEM load; row sums in 2 independent chains of
+                    // paired FP32 adds (FADD2; BND is even, so no pair straddles the
+                    // data / reference boundary)
+                    float2 rs2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
                     const bool w3 = ew == 3;
                     const bool rows_only = a.ft_level == FTGEMM_FT_DETECT_ROWS;   // offline ABFT: no column sums
 #pragma unroll
@@ -535,8 +537,9 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         float v[64];
                         tmem_ld64(tb + lane_off + c2 * 32, v);
 #pragma unroll
-                        for (int i = 0; i < 64; ++i)
-                            if (c2 * 32 + i < Cfg::BND) rs[i & 3] += v[i];
+                        for (int i = 0; i < 32; ++i)
+                            if (c2 * 32 + 2 * i < Cfg::BND)
+                                rs2[i & 1] = __fadd2_rn(rs2[i & 1], make_float2(v[2 * i], v[2 * i + 1]));
                         if (c2 + 2 == Cfg::NCHUNK) rref = (v[60] + v[61]) + v[62];
 #pragma unroll
                         for (int h = 0; h < 2 && !rows_only; ++h) {
@@ -554,26 +557,28 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                                 for (int i = 0; i < 32; ++i) tbuf[i * 36 + lane] = (rvalid || isref) ? v[32 * h + i] : 0.0f;
                             }
                             __syncwarp();
-                            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+                            float2 s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
 #pragma unroll
                             for (int r4 = 0; r4 < 7; ++r4) {
                                 const float4 x = *reinterpret_cast<const float4*>(tbuf + lane * 36 + 4 * r4);
-                                s0 += x.x; s1 += x.y; s2 += x.z; s3 += x.w;
+                                s01 = __fadd2_rn(s01, make_float2(x.x, x.y));
+                                s23 = __fadd2_rn(s23, make_float2(x.z, x.w));
                             }
                             const float4 x = *reinterpret_cast<const float4*>(tbuf + lane * 36 + 28);
-                            s0 += x.x;
                             if (w3) {
+                                s01.x += x.x;
                                 refrow[0 * BN + c * 32 + lane] = x.y;
                                 refrow[1 * BN + c * 32 + lane] = x.z;
                                 refrow[2 * BN + c * 32 + lane] = x.w;
                             } else {
-                                s1 += x.y; s2 += x.z; s3 += x.w;
+                                s01 = __fadd2_rn(s01, make_float2(x.x, x.y));
+                                s23 = __fadd2_rn(s23, make_float2(x.z, x.w));
                             }
-                            colsum[ew * BN + c * 32 + lane] = (s0 + s1) + (s2 + s3);
+                            colsum[ew * BN + c * 32 + lane] = (s01.x + s01.y) + (s23.x + s23.y);
                             __syncwarp();
                         }
                     }
-                    srow = (rs[0] + rs[1]) + (rs[2] + rs[3]);
+                    srow = (rs2[0].x + rs2[0].y) + (rs2[1].x + rs2[1].y);
                 }
                 named_bar_sync(ebar, 128);
                 // ---- row residuals ----
