@@ -127,9 +127,9 @@ Geometry geometry(const ftgemm_plan_t& p, int64_t K) {
     // for every profiled shape, profiles/r1_encode.md)
     g.enc_b_rows = kEncBRows;
     {
-        if (const char* e = getenv("FTGEMM_ENC_B_ROWS")) {       // tuning override (32 .. 256)
+        if (const char* e = getenv("FTGEMM_ENC_B_ROWS")) {       // tuning override (32 .. 1024)
             const int r = atoi(e);
-            if (r >= 32 && r <= 256 && r % 32 == 0) g.enc_b_rows = r;
+            if (r >= 32 && r <= 1024 && r % 32 == 0) g.enc_b_rows = r;
         }
     }
     g.nkc_b = (g.kp + g.enc_b_rows - 1) / g.enc_b_rows;

@@ -16,7 +16,7 @@ A = (torch.rand(M, K, device="cuda") * 2 - 1).to(tdt)
 B = (torch.rand(K, N, device="cuda") * 2 - 1).to(tdt)
 s = torch.cuda.current_stream()
 elt = A.element_size()
-VARIANTS = {"default": {}, "b_rows64": {"FTGEMM_ENC_B_ROWS": "64"}, "b_rows128": {"FTGEMM_ENC_B_ROWS": "128"}}
+VARIANTS = {"default": {}, "b_rows128": {"FTGEMM_ENC_B_ROWS": "128"}, "b_rows512": {"FTGEMM_ENC_B_ROWS": "512"}, "b_rows1024": {"FTGEMM_ENC_B_ROWS": "1024"}}
 for vname, env in VARIANTS.items():
     for k in ("FTGEMM_ENC_B_ROWS",):
         os.environ.pop(k, None)
@@ -43,3 +43,26 @@ for vname, env in VARIANTS.items():
     out["ab_gbs"] = (M * K * elt + K * N * elt + K * pl.tiles_n * pl.bn * elt * (dt != "f32_simt")) / out["ab"] / 1e3
     print(json.dumps({"variant": vname, "dtype": dt, "M": M, "N": N, "K": K,
                       **{k: round(v, 1) for k, v in out.items()}}), flush=True)
+
+# reference points: torch's own streaming kernels on the same bytes
+def _best(fn):
+    for _ in range(3):
+        fn()
+    best = 1e9
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(20):
+            fn()
+        e1.record(s)
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1) * 1e3 / 20)
+    return best
+
+
+Bc = torch.empty_like(B)
+t_sum = _best(lambda: A.sum(dim=0))
+t_cp = _best(lambda: Bc.copy_(B))
+print(json.dumps({"ref": "torch", "dtype": dt, "colsum_A_us": round(t_sum, 1),
+                  "colsum_A_gbs": round(M * K * elt / t_sum / 1e3, 1), "copy_B_us": round(t_cp, 1),
+                  "copy_B_gbs": round(2 * K * N * elt / t_cp / 1e3, 1)}), flush=True)
