@@ -15,7 +15,7 @@
 // 16-byte (A; TF32 / FP32 B) or 8-byte (BF16 B: 252-column tiles start on
 // 8-byte boundaries) vector with several rows in flight per lane; reductions go
 // through registers, warp shuffles and shared memory; with both operands,
-// encode B runs on a side stream beside encode A (launch_encode).  The
+// one launch (encode_ab_kernel) runs the blocks of both passes.  The
 // per-row / per-column norms are reduced across K-chunk blocks by the LAST
 // block of each tile (atomic ticket, self-resetting), so no extra launch is
 // needed.  TF32 mode sums the values exactly as the tensor core will see them
@@ -29,7 +29,6 @@
 // copies, shifted re-reads for the 4-column slot offset) and a shuffle-based
 // tile-pair kernel were 2-40 % slower than the 8-byte register kernel.
 #include <cstdint>
-#include <mutex>
 #include <type_traits>
 
 #include "common.cuh"
@@ -74,6 +73,17 @@ __device__ __forceinline__ bool last_block(int* ticket, int idx, int nblocks, in
     return last;
 }
 
+// parameters of the encode passes (one struct per operand, so that one launch
+// can carry both: encode_ab_kernel)
+struct EncAP {
+    const void* A; int64_t lda; int M, K, bmd, kp, bk, nkc;
+    float* Ac; uint8_t* Y; float* rn2; float* acn2; int* ticket; float* rownorm; float* acnorm;
+};
+struct EncBP {
+    const void* B; int64_t ldb; int N, K, bnd, bn, kp, ldt, nkc, rpb;
+    float* Br; uint8_t* Bt; float* cn2; float* brn2; int* ticket; float* colnorm; float* brnorm;
+};
+
 // ------------------------------------------ encode A (register streaming) --
 // grid (nkc = ceil(kp/KC), tiles_m); block 256.  Same outputs as the TMA-fed
 // kernel above, without the shared-memory round trip: warp w streams rows
@@ -93,17 +103,23 @@ constexpr int ENC_U = 8;
 #define ENC_A_MINB 4
 #endif
 template <int MODE>
-__global__ void __launch_bounds__(256, ENC_A_MINB) encode_a_kernel(const void* __restrict__ A_, int64_t lda, int M, int K, int bmd,
-                                                       int kp, int bk, int nkc, float* __restrict__ Ac,
-                                                       uint8_t* __restrict__ Y, float* rn2, float* acn2, int* ticket,
-                                                       float* __restrict__ rownorm, float* __restrict__ acnorm) {
+__device__ __forceinline__ void encode_a_body(const int kc, const int ti, const EncAP& P) {
+    const void* __restrict__ A_ = P.A;
+    const int64_t lda = P.lda;
+    const int M = P.M, K = P.K, bmd = P.bmd, kp = P.kp, bk = P.bk, nkc = P.nkc;
+    float* __restrict__ Ac = P.Ac;
+    uint8_t* __restrict__ Y = P.Y;
+    float* rn2 = P.rn2;
+    float* acn2 = P.acn2;
+    int* ticket = P.ticket;
+    float* __restrict__ rownorm = P.rownorm;
+    float* __restrict__ acnorm = P.acnorm;
     constexpr int ELT = MODE == 0 ? 2 : 4;
     constexpr int KC = 512 / ELT;                       // k per block (512-byte rows)
     constexpr int VPL = 16 / ELT;                       // values per lane
     __shared__ __align__(16) float colp[8][KC];
     __shared__ float red8[8];
     __shared__ int s_flag;
-    const int kc = blockIdx.x, ti = blockIdx.y;
     const int t = threadIdx.x, w = t >> 5, lane = t & 31;
     const int rbeg = ti * bmd, rows = min(bmd, M - rbeg);
     const int k0 = kc * KC + lane * VPL;
@@ -265,14 +281,19 @@ __global__ void __launch_bounds__(256, ENC_A_MINB) encode_a_kernel(const void* _
 
 // ----------------------------------------------------- encode B (FP32 SIMT) --
 // grid (nkc = ceil(kp/rpb), tiles_n): Br_j (warp per k-row) and column squares.
-__global__ void __launch_bounds__(256) encode_b_simt_kernel(const float* __restrict__ B, int64_t ldb, int N, int K,
-                                                            int bnd, int kp, int nkc, int rpb, float* __restrict__ Br,
-                                                            float* cn2, float* brn2, int* ticket,
-                                                            float* __restrict__ colnorm, float* __restrict__ brnorm) {
+__device__ __forceinline__ void encode_b_simt_body(const int kc, const int tj, const EncBP& P) {
+    const float* __restrict__ B = reinterpret_cast<const float*>(P.B);
+    const int64_t ldb = P.ldb;
+    const int N = P.N, K = P.K, bnd = P.bnd, kp = P.kp, nkc = P.nkc, rpb = P.rpb;
+    float* __restrict__ Br = P.Br;
+    float* cn2 = P.cn2;
+    float* brn2 = P.brn2;
+    int* ticket = P.ticket;
+    float* __restrict__ colnorm = P.colnorm;
+    float* __restrict__ brnorm = P.brnorm;
     __shared__ float red[8][257];
     __shared__ float red8[8];
     __shared__ int s_flag;
-    const int kc = blockIdx.x, tj = blockIdx.y;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nch = bnd / 4;
     const int c0 = tj * bnd;
@@ -352,11 +373,17 @@ __global__ void __launch_bounds__(256) encode_b_simt_kernel(const float* __restr
 // (B^r of Eq. (2), N-major, every tile slot 16-byte / 128-byte aligned so the
 // fused kernel's TMA boxes start on cache-line boundaries).
 template <int MODE>
-__global__ void __launch_bounds__(256) encode_b_tc_kernel(const void* __restrict__ B_, int64_t ldb, int N, int K,
-                                                          int bnd, int bn, int kp, int ldt, int nkc, int rpb,
-                                                          float* __restrict__ Br, uint8_t* __restrict__ Bt,
-                                                          float* cn2, float* brn2, int* ticket,
-                                                          float* __restrict__ colnorm, float* __restrict__ brnorm) {
+__device__ __forceinline__ void encode_b_tc_body(const int kc, const int tj, const EncBP& P) {
+    const void* __restrict__ B_ = P.B;
+    const int64_t ldb = P.ldb;
+    const int N = P.N, K = P.K, bnd = P.bnd, bn = P.bn, kp = P.kp, ldt = P.ldt, nkc = P.nkc, rpb = P.rpb;
+    float* __restrict__ Br = P.Br;
+    uint8_t* __restrict__ Bt = P.Bt;
+    float* cn2 = P.cn2;
+    float* brn2 = P.brn2;
+    int* ticket = P.ticket;
+    float* __restrict__ colnorm = P.colnorm;
+    float* __restrict__ brnorm = P.brnorm;
     constexpr int ELT = MODE == 0 ? 2 : 4;
     using T = typename std::conditional<MODE == 0, uint16_t, float>::type;
     using V = typename std::conditional<MODE == 0, uint2, uint4>::type;     // 4 elements
@@ -364,7 +391,6 @@ __global__ void __launch_bounds__(256) encode_b_tc_kernel(const void* __restrict
     __shared__ float red[8][257];
     __shared__ float red8[8];
     __shared__ int s_flag;
-    const int kc = blockIdx.x, tj = blockIdx.y;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c0 = tj * bnd;
     const int nch = bnd / 4;                  // data chunks; chunk index nch is the split slot
@@ -609,16 +635,37 @@ __global__ void __launch_bounds__(256) encode_b_tc_kernel(const void* __restrict
     }
 }
 
+// ---------------------------------------------------------------- kernels ---
+// grid (nkc, tiles) per operand; encode_ab_kernel runs both operands in one
+// 1-D launch (the B blocks first: they carry more bytes each), so a step's
+// encode is one kernel on the caller's stream -- no side stream, no fork / join
+// events -- and releases the fused GEMM (programmatic dependent launch) as soon
+// as every block has started.
+template <int MODE>
+__global__ void __launch_bounds__(256, ENC_A_MINB) encode_a_kernel(const EncAP P) {
+    encode_a_body<MODE>(blockIdx.x, blockIdx.y, P);
+}
+template <int MODE>
+__global__ void __launch_bounds__(256) encode_b_tc_kernel(const EncBP P) {
+    encode_b_tc_body<MODE>(blockIdx.x, blockIdx.y, P);
+}
+__global__ void __launch_bounds__(256) encode_b_simt_kernel(const EncBP P) {
+    encode_b_simt_body(blockIdx.x, blockIdx.y, P);
+}
+template <int MODE>
+__global__ void __launch_bounds__(256, 4) encode_ab_kernel(const EncAP PA, const EncBP PB, const int nblk_b) {
+    griddep_launch_dependents();
+    const int i = blockIdx.x;
+    if (i < nblk_b) {
+        if constexpr (MODE == 2) encode_b_simt_body(i % PB.nkc, i / PB.nkc, PB);
+        else encode_b_tc_body<MODE>(i % PB.nkc, i / PB.nkc, PB);
+    } else {
+        const int j = i - nblk_b;
+        encode_a_body<MODE>(j % PA.nkc, j / PA.nkc, PA);
+    }
+}
+
 // ---------------------------------------------------------------- launch ---
-namespace {
-// side stream + events for running encode B beside encode A (one per device)
-struct EncodeFork {
-    cudaStream_t side = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
-};
-std::mutex g_fork_mu;
-EncodeFork g_fork[64];
-}  // namespace
 
 cudaError_t launch_encode(const Geometry& g, const EncLayout& L, int64_t M, int64_t N, int64_t K,
                           const void* A, int64_t lda, const void* B, int64_t ldb, void* enc, int which,
@@ -627,58 +674,41 @@ cudaError_t launch_encode(const Geometry& g, const EncLayout& L, int64_t M, int6
     const int mode = g.dtype == FTGEMM_BF16 ? 0 : (g.dtype == FTGEMM_TF32 ? 1 : 2);
     auto F = [&](size_t off) { return reinterpret_cast<float*>(base + off); };
     cudaError_t e;
-    // Both operands: encode B runs on a side stream beside encode A (both are
-    // HBM streams far smaller than the machine's concurrency, so the two
-    // overlap their ramp-up and tails); the caller's stream waits for both.
-    cudaStream_t sb = st;
-    EncodeFork* fk = nullptr;
-    if ((which & 3) == 3) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        std::lock_guard<std::mutex> lk(g_fork_mu);
-        fk = (dev >= 0 && dev < 64) ? &g_fork[dev] : nullptr;
-        if (fk && !fk->side) {
-            if ((e = cudaStreamCreateWithFlags(&fk->side, cudaStreamNonBlocking)) != cudaSuccess) return e;
-            if ((e = cudaEventCreateWithFlags(&fk->fork, cudaEventDisableTiming)) != cudaSuccess) return e;
-            if ((e = cudaEventCreateWithFlags(&fk->join, cudaEventDisableTiming)) != cudaSuccess) return e;
-        }
-        if (fk) {
-            if ((e = cudaEventRecord(fk->fork, st)) != cudaSuccess) return e;
-            if ((e = cudaStreamWaitEvent(fk->side, fk->fork, 0)) != cudaSuccess) return e;
-            sb = fk->side;
-        }
-    }
+    EncAP pa{};
+    EncBP pb{};
     if (which & 2) {
-        if ((e = cudaMemsetAsync(base + L.cnt_b, 0, sizeof(int) * (size_t)g.tiles_n, sb)) != cudaSuccess) return e;
-        int* tk = reinterpret_cast<int*>(base + L.cnt_b);
-        dim3 grid(g.nkc_b, g.tiles_n);
-        if (mode == 2) {
-            encode_b_simt_kernel<<<grid, 256, 0, sb>>>(reinterpret_cast<const float*>(B), ldb, (int)N, (int)K, g.bnd,
-                                                       g.kp, g.nkc_b, g.enc_b_rows, F(L.br), F(L.cn2), F(L.brn2), tk,
-                                                       F(L.colnorm), F(L.brnorm));
-        } else {
-            uint8_t* Bt = (which & 4) ? nullptr : reinterpret_cast<uint8_t*>(base + L.bt);   // 4: no encoded operand
-#define ENC_B(MD) encode_b_tc_kernel<MD><<<grid, 256, 0, sb>>>(B, ldb, (int)N, (int)K, g.bnd, g.bn, g.kp, \
-            g.tiles_n * g.bn, g.nkc_b, g.enc_b_rows, F(L.br), Bt, F(L.cn2), F(L.brn2), tk, F(L.colnorm), F(L.brnorm))
-            if (mode == 0) ENC_B(0); else ENC_B(1);
-#undef ENC_B
-        }
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        // tickets of the last-block norm reduction (self-resetting; zeroed here
+        // because enc_ws is caller memory of unknown content)
+        if ((e = cudaMemsetAsync(base + L.cnt_b, 0, sizeof(int) * (size_t)g.tiles_n, st)) != cudaSuccess) return e;
+        uint8_t* Bt = (mode == 2 || (which & 4)) ? nullptr : reinterpret_cast<uint8_t*>(base + L.bt);   // 4: no encoded operand
+        pb = EncBP{B, ldb, (int)N, (int)K, g.bnd, g.bn, g.kp, g.tiles_n * g.bn, g.nkc_b, g.enc_b_rows,
+                   F(L.br), Bt, F(L.cn2), F(L.brn2), reinterpret_cast<int*>(base + L.cnt_b), F(L.colnorm), F(L.brnorm)};
     }
     if (which & 1) {
         if ((e = cudaMemsetAsync(base + L.cnt_a, 0, sizeof(int) * (size_t)g.tiles_m, st)) != cudaSuccess) return e;
-        uint8_t* Y = reinterpret_cast<uint8_t*>(base + L.y);
-        int* tk = reinterpret_cast<int*>(base + L.cnt_a);
-        dim3 grid(g.nkc_a, g.tiles_m);
-#define ENC_A(MD) encode_a_kernel<MD><<<grid, 256, 0, st>>>(A, lda, (int)M, (int)K, g.bmd, g.kp, g.bk, g.nkc_a, \
-            F(L.ac), Y, F(L.rn2), F(L.acn2), tk, F(L.rownorm), F(L.acnorm))
-        if (mode == 0) ENC_A(0); else if (mode == 1) ENC_A(1); else ENC_A(2);
-#undef ENC_A
+        pa = EncAP{A, lda, (int)M, (int)K, g.bmd, g.kp, g.bk, g.nkc_a, F(L.ac), reinterpret_cast<uint8_t*>(base + L.y),
+                   F(L.rn2), F(L.acn2), reinterpret_cast<int*>(base + L.cnt_a), F(L.rownorm), F(L.acnorm)};
+    }
+    if ((which & 3) == 3) {                      // both operands: one launch
+        const int nb = g.nkc_b * g.tiles_n, na = g.nkc_a * g.tiles_m;
+#define ENC_AB(MD) encode_ab_kernel<MD><<<nb + na, 256, 0, st>>>(pa, pb, nb)
+        if (mode == 0) ENC_AB(0); else if (mode == 1) ENC_AB(1); else ENC_AB(2);
+#undef ENC_AB
+        return cudaGetLastError();
+    }
+    if (which & 2) {
+        dim3 grid(g.nkc_b, g.tiles_n);
+        if (mode == 2) encode_b_simt_kernel<<<grid, 256, 0, st>>>(pb);
+        else if (mode == 0) encode_b_tc_kernel<0><<<grid, 256, 0, st>>>(pb);
+        else encode_b_tc_kernel<1><<<grid, 256, 0, st>>>(pb);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    if (sb != st) {
-        if ((e = cudaEventRecord(fk->join, sb)) != cudaSuccess) return e;
-        if ((e = cudaStreamWaitEvent(st, fk->join, 0)) != cudaSuccess) return e;
+    if (which & 1) {
+        dim3 grid(g.nkc_a, g.tiles_m);
+        if (mode == 0) encode_a_kernel<0><<<grid, 256, 0, st>>>(pa);
+        else if (mode == 1) encode_a_kernel<1><<<grid, 256, 0, st>>>(pa);
+        else encode_a_kernel<2><<<grid, 256, 0, st>>>(pa);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     return cudaSuccess;
 }

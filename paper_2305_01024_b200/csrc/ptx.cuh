@@ -134,6 +134,14 @@ __device__ __forceinline__ void tma_load_3d_pair(void* smem_dst, const CUtensorM
            "r"(c0), "r"(c1), "r"(c2) : "memory");
 }
 
+// programmatic dependent launch: the primary lets the next kernel in the stream
+// start launching; the dependent waits for the primary grid's completion and
+// memory visibility before touching its outputs
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // L2 eviction-priority policies for the TMA cache hints (kind: 1 evict_first,
 // 2 evict_last, 3 evict_normal); kind 0 = no hint (plain instructions below).
 __device__ __forceinline__ uint64_t l2_policy(int kind) {

@@ -196,6 +196,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
+    griddep_wait();                     // the encode (or any earlier kernel) has completed
     const uint32_t tmem_base = *tmem_holder;
 
     if (warp == 0) {
@@ -955,13 +956,18 @@ cudaError_t launch_tc_t(const CUtensorMap& mA, const CUtensorMap& mB, const CUte
     cfg.blockDim = dim3(Cfg::THREADS, 1, 1);
     cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    // programmatic dependent launch: the prologue (barrier init, TMEM
+    // allocation, descriptor prefetch) overlaps the tail of the encode kernel
+    // before it; every thread waits (griddepcontrol.wait) before reading anything
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, kern, mA, mB, mC, mC29, mY, a);
 }
 
