@@ -94,9 +94,38 @@ __global__ void __launch_bounds__(256, FTGEMM_SIMT_MINB) simt_ftgemm_kernel(cons
     }
 
     // global -> shared copies of one k-block (16-byte cp.async, NST-stage ring,
-    // out-of-range elements zero-filled), issued NST-1 k-blocks ahead
+    // out-of-range elements zero-filled), issued NST-1 k-blocks ahead.
+    // Interior tiles (whole 128 x 128 tile inside C, K a multiple of SK) take a
+    // guard-free path over per-thread source pointers computed once: the
+    // per-k-block index arithmetic of the general path ran on the FMA pipe
+    // beside the FFMA2 stream and spilled registers.
+    const bool interior = r0 + SB <= a.M && c0 + SB <= a.N && a.K % SK == 0;
+    const float* pa0 = a.A + (int64_t)(r0 + tid / (SK / 4)) * a.lda + (tid % (SK / 4)) * 4;
+    const float* pb0 = a.B + (int64_t)(tid >> 5) * a.ldb + c0 + (tid & 31) * 4;
+    constexpr int A_ROWS_PER_U = 256 / (SK / 4);        // A rows covered by one 256-thread pass
+    const int64_t a_ustep = (int64_t)A_ROWS_PER_U * a.lda, b_ustep = (int64_t)8 * a.ldb;
+    const uint32_t sa0 = (uint32_t)__cvta_generic_to_shared(&As[0][tid / (SK / 4)][(tid % (SK / 4)) * 4]);
+    const uint32_t sb0 = (uint32_t)__cvta_generic_to_shared(&Bs[0][tid >> 5][(tid & 31) * 4]);
     auto issue = [&](int kb, int s) {
         const int k0 = kb * SK;
+        if (interior) {
+            const float* pa = pa0 + k0;
+            const float* pb = pb0 + (int64_t)k0 * a.ldb;
+#pragma unroll
+            for (int u = 0; u < SK / 8; ++u) {
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
+                             :: "r"(sa0 + (uint32_t)(s * SB * SK + u * A_ROWS_PER_U * SK) * 4u), "l"(pa + u * a_ustep)
+                             : "memory");
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
+                             :: "r"(sb0 + (uint32_t)(s * SK * SB + u * 8 * SB) * 4u), "l"(pb + u * b_ustep)
+                             : "memory");
+            }
+            if (FT) {
+                if (tid < SK) cp_async4(&acs[s][tid], a.Ac + (int64_t)ti * a.kp + k0 + tid, 4);
+                else if (tid < 2 * SK) cp_async4(&brs[s][tid - SK], a.Br + (int64_t)tj * a.kp + k0 + tid - SK, 4);
+            }
+            return;
+        }
 #pragma unroll
         for (int u = 0; u < SK / 8; ++u) {                  // A: 128 rows x SK k, 16-byte chunks
             const int L = tid + 256 * u;
