@@ -46,6 +46,9 @@ __device__ __forceinline__ float simt_fault(float x, const DevInject& f) {
     return __uint_as_float(__float_as_uint(x) ^ (1u << (f.bit & 31)));
 }
 
+#ifndef FTGEMM_SIMT_AK
+#define FTGEMM_SIMT_AK 4     // k per A-fragment load (4: 16-byte loads, 2: 8-byte loads)
+#endif
 #ifndef FTGEMM_SIMT_MINB
 #define FTGEMM_SIMT_MINB 2
 #endif
@@ -177,6 +180,7 @@ __global__ void __launch_bounds__(256, FTGEMM_SIMT_MINB) simt_ftgemm_kernel(cons
         // two halves of 4 k: the thread's 8 rows x 4 k of A (one 16-byte load
         // per row), then per k the 8 columns of B; every output still sees
         // one fmaf per k in ascending k
+#if FTGEMM_SIMT_AK == 4
 #pragma unroll
         for (int kh = 0; kh < SK; kh += 4) {
             float4 ar[8];
@@ -197,6 +201,31 @@ __global__ void __launch_bounds__(256, FTGEMM_SIMT_MINB) simt_ftgemm_kernel(cons
                 }
             }
         }
+#else
+        // 2 k per A fragment load (8-byte loads): 16 fragment registers instead
+        // of 32, so the 8 x 8 accumulators, both fragments and the copy
+        // pointers fit the 128-register budget of 2 CTAs per SM without spills
+#pragma unroll
+        for (int kh = 0; kh < SK; kh += 2) {
+            float2 ar[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                ar[i] = *reinterpret_cast<const float2*>(&As[buf][(i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4)][kh]);
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kh + k][tx * 4]);
+                const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][kh + k][64 + tx * 4]);
+                const float2 bf2[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                                       make_float2(b1.z, b1.w)};
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const float av = k == 0 ? ar[i].x : ar[i].y;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc2[i][j] = __ffma2_rn(make_float2(av, av), bf2[j], acc2[i][j]);
+                }
+            }
+        }
+#endif
         if (FT) {
             // carried references, ascending k, once per k-block (one branch per warp)
             if (tid < SB) {
