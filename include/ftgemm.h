@@ -248,6 +248,10 @@ FTGEMM_API int ftgemm_plan(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_pl
  * 256-byte aligned); A and B are read-only.  The A part and the B part are
  * disjoint ([0, enc_b_offset) and [enc_b_offset, +enc_b_bytes)), so a B
  * encoded on one GPU can be broadcast with B and reused (weights).
+ * Asynchronous on stream: which = 3 is one kernel launch (plus two small
+ * memsets of the reduction tickets); a following ftgemm_run on the same stream
+ * may begin its prologue before the encode finishes (programmatic dependent
+ * launch) but reads nothing until it has.
  * Errors: INVALID_VALUE, UNSUPPORTED (misaligned), CUDA.                      */
 FTGEMM_API int ftgemm_encode(int dtype, int64_t M, int64_t N, int64_t K,
                   const void* A, int64_t lda, const void* B, int64_t ldb,

@@ -136,3 +136,35 @@ def test_encode_outputs(dtype, shape, dist):
             terms = rows.copy().view(np.float32).astype(np.float64)
         total = terms if r == 0 else total + terms
     assert np.array_equal(total, ac)                                # exact three-term split of Ac
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32", "f32_simt"])
+@pytest.mark.parametrize("shape", [SHAPES[1], SHAPES[2], SHAPES[4]], ids=lambda s: "x".join(map(str, s[:3])))
+def test_encode_one_launch_equals_per_operand(dtype, shape):
+    """Both operands in one launch (encode_ab_kernel, which = 3) write the same
+    bytes as the per-operand kernels (which = 1, then which = 2): the same
+    per-block arithmetic, only the block-index mapping differs."""
+    import torch
+    from paper_2305_01024_b200 import ftgemm as F
+    M, N, K, lda, ldb = shape
+    A, B, _ = synth.problem(M, N, K, dist="signed", dtype=odt(dtype))
+    Ad, Bd = padded(A, dtype, lda), padded(B, dtype, ldb)
+    g = F.FTGemm(dtype, M, N, K)
+    L = F.encode_layout(dtype, M, N, K)
+    p = g.plan
+    g.enc_ws.fill_(0x5A)
+    g.encode(Ad, Bd)
+    one = g.enc_ws.clone()
+    g.enc_ws.fill_(0xC3)
+    g.encode(Ad, None, which=1)
+    g.encode(None, Bd, which=2)
+    torch.cuda.synchronize()
+    two = g.enc_ws
+    kp = L["kp"]
+    regions = [("ac", p.tiles_m * kp * 4), ("br", p.tiles_n * kp * 4), ("rownorm", M * 4), ("colnorm", N * 4),
+               ("acnorm", p.tiles_m * 4), ("brnorm", p.tiles_n * 4)]
+    if dtype != "f32_simt":
+        regions += [("bt", kp * L["bt_ld"] * (2 if dtype == "bf16" else 4)), ("y", p.tiles_m * (kp // p.bk) * 384)]
+    for name, nbytes in regions:
+        o = L[name]
+        assert torch.equal(one[o:o + nbytes], two[o:o + nbytes]), name
