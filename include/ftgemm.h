@@ -236,6 +236,16 @@ typedef struct ftgemm_plan {
 /* Fill *out for a problem.  Errors: INVALID_VALUE (dims < 1, bad dtype, null out). */
 FTGEMM_API int ftgemm_plan(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* out);
 
+/* Force the tile class of the tensor-core paths (TF32, BF16) for every later
+ * ftgemm_plan / ftgemm_encode / ftgemm_run* call in this process: bn in
+ * {128, 256} (check tile 125 x (bn - 4)), cta_group in {1, 2}; (0, 0) restores
+ * the plan's own choice (wave-quantised cost model, skinny-shape rules, which
+ * are never overridden).  Used by M-block partitions so that every rank runs the
+ * full problem's check tiles (concatenated C and event positions
+ * identical to the one-GPU run).  Process-wide; not synchronised with calls in
+ * flight on other host threads.  Errors: INVALID_VALUE.                        */
+FTGEMM_API int ftgemm_set_tile_class(int bn, int cta_group);
+
 /* ---- encode (Eq. 1 / Eq. 2) -------------------------
  * which = 1: encode A  ->  per check-tile i: Ac_i[k] = sum_{p in tile rows} A[p,k]
  *                         (FP32), its exact split into three operand-format

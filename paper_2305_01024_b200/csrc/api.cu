@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cstdarg>
+#include <atomic>
 #include <cmath>
 #include <limits>
 #include <cstdio>
@@ -66,6 +67,9 @@ int fail_cuda(cudaError_t e, const char* where) {
 
 bool valid_dtype(int d) { return d == FTGEMM_F32_SIMT || d == FTGEMM_TF32 || d == FTGEMM_BF16; }
 
+// forced tile class of the tensor-core paths (0 = the plan's own choice)
+std::atomic<int> g_force_bn{0}, g_force_cg{0};
+
 // The shape-class table (north_star item 4): compile-time instantiations
 // chosen per problem shape.
 void fill_plan(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* p) {
@@ -88,19 +92,37 @@ void fill_plan(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* p) {
         // 252-column tile; M <= 250: a CTA pair (2 x 125 rows) per unit
         const bool skinny_n = N <= 252;
         const bool skinny_m = M <= 250 && !skinny_n;
-        const bool small = !skinny_n && !skinny_m && (tiles256 < 2 * kNumSMsB200 || N <= 512);
-        const int bn = small ? 128 : 256;
-        p->shape_class = small ? FTGEMM_SHAPE_SMALL_N : FTGEMM_SHAPE_SQUARE;
+        const int64_t tiles_m125 = (M + 124) / 125;
+        bool small = !skinny_n && !skinny_m && (tiles256 < 2 * kNumSMsB200 || N <= 512);
+        // CTA pairs (cta_group::2, M = 256 per MMA) halve the B tile each SM
+        // loads; they lose on K = 128 shapes (epilogue-bound) and skinny M
+        int cg = (!small && ((tiles_m125 >= 4 && (K >= 2048 || (dtype == FTGEMM_TF32 && K >= 1024))) ||
+                             (skinny_m && K >= 1024))) ? 2 : 1;
+        if (!skinny_n && !skinny_m && K >= 1024) {
+            // Mainloop-bound shapes: wave-quantised cost model over the four tile
+            // classes, time = ceil(units / concurrent units) x (per-wave time of
+            // the class at K = 8192, measured on B200: profiles/r1d_tile_classes.md)
+            struct Cls { int bn, cg; double c_bf16, c_tf32; };
+            const Cls cls[4] = {{256, 2, 54.5, 108.7}, {256, 1, 68.7, 140.2}, {128, 1, 48.0, 98.8}, {128, 2, 49.8, 102.9}};
+            double best = 1e300;
+            for (const Cls& c : cls) {
+                const int64_t tn = (N + c.bn - 5) / (c.bn - 4);
+                const int64_t units = ((tiles_m125 + c.cg - 1) / c.cg) * tn;
+                const int64_t slots = kNumSMsB200 / c.cg;
+                const double t = (double)((units + slots - 1) / slots) * (dtype == FTGEMM_TF32 ? c.c_tf32 : c.c_bf16);
+                if (t < best * (1.0 - 1e-9)) { best = t; small = c.bn == 128; cg = c.cg; }
+            }
+        }
+        int bn = small ? 128 : 256;
+        // explicit class (ftgemm_set_tile_class: multi-GPU ranks use the full
+        // problem's class), then the tuning environment overrides
+        const int fbn = g_force_bn.load(std::memory_order_relaxed), fcg = g_force_cg.load(std::memory_order_relaxed);
+        if (fbn && !skinny_n && !skinny_m) { bn = fbn; cg = fcg; }
+        if (const char* e = getenv("FTGEMM_BN")) bn = atoi(e) == 128 ? 128 : 256;
+        p->shape_class = bn == 128 ? FTGEMM_SHAPE_SMALL_N : FTGEMM_SHAPE_SQUARE;
         p->bm = 128; p->bn = bn; p->bk = bk;
         p->check_tile_m = 125; p->check_tile_n = bn - 4;
         p->off_tile_m = 128; p->off_tile_n = bn;
-        // CTA pairs (cta_group::2, M = 256 per MMA) halve the B tile each SM
-        // loads; measured on B200 (profiles/r1_sweep.md, the CG sweep) they pay
-        // off for the large-tile class with enough K to amortise the pair
-        // handshake (BF16 K >= 2048, TF32 K >= 1024) and lose on K = 128 shapes
-        const int64_t tiles_m125 = (M + 124) / 125;
-        int cg = (bn == 256 && ((tiles_m125 >= 4 && (K >= 2048 || (dtype == FTGEMM_TF32 && K >= 1024))) ||
-                                (skinny_m && K >= 1024))) ? 2 : 1;
         if (const char* e = getenv("FTGEMM_CG")) cg = atoi(e) == 2 ? 2 : 1;
         p->cta_group = cg;
         const int elt = dtype == FTGEMM_TF32 ? 4 : 2;
@@ -227,6 +249,20 @@ int tile_key(const ftgemm_plan_t& p, int ti, int tj) {
 extern "C" {
 
 int ftgemm_version(void) { return FTGEMM_ABI_VERSION; }
+
+int ftgemm_set_tile_class(int bn, int cta_group) {
+    if (bn == 0 && cta_group == 0) {
+        g_force_bn.store(0); g_force_cg.store(0);
+        g_err.clear();
+        return FTGEMM_OK;
+    }
+    if ((bn != 128 && bn != 256) || (cta_group != 1 && cta_group != 2))
+        return fail(FTGEMM_ERR_INVALID_VALUE, "tile class must be bn in {128, 256}, cta_group in {1, 2} (or 0, 0)");
+    g_force_cg.store(cta_group);
+    g_force_bn.store(bn);
+    g_err.clear();
+    return FTGEMM_OK;
+}
 int ftgemm_device_arch(void) { return 1000; }
 const char* ftgemm_last_error(void) { return g_err.c_str(); }
 

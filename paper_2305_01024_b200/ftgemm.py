@@ -65,7 +65,8 @@ class Cost(C.Structure):
 
 SYMBOLS = ("ftgemm_plan", "ftgemm_encode", "ftgemm_encode_layout", "ftgemm_run", "ftgemm_run_fused", "ftgemm_run_online", "ftgemm_run_offline", "ftgemm_cost_model",
            "ftgemm_nonfused_workspace", "ftgemm_run_nonfused",
-           "ftgemm_report", "ftgemm_report_reset", "ftgemm_last_error", "ftgemm_version", "ftgemm_device_arch")
+           "ftgemm_report", "ftgemm_report_reset", "ftgemm_last_error", "ftgemm_version", "ftgemm_device_arch",
+           "ftgemm_set_tile_class")
 
 _lib = None
 
@@ -95,6 +96,7 @@ def lib():
                                           vp, vp, C.c_int, vp, i32, vp, vp]
         L.ftgemm_report.argtypes = [vp, C.POINTER(Counts), vp, i32, vp]
         L.ftgemm_report_reset.argtypes = [vp, i64, vp]
+        L.ftgemm_set_tile_class.argtypes = [C.c_int, C.c_int]
         L.ftgemm_last_error.restype = C.c_char_p
         for n in SYMBOLS:
             if n != "ftgemm_last_error":
@@ -155,6 +157,27 @@ def plan(dtype, M: int, N: int, K: int) -> Plan:
     p = PlanStruct()
     _check(lib().ftgemm_plan(_dt(dtype), M, N, K, C.byref(p)), "ftgemm_plan")
     return Plan(**{f: getattr(p, f) for f in Plan.__dataclass_fields__})
+
+
+def set_tile_class(bn: int = 0, cta_group: int = 0) -> None:
+    """Force the tensor-core tile class (bn 128 | 256, cta_group 1 | 2) for later
+    calls in this process; (0, 0) restores the plan's own choice."""
+    _check(lib().ftgemm_set_tile_class(bn, cta_group), "ftgemm_set_tile_class")
+
+
+class tile_class:
+    """Context manager around set_tile_class (restores automatic choice on exit)."""
+
+    def __init__(self, bn: int, cta_group: int):
+        self.bn, self.cg = bn, cta_group
+
+    def __enter__(self):
+        set_tile_class(self.bn, self.cg)
+        return self
+
+    def __exit__(self, *exc):
+        set_tile_class(0, 0)
+        return False
 
 
 def encode_layout(dtype, M: int, N: int, K: int) -> dict:

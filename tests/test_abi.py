@@ -90,6 +90,14 @@ def test_plan_table(F, dtype):
         assert sn.bn == 256 and sn.tiles_n == 1
         big = F.plan(dtype, 8192, 8192, 8192)
         assert big.cta_group == 2 and big.stages >= 4
+        # wave-quantised class choice (profiles/r1d_tile_classes.md): 99 pair units
+        # (2 waves) beat 330 BN=128 tiles (3 waves) at 8192 x 512 x 8192
+        nar = F.plan(dtype, 8192, 512, 8192)
+        assert nar.bn == 256 and nar.cta_group == 2
+        k1 = F.plan(dtype, 8192, 8192, 1024)
+        assert k1.bn == 256 and k1.cta_group == 2
+        k128 = F.plan(dtype, 16384, 16384, 128)       # epilogue-bound: one CTA per MMA
+        assert k128.bn == 256 and k128.cta_group == 1
 
 
 def test_plan_errors(F):
@@ -184,3 +192,24 @@ def test_nonfused_host_checks(F):
     vp = C.c_void_p(16)
     assert lib.ftgemm_run_nonfused(1, 64, 64, 64, 1.0, vp, 64, vp, 64, 0.0, vp, 64, vp, vp, 2, None, 0, vp, None) == 2
     assert lib.ftgemm_run_nonfused(2, 64, 64, 64, 1.0, vp, 64, vp, 64, 0.0, vp, 64, None, None, 2, None, 0, vp, None) == 1
+
+
+def test_set_tile_class(F):
+    """ftgemm_set_tile_class forces the tensor-core class for later plans (the
+    multi-GPU partition runs every rank with the full problem's check tiles);
+    (0, 0) restores the plan's own choice; skinny shapes keep their rule."""
+    auto = F.plan("bf16", 8192, 8192, 8192)
+    assert (auto.bn, auto.cta_group) == (256, 2)
+    with F.tile_class(128, 1):
+        p = F.plan("bf16", 8192, 8192, 8192)
+        assert (p.bn, p.cta_group, p.check_tile_n) == (128, 1, 124)
+        sn = F.plan("bf16", 16384, 128, 16384)
+        assert sn.bn == 256 and sn.tiles_n == 1
+        s = F.plan("f32_simt", 1024, 1024, 1024)
+        assert s.bn == 128 and s.check_tile_n == 128
+    back = F.plan("bf16", 8192, 8192, 8192)
+    assert (back.bn, back.cta_group) == (256, 2)
+    with pytest.raises(F.FtgemmError):
+        F.set_tile_class(192, 1)
+    with pytest.raises(F.FtgemmError):
+        F.set_tile_class(256, 3)

@@ -3,6 +3,7 @@ same seeded inputs.  Bars (north_star): detected / corrected positions and
 counts bit-exact; C within a relative Frobenius tolerance of 1e-6 (FP32 SIMT),
 5e-3 (TF32), 2e-2 (BF16); bit-exact where the arithmetic is exact (integer
 inputs; the SIMT kernel against the oracle's sequential-fmaf mode)."""
+import contextlib
 import math
 
 import numpy as np
@@ -298,15 +299,18 @@ def test_partition_invariance(dtype, shape):
         parts = row_partition(M, world, tm)
         Cp, evs = [], []
         for row0, rows in parts:
-            gp = F.FTGemm(dtype, rows, N, K)
-            assert (gp.plan.bn, gp.plan.cta_group, gp.plan.check_tile_m, gp.plan.check_tile_n) == \
-                (full_plan.bn, full_plan.cta_group, full_plan.check_tile_m, full_plan.check_tile_n)
-            mine = [(r - row0, c, k, b, m, tg, ad) for (r, c, k, b, m, tg, ad) in inj if row0 <= r < row0 + rows]
-            Cd = synth.to_torch(Cin[row0:row0 + rows], odt(dtype)).cuda()
-            Ar = Ad[row0:row0 + rows].contiguous()
-            gp.encode(Ar, Bd)
-            gp.run(Ar, Bd, Cd, alpha=1.0, beta=0.5, injections=mine)
-            torch.cuda.synchronize()
+            # a rank runs the full problem's tile class (as distributed.PartitionedFTGemm does)
+            cls = F.tile_class(full_plan.bn, full_plan.cta_group) if dtype != "f32_simt" else contextlib.nullcontext()
+            with cls:
+                gp = F.FTGemm(dtype, rows, N, K)
+                assert (gp.plan.bn, gp.plan.cta_group, gp.plan.check_tile_m, gp.plan.check_tile_n) == \
+                    (full_plan.bn, full_plan.cta_group, full_plan.check_tile_m, full_plan.check_tile_n)
+                mine = [(r - row0, c, k, b, m, tg, ad) for (r, c, k, b, m, tg, ad) in inj if row0 <= r < row0 + rows]
+                Cd = synth.to_torch(Cin[row0:row0 + rows], odt(dtype)).cuda()
+                Ar = Ad[row0:row0 + rows].contiguous()
+                gp.encode(Ar, Bd)
+                gp.run(Ar, Bd, Cd, alpha=1.0, beta=0.5, injections=mine)
+                torch.cuda.synchronize()
             _, e = gp.report()
             for x in e:
                 x = dict(x)
