@@ -19,14 +19,16 @@
 //
 // so the check tile is 125 x (BN-4) and verification needs no extra MMA.
 // With FT off the same kernel family reads A and the row-major B directly
-// (B N-major, 128 x BN data tiles).  Warp roles (one CTA per SM, persistent):
-//   warp 0      TMA producer
-//   warp 1      MMA issuer (one thread: tcgen05.mma, tcgen05.commit)
-//   warp 2      TMEM allocator
-//   warps 4..7  epilogue: TMEM -> registers; row sums (thread = row), column
-//               sums (warp transpose-reduce + smem), residuals vs thresholds,
-//               locate, correct, alpha/beta, store; they
-//               also service mid-mainloop fault injections
+// (B N-major, 128 x BN data tiles).  Warp roles (one CTA per SM, persistent;
+// E = 4 x epilogue warpgroups = 8 with FT, 4 without):
+//   warps 0..E-1  epilogue: TMEM -> registers; row sums (thread = row), column
+//                 sums (warp transpose-reduce + smem), residuals vs thresholds,
+//                 locate, correct, alpha/beta, store; they
+//                 also service mid-mainloop fault injections
+//   warp E        TMEM allocator (+ in-kernel A encode with warp E+1)
+//   warp E+2      TMA producer
+//   warp E+3      MMA issuer (one thread: tcgen05.mma, tcgen05.commit)
+// (FTGEMM_ROLES_HI=0 restores the earlier layout: producer 0, MMA 1, epilogue 4..)
 // The accumulator is double-buffered in TMEM (2 x BN columns), so the epilogue
 // of tile t (verification included) overlaps the mainloop of tile t+1.
 #include <cstdint>
@@ -40,6 +42,9 @@ namespace ftg {
 // epilogue warpgroups: 2 = one warpgroup per TMEM accumulator buffer, so the
 // epilogues (verification included) of two consecutive tiles run concurrently
 // (FT on); FT off keeps one and spends the staging memory on a deeper ring
+#ifndef FTGEMM_ROLES_HI
+#define FTGEMM_ROLES_HI 1
+#endif
 #ifndef FTGEMM_EPI_WG
 #define FTGEMM_EPI_WG 2
 #endif
@@ -156,6 +161,17 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     float* acsq = nsq + 2 * 2 * 128;                          // [2 acc][2 half] sum of (e^T A)^2
 
     const int warp = threadIdx.x >> 5;
+    // Warp roles.  The SM sub-partition scheduler favours the highest warp id
+    // among eligible warps, and the single MMA-issuing thread is latency
+    // critical, so the control warps take the highest ids (MMA issuer = the last
+    // warp, TMA producer = the one before) and the epilogue warps (whose TMEM
+    // lane quadrant is warp % 4) the lowest.
+    constexpr int kEpiWarps = 4 * kEpiWG;
+#if FTGEMM_ROLES_HI
+    constexpr int W_EPI0 = 0, W_ALLOC = kEpiWarps, W_ENC0 = kEpiWarps, W_PROD = kEpiWarps + 2, W_MMA = kEpiWarps + 3;
+#else
+    constexpr int W_PROD = 0, W_MMA = 1, W_ALLOC = 2, W_ENC0 = 2, W_EPI0 = 4;
+#endif
     const uint32_t lane = lane_id();
     // CTA pair: rank 0 is the MMA leader; each CTA owns 128 of the 256 MMA rows
     // (one check tile) and half of the B tile's columns
@@ -163,7 +179,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const bool leader = rank == 0;
     const int cluster_id = blockIdx.x / CG, num_clusters = gridDim.x / CG;
 
-    if (warp == 0 && lane == 0) {
+    if (warp == W_PROD && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
         tma_prefetch_desc(&tmC);
@@ -192,14 +208,14 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         }
         fence_barrier_init();
     }
-    if (warp == 2) tmem_alloc<Cfg::TMEM_COLS, CG>(tmem_holder);
+    if (warp == W_ALLOC) tmem_alloc<Cfg::TMEM_COLS, CG>(tmem_holder);
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
     griddep_wait();                     // the encode (or any earlier kernel) has completed
     const uint32_t tmem_base = *tmem_holder;
 
-    if (warp == 0) {
+    if (warp == W_PROD) {
         // ------------------------------------------------ TMA producer ----
         if (lane == 0) {
             int s = 0; uint32_t ph = 0;
@@ -275,7 +291,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == W_MMA) {
         // ------------------------------------------------- MMA issuer -----
         if (lane == 0 && leader) {
             constexpr uint32_t idesc = instr_desc(kTF32, Cfg::BM * CG, BN, false, true);
@@ -354,7 +370,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             }
         }
         __syncwarp();
-    } else if (warp == 2 || warp == 3) {
+    } else if (warp == W_ENC0 || warp == W_ENC0 + 1) {
         // ------------------------------------- in-kernel encode of A -------
         // (the paper's threadblock-level fusion of the
         // checksum encoding into the prefetch stage.)  Per k-block,
@@ -365,7 +381,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         // row, warp 3 chunks 4..7; lane = (row group rg, chunk cq).
         if (FT && a.fuse_a) {
             constexpr int EPC = kTF32 ? 4 : 8;            // elements per 16-byte chunk
-            const int half = warp - 2;
+            const int half = warp - W_ENC0;
             const int cq = lane & 3, rg = lane >> 2;
             const int c = 4 * half + cq;                  // 16-byte chunk of the row
             auto arrive_yrdy = [&](uint64_t* bar) {
@@ -466,13 +482,13 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 if (lane == 0) mbar_arrive(&nrdy[acc]);     // release: the epilogue of this tile may read them
             }
         }
-    } else if (warp >= 4) {
+    } else if (warp >= W_EPI0 && warp < W_EPI0 + kEpiWarps) {
         // ----------------------------------------------------- epilogue -----
-        const int wg = (warp - 4) >> 2;          // epilogue warpgroup (owns accumulator buffer wg when kEpiWG == 2)
-        const int ew = (warp - 4) & 3;           // TMEM lane quadrant
+        const int wg = (warp - W_EPI0) >> 2;          // epilogue warpgroup (owns accumulator buffer wg when kEpiWG == 2)
+        const int ew = (warp - W_EPI0) & 3;           // TMEM lane quadrant
         const int rloc = ew * 32 + (int)lane;    // row of the 128-row tile
         const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
-        const int et = threadIdx.x - 128 - 128 * wg;   // 0..127
+        const int et = threadIdx.x - 32 * W_EPI0 - 128 * wg;   // 0..127
         const uint32_t ebar = 1 + wg;            // named barrier of this warpgroup
         uint32_t injph0 = 0, injph1 = 0, cph = 0, gcount = 0;   // gcount: store groups issued by this warp
         const int hc = (a.l2hint >> 4) & 3;
@@ -931,7 +947,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     tc_fence_before();
     // a CTA pair stays resident until both are done (remote arrivals, pair MMA into the peer's TMEM)
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
-    if (warp == 2) {
+    if (warp == W_ALLOC) {
         tc_fence_after();
         tmem_dealloc<Cfg::TMEM_COLS, CG>(tmem_base);
     }
