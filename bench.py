@@ -265,7 +265,7 @@ def run_ours(args):
     counts, events = g.report()
     ok_faults = counts["corrected"] == n_injected and counts["uncorrectable"] == 0 and counts["checksum_only"] == 0
     value = flops_rank * world / (ms_step * 1e-3) / 1e12
-    launches_per_step = 3   # encode_a, encode_b, fused GEMM (tickets reset by cudaMemsetAsync, not kernels)
+    launches_per_step = 2   # encode_ab (both operands, one launch), fused GEMM (tickets reset by cudaMemsetAsync, not kernels)
 
     extra = {}
     if not args.no_sweep:
