@@ -395,6 +395,8 @@ def run_ours(args):
             "ft_step_ms": med["ft_step"], "ft_run_only_ms": med["ft_run"],
             "encode_ms": med["encode"], "encode_a_ms": med["encode_a"],
             "encode_gbs": (2 * Mr * K + 2 * K * N + 2 * K * pl.tiles_n * pl.bn) / (med["encode"] * 1e-3) / 1e9,
+            "encode_hbm_frac": (2 * Mr * K + 2 * K * N + 2 * K * pl.tiles_n * pl.bn) / (med["encode"] * 1e-3) / 1e9
+            / load_peaks()[0]["hbm_gbs"],
             "overhead_vs_ft_off_pct": 100.0 * (med["ft_step"] - t_off) / t_off,
             "overhead_vs_cublas_pct": 100.0 * (med["ft_step"] - t_cub) / t_cub,
             "overhead_run_only_vs_ft_off_pct": 100.0 * (med["ft_run"] - t_off) / t_off,
@@ -434,6 +436,10 @@ def run_ours(args):
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": "tc_ftgemm_kernel<bf16,256,FT>", "peak_kind": f"{kind} bf16 burst",
                 "algorithmic_flops_per_launch": flops_rank}
+    if peaks.get("bf16_tflops_sustained"):
+        # the same kernel against cuBLAS's sustained (power-capped, 4 s back to back) figure
+        roofline["peak_sustained"] = peaks["bf16_tflops_sustained"]
+        roofline["frac_sustained"] = achieved / peaks["bf16_tflops_sustained"]
 
     if rank == 0:
         cpu = None
