@@ -682,3 +682,42 @@ def test_back_to_back_steps_no_stale_encode(dtype):
     assert counts["tiles_detected"] == 0, counts
     for i, C in enumerate(outs):
         assert torch.equal(C, ref[i % 2]), i
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("beta", [0.0, 0.5])
+def test_host_pipeline_matches_isolated_steps(dtype, beta):
+    """paper_2305_01024_b200.pipeline.HostPipeline (H2D of step s+1, kernels of
+    step s, D2H of step s-1 on three streams, two device slots) returns, for
+    every step, the same bits as an isolated synchronised step on the same host
+    inputs -- with alternating inputs, so a slot reused too early would show."""
+    import torch
+    from paper_2305_01024_b200 import ftgemm as F
+    from paper_2305_01024_b200.pipeline import HostPipeline
+    M, N, K = 1000, 2016, 1024
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    sets = []
+    for s in range(3):
+        A, B, Cin = synth.problem(M, N, K, dtype=odt(dtype), seed=230501024 + 31 * s)
+        sets.append(tuple(synth.to_torch(x, odt(dtype)).pin_memory() for x in (A, B, Cin)))
+    g = F.FTGemm(dtype, M, N, K)
+    ref = []
+    for A, B, Cin in sets:
+        C = Cin.cuda()
+        g.encode(A.cuda(), B.cuda())
+        g.run(A.cuda(), B.cuda(), C, beta=beta)
+        torch.cuda.synchronize()
+        ref.append(C.cpu())
+    g.reset()
+    pipe = HostPipeline(g)
+    outs = []
+    for i in range(7):
+        A, B, Cin = sets[i % 3]
+        Ch = Cin.clone().pin_memory()          # beta != 0: C_in travels in, C out
+        pipe.submit(A, B, Ch, beta=beta)
+        outs.append(Ch)
+    pipe.synchronize()
+    counts, _ = g.report()
+    assert counts["tiles_detected"] == 0, counts
+    for i, Ch in enumerate(outs):
+        assert torch.equal(Ch, ref[i % 3]), i
