@@ -463,7 +463,6 @@ static int run_impl(int dtype, int64_t M, int64_t N, int64_t K, float alpha, con
         a.ks_kb = ks > 0 ? (int)std::min<int64_t>(ks / p.bk, num_kb) : 0;
         a.fuse_a = fuse_a;
         a.b3d = b3d ? 1 : 0;
-        a.l2hint = l2_hint_bits();
         if (ft) {
             a.Y = enc + L.y; a.kp = g.kp;
             a.rownorm = (const float*)(enc + L.rownorm); a.colnorm = (const float*)(enc + L.colnorm);

@@ -44,7 +44,6 @@ struct TcArgs {
     int ks_kb;            // > 0: verify after every ks_kb k-blocks too (online-interval mode)
     int fuse_a;           // 1: the A-side encode (split e^T A rows, row / tile norms) runs in the kernel
     int b3d;              // 1: tmB is the 3-D (column slice, k, column block) view of B / B^r
-    int l2hint;           // TMA L2 eviction hints: bits 0-1 A, 2-3 B, 4-5 C stores (0 none, 1 first, 2 last, 3 normal)
     float alpha, beta;
     void* C; int64_t ldc;
     const void* Y; int kp;
@@ -75,14 +74,6 @@ inline int tc_group(int units_m, int cg) {
     if (const char* e = getenv("FTGEMM_GROUP")) g0 = atoi(e) > 0 ? atoi(e) : g0;
     const int ng = units_m / g0 > 0 ? (units_m + g0 / 2) / g0 : 1;
     return (units_m + ng - 1) / ng;
-}
-
-// TMA L2 eviction hints of the tensor-core kernel (TcArgs::l2hint; FTGEMM_L2HINT
-// overrides, for tuning)
-inline int l2_hint_bits() {
-    int h = 0;
-    if (const char* e = getenv("FTGEMM_L2HINT")) h = atoi(e) & 63;
-    return h;
 }
 
 // ---- tile geometry of a plan ---------------------------------------------

@@ -142,55 +142,6 @@ __device__ __forceinline__ void griddep_launch_dependents() {
 }
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-// L2 eviction-priority policies for the TMA cache hints (kind: 1 evict_first,
-// 2 evict_last, 3 evict_normal); kind 0 = no hint (plain instructions below).
-__device__ __forceinline__ uint64_t l2_policy(int kind) {
-    uint64_t p;
-    if (kind == 1)      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    else if (kind == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    else                asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-// hinted variants of the loads above (same operands + the 64-bit policy)
-__device__ __forceinline__ void tma_load_2d_h(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
-                                              int32_t c0, int32_t c1, uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%3, %4}], [%2], %5;"
-        :: "r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)),
-           "r"(c0), "r"(c1), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void tma_load_2d_pair_h(void* smem_dst, const CUtensorMap* map, uint32_t mbar_cluster_addr,
-                                                   int32_t c0, int32_t c1, uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%3, %4}], [%2], %5;"
-        :: "r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar_cluster_addr),
-           "r"(c0), "r"(c1), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void tma_load_3d_h(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
-                                              int32_t c0, int32_t c1, int32_t c2, uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%3, %4, %5}], [%2], %6;"
-        :: "r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)),
-           "r"(c0), "r"(c1), "r"(c2), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void tma_load_3d_pair_h(void* smem_dst, const CUtensorMap* map, uint32_t mbar_cluster_addr,
-                                                   int32_t c0, int32_t c1, int32_t c2, uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%3, %4, %5}], [%2], %6;"
-        :: "r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar_cluster_addr),
-           "r"(c0), "r"(c1), "r"(c2), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void tma_store_2d_h(const CUtensorMap* map, const void* smem_src, int32_t c0, int32_t c1,
-                                               uint64_t pol) {
-    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;"
-                 :: "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem_src)), "r"(c0), "r"(c1), "l"(pol)
-                 : "memory");
-}
-
 // TMA tile store shared -> global (bulk-group completion)
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* smem_src, int32_t c0, int32_t c1) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"

@@ -236,8 +236,6 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             const uint32_t bytes_cta = !FT ? (Cfg::A_BYTES + Cfg::B_BYTES)
                                      : fa ? Cfg::B_BYTES : (Cfg::BMD * 128 + Cfg::Y_BYTES + Cfg::B_BYTES);
 #endif
-            const int ha = a.l2hint & 3, hb = (a.l2hint >> 2) & 3;
-            const uint64_t pa = l2_policy(ha), pb = l2_policy(hb);
             for (int u = cluster_id; u < a.num_units; u += num_clusters) {
                 int tmu, tj;
                 tile_coords(u, a.units_m, a.tiles_n, a.group, tmu, tj);
@@ -254,16 +252,12 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         tma_load_2d(sa, &tmA, &afull[s], kb * Cfg::BK, row0);
                     }
                     if constexpr (CG == 1) {
-                        if (!fa) {
-                            if (ha) tma_load_2d_h(sa, &tmA, &full[s], kb * Cfg::BK, row0, pa);
-                            else tma_load_2d(sa, &tmA, &full[s], kb * Cfg::BK, row0);
-                        }
+                        if (!fa) tma_load_2d(sa, &tmA, &full[s], kb * Cfg::BK, row0);
 #if !defined(FTGEMM_EXP_A128)
                         if (FT && !fa) tma_load_2d(sa + Cfg::BMD * 128, &tmY, &full[s], 0, ti * a.num_kb + kb);
 #endif
                         if (b3d) {
-                            if (hb) tma_load_3d_h(sb, &tmB, &full[s], 0, kb * Cfg::BK, colb / Cfg::BOXN, pb);
-                            else tma_load_3d(sb, &tmB, &full[s], 0, kb * Cfg::BK, colb / Cfg::BOXN);
+                            tma_load_3d(sb, &tmB, &full[s], 0, kb * Cfg::BK, colb / Cfg::BOXN);
                         } else {
 #pragma unroll
                             for (int b = 0; b < Cfg::NBOX; ++b)
@@ -271,16 +265,12 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         }
                     } else {
                         const uint32_t mb = smem_u32(&full[s]) & kPeerBitMask;
-                        if (!fa) {
-                            if (ha) tma_load_2d_pair_h(sa, &tmA, mb, kb * Cfg::BK, row0, pa);
-                            else tma_load_2d_pair(sa, &tmA, mb, kb * Cfg::BK, row0);
-                        }
+                        if (!fa) tma_load_2d_pair(sa, &tmA, mb, kb * Cfg::BK, row0);
 #if !defined(FTGEMM_EXP_A128)
                         if (FT && !fa) tma_load_2d_pair(sa + Cfg::BMD * 128, &tmY, mb, 0, ti * a.num_kb + kb);
 #endif
                         if (b3d) {
-                            if (hb) tma_load_3d_pair_h(sb, &tmB, mb, 0, kb * Cfg::BK, colb / Cfg::BOXN, pb);
-                            else tma_load_3d_pair(sb, &tmB, mb, 0, kb * Cfg::BK, colb / Cfg::BOXN);
+                            tma_load_3d_pair(sb, &tmB, mb, 0, kb * Cfg::BK, colb / Cfg::BOXN);
                         } else {
 #pragma unroll
                             for (int b = 0; b < Cfg::NBOX / CG; ++b)
@@ -491,8 +481,6 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const int et = threadIdx.x - 32 * W_EPI0 - 128 * wg;   // 0..127
         const uint32_t ebar = 1 + wg;            // named barrier of this warpgroup
         uint32_t injph0 = 0, injph1 = 0, cph = 0, gcount = 0;   // gcount: store groups issued by this warp
-        const int hc = (a.l2hint >> 4) & 3;
-        const uint64_t pc = l2_policy(hc);
         uint64_t* cbw = &cbar[4 * wg + ew];
         uint8_t* stg = stg0 + wg * Cfg::STG_BYTES;
         float* colsum = reinterpret_cast<float*>(stg);                            // [4][BN] (aliases staging)
@@ -933,8 +921,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 __syncwarp();
                 if (lane == 0) {
 #if !defined(FTGEMM_EXP_NO_STORE)
-                    if (hc) tma_store_2d_h(cmap, sbuf, gcol, grow, pc);
-                    else tma_store_2d(cmap, sbuf, gcol, grow);
+                    tma_store_2d(cmap, sbuf, gcol, grow);
 #endif
                     bulk_commit();
                 }

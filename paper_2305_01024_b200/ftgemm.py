@@ -96,11 +96,12 @@ def lib():
                                           vp, vp, C.c_int, vp, i32, vp, vp]
         L.ftgemm_report.argtypes = [vp, C.POINTER(Counts), vp, i32, vp]
         L.ftgemm_report_reset.argtypes = [vp, i64, vp]
-        L.ftgemm_set_tile_class.argtypes = [C.c_int, C.c_int]
         L.ftgemm_last_error.restype = C.c_char_p
         for n in SYMBOLS:
-            if n != "ftgemm_last_error":
+            if n != "ftgemm_last_error" and hasattr(L, n):
                 getattr(L, n).restype = C.c_int
+        if hasattr(L, "ftgemm_set_tile_class"):          # absent from development builds of older sources
+            L.ftgemm_set_tile_class.argtypes = [C.c_int, C.c_int]
         _lib = L
     return _lib
 

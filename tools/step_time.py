@@ -38,6 +38,7 @@ for lib, F, g in gs:
     fns[name + ":step"] = (lambda g=g, F=F: (g.encode(A, B), g.run(A, B, C, ft_level=F.FT_CORRECT)))
     fns[name + ":run"] = (lambda g=g, F=F: g.run(A, B, C, ft_level=F.FT_CORRECT))
     fns[name + ":encode"] = (lambda g=g: g.encode(A, B))
+    fns[name + ":off"] = (lambda g=g, F=F: g.run(A, B, C, ft_level=F.FT_OFF))
 ev = {k: [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)] for k in fns}
 for f in fns.values():
     f()
