@@ -29,7 +29,11 @@ namespace ftg {
 #endif
 constexpr int SB = 128, SK = FTGEMM_SIMT_SK;       // tile, k-block (plan.bk)
 constexpr int NST = SK == 8 ? 4 : 3;                // smem pipeline stages
-constexpr int STAGE_FLOATS = SB * SK + SK * SB + 2 * SK;
+// A tile rows padded by 4 floats: the row-reference FMAs read A[p][k] with one
+// thread per row, which at a 64-byte row pitch hit 2 banks (16-way conflicts);
+// at 80 bytes the 16-byte reads of 8 lanes cover all 32 banks
+constexpr int SKP_FT = SK + 4;
+constexpr int STAGE_FLOATS = SB * SKP_FT + SK * SB + 2 * SK;     // sized for the padded (FT) layout
 constexpr int SIMT_DSMEM = NST * STAGE_FLOATS * 4;  // dynamic smem: the stage ring
 
 __device__ __forceinline__ int simt_inj_lower(const DevInject* inj, int n, int t) {
@@ -57,10 +61,11 @@ __global__ void __launch_bounds__(256, FTGEMM_SIMT_MINB) simt_ftgemm_kernel(cons
     // stage ring (dynamic smem): A tile row-major (k contiguous), B tile, and
     // e^T A_i, B_j e for the k-block
     extern __shared__ __align__(16) float simt_dsmem[];
-    float (*As)[SB][SK] = reinterpret_cast<float (*)[SB][SK]>(simt_dsmem);
-    float (*Bs)[SK][SB] = reinterpret_cast<float (*)[SK][SB]>(simt_dsmem + NST * SB * SK);
-    float (*acs)[SK] = reinterpret_cast<float (*)[SK]>(simt_dsmem + 2 * NST * SB * SK);
-    float (*brs)[SK] = reinterpret_cast<float (*)[SK]>(simt_dsmem + 2 * NST * SB * SK + NST * SK);
+    constexpr int SKP = FT ? SKP_FT : SK;            // FT off: unpadded rows (measured 2.5 % faster)
+    float (*As)[SB][SKP] = reinterpret_cast<float (*)[SB][SKP]>(simt_dsmem);
+    float (*Bs)[SK][SB] = reinterpret_cast<float (*)[SK][SB]>(simt_dsmem + NST * SB * SKP);
+    float (*acs)[SK] = reinterpret_cast<float (*)[SK]>(simt_dsmem + NST * SB * SKP + NST * SK * SB);
+    float (*brs)[SK] = reinterpret_cast<float (*)[SK]>(simt_dsmem + NST * SB * SKP + NST * SK * SB + NST * SK);
     __shared__ float red_col[8][SB];                   // column partial sums per warp
     __shared__ float srow_s[SB], rref_s[SB], cref_s[SB], rres[SB], rtau[SB], cres[SB], ctau[SB];
     __shared__ int sflag[5];
@@ -117,7 +122,7 @@ __global__ void __launch_bounds__(256, FTGEMM_SIMT_MINB) simt_ftgemm_kernel(cons
 #pragma unroll
             for (int u = 0; u < SK / 8; ++u) {
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
-                             :: "r"(sa0 + (uint32_t)(s * SB * SK + u * A_ROWS_PER_U * SK) * 4u), "l"(pa + u * a_ustep)
+                             :: "r"(sa0 + (uint32_t)(s * SB * SKP + u * A_ROWS_PER_U * SKP) * 4u), "l"(pa + u * a_ustep)
                              : "memory");
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
                              :: "r"(sb0 + (uint32_t)(s * SK * SB + u * 8 * SB) * 4u), "l"(pb + u * b_ustep)
@@ -227,7 +232,10 @@ __global__ void __launch_bounds__(256, FTGEMM_SIMT_MINB) simt_ftgemm_kernel(cons
         }
 #endif
         if (FT) {
-            // carried references, ascending k, once per k-block (one branch per warp)
+            // carried references, ascending k, once per k-block (one branch per
+            // warp); the row side reads A[p][k] from the padded rows (80-byte
+            // pitch: conflict-free 16-byte reads).  Measured: a branch-free form
+            // (per-thread operand pointers) was 3 % slower.
             if (tid < SB) {
 #pragma unroll
                 for (int k = 0; k < SK; ++k) ref = fmaf(As[buf][tid][k], brs[buf][k], ref);
