@@ -721,3 +721,23 @@ def test_host_pipeline_matches_isolated_steps(dtype, beta):
     assert counts["tiles_detected"] == 0, counts
     for i, Ch in enumerate(outs):
         assert torch.equal(Ch, ref[i % 3]), i
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("cls", [(256, 2), (256, 1), (128, 1), (128, 2)], ids=lambda c: f"bn{c[0]}cg{c[1]}")
+def test_forced_tile_classes_parity(dtype, cls):
+    """Every tensor-core tile class the plan's cost model can choose (and
+    ftgemm_set_tile_class can force) gives the oracle's C, events and counts,
+    with detectable flips in several tiles, including the ragged last ones."""
+    F = ftmod()
+    M, N, K = 1000, 2016, 1024
+    with F.tile_class(*cls):
+        plan = F.plan(dtype, M, N, K)
+        assert (plan.bn, plan.cta_group) == cls
+        A, B, _ = synth.problem(M, N, K, dtype=odt(dtype))
+        inj = detectable_sites(dtype, 8, M, N, K, plan, A, B, seed=71)
+        assert len(inj) >= 5
+        c = Case(dtype, M, N, K, injections=inj, alpha=1.0, beta=0.25)
+    assert c.counts["corrected"] == len(inj), (c.counts, c.ref.counts)
+    assert c.events_match() and c.counts_match()
+    assert c.fro() < TOL[dtype]
