@@ -98,7 +98,11 @@ void fill_plan(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* p) {
         // loads; they lose on K = 128 shapes (epilogue-bound) and skinny M
         int cg = (!small && ((tiles_m125 >= 4 && (K >= 2048 || (dtype == FTGEMM_TF32 && K >= 1024))) ||
                              (skinny_m && K >= 1024))) ? 2 : 1;
-        if (!skinny_n && !skinny_m && K >= 1024) {
+        // small K is epilogue-bound: TF32 K <= 128 runs fastest on the narrow
+        // tile (one CTA per MMA), measured 7-10 % over BN = 256 (profiles/r1d_tile_classes.md)
+        if (!skinny_n && !skinny_m && dtype == FTGEMM_TF32 && K <= 128) { small = true; cg = 1; }
+        // the cost model from K = 1024 (BF16) / 512 (TF32: twice the MMA time per k)
+        if (!skinny_n && !skinny_m && K >= (dtype == FTGEMM_TF32 ? 512 : 1024)) {
             // Mainloop-bound shapes: wave-quantised cost model over the four tile
             // classes, time = ceil(units / concurrent units) x (per-wave time of
             // the class at K = 8192, measured on B200: profiles/r1d_tile_classes.md)

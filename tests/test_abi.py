@@ -97,7 +97,9 @@ def test_plan_table(F, dtype):
         k1 = F.plan(dtype, 8192, 8192, 1024)
         assert k1.bn == 256 and k1.cta_group == 2
         k128 = F.plan(dtype, 16384, 16384, 128)       # epilogue-bound: one CTA per MMA
-        assert k128.bn == 256 and k128.cta_group == 1
+        assert k128.cta_group == 1 and k128.bn == (128 if dtype == "tf32" else 256)
+        k512 = F.plan(dtype, 8192, 8192, 512)         # TF32: the cost model from K = 512
+        assert (k512.bn, k512.cta_group) == ((256, 2) if dtype == "tf32" else (256, 1))
 
 
 def test_plan_errors(F):
