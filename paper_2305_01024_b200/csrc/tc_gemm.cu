@@ -549,6 +549,69 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     float2 rs2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
                     const bool w3 = ew == 3;
                     const bool rows_only = a.ft_level == FTGEMM_FT_DETECT_ROWS;   // offline ABFT: no column sums
+                    if constexpr (CG == 1) {
+                    // (one CTA per MMA: the small-K classes, where the epilogue bounds the
+                    // kernel; measured -3 % at 16384^2 x 128.  The CTA-pair instantiation
+                    // keeps the single-buffer form below: the extra live registers spill
+                    // there and cost 0.9 % at 8192^3.)
+                    // 32-column chunks, double-buffered: the TMEM load of chunk
+                    // c+1 is in flight while chunk c is summed and transposed
+                    uint32_t rb[2][32];
+                    __syncwarp();
+                    tmem_ld32_issue(tb + lane_off, rb[0]);
+                    tmem_ld32_wait(rb[0]);
+#pragma unroll
+                    for (int c = 0; c < Cfg::NCHUNK; ++c) {
+                        uint32_t (&cur)[32] = rb[c & 1];
+                        if (c + 1 < Cfg::NCHUNK) {
+                            __syncwarp();
+                            tmem_ld32_issue(tb + lane_off + (c + 1) * 32, rb[(c + 1) & 1]);
+                        }
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            if (c * 32 + 2 * i < Cfg::BND)
+                                rs2[i & 1] = __fadd2_rn(rs2[i & 1], make_float2(__uint_as_float(cur[2 * i]),
+                                                                                __uint_as_float(cur[2 * i + 1])));
+                        if (c + 1 == Cfg::NCHUNK)
+                            rref = (__uint_as_float(cur[28]) + __uint_as_float(cur[29])) + __uint_as_float(cur[30]);
+                        if (!rows_only) {
+                            // column partial sums over this warp's 32 rows: transpose
+                            // through shared memory (row-major writes, 16-byte column
+                            // reads).  Warp 3's lanes 29..31 are the split rows of
+                            // e^T A B: they pass through the transpose unmasked and
+                            // come out as the column references.
+                            if (all_rows) {
+#pragma unroll
+                                for (int i = 0; i < 32; ++i) tbuf[i * 36 + lane] = __uint_as_float(cur[i]);
+                            } else {
+#pragma unroll
+                                for (int i = 0; i < 32; ++i)
+                                    tbuf[i * 36 + lane] = (rvalid || isref) ? __uint_as_float(cur[i]) : 0.0f;
+                            }
+                            __syncwarp();
+                            float2 s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
+#pragma unroll
+                            for (int r4 = 0; r4 < 7; ++r4) {
+                                const float4 x = *reinterpret_cast<const float4*>(tbuf + lane * 36 + 4 * r4);
+                                s01 = __fadd2_rn(s01, make_float2(x.x, x.y));
+                                s23 = __fadd2_rn(s23, make_float2(x.z, x.w));
+                            }
+                            const float4 x = *reinterpret_cast<const float4*>(tbuf + lane * 36 + 28);
+                            if (w3) {
+                                s01.x += x.x;
+                                refrow[0 * BN + c * 32 + lane] = x.y;
+                                refrow[1 * BN + c * 32 + lane] = x.z;
+                                refrow[2 * BN + c * 32 + lane] = x.w;
+                            } else {
+                                s01 = __fadd2_rn(s01, make_float2(x.x, x.y));
+                                s23 = __fadd2_rn(s23, make_float2(x.z, x.w));
+                            }
+                            colsum[ew * BN + c * 32 + lane] = (s01.x + s01.y) + (s23.x + s23.y);
+                            __syncwarp();
+                        }
+                        if (c + 1 < Cfg::NCHUNK) tmem_ld32_wait(rb[(c + 1) & 1]);
+                    }
+                    } else {
 #pragma unroll
                     for (int c2 = 0; c2 < Cfg::NCHUNK; c2 += 2) {
                         float v[64];
@@ -594,6 +657,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                             colsum[ew * BN + c * 32 + lane] = (s01.x + s01.y) + (s23.x + s23.y);
                             __syncwarp();
                         }
+                    }
                     }
                     srow = (rs2[0].x + rs2[0].y) + (rs2[1].x + rs2[1].y);
                 }
