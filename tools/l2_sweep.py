@@ -1,7 +1,9 @@
 """Schedule-group / TMA L2-hint variants of the fused kernel, interleaved call by
 call (development timing; never a bench number):
 python tools/l2_sweep.py dtype M N K ft "G:HINT" ["G:HINT" ...]
-G = FTGEMM_GROUP (0 = default), HINT = FTGEMM_L2HINT bits (A | B<<2 | C<<4)."""
+G = FTGEMM_GROUP (0 = default), HINT = FTGEMM_L2HINT bits (A | B<<2 | C<<4).
+The FTGEMM_L2HINT knob was removed from the kernel after this experiment
+(profiles/r1b_l2_schedule.md); with the current library HINT has no effect."""
 import json
 import os
 import statistics
