@@ -591,6 +591,51 @@ def test_cfg3_full_size_sampled():
         assert mine == sorted((e["row"], e["col"]) for e in ref.events)
 
 
+def test_cfg5_rank_share_sampled():
+    """cfg5 (BF16 32768 x 32768 x 16384 over 8 GPUs): one rank's share of the
+    M-block partition, run as distributed.PartitionedFTGemm runs it -- the rank's
+    4096 rows (check tiles 98..130 of the full problem, generated by global row
+    index) with the full problem's tile class -- faults in 3 tiles; whole sampled
+    tiles against the tile-local oracle."""
+    import torch
+    F = ftmod()
+    from paper_2305_01024_b200.distributed import row_partition
+    Mf, N, K, world, rank = 32768, 32768, 16384, 8, 3
+    full = F.plan("bf16", Mf, N, K)
+    tm, tn = full.check_tile_m, full.check_tile_n
+    row0, M = row_partition(Mf, world, tm)[rank]
+    seedA, seedB = synth.BASE_SEED + 11, synth.BASE_SEED + 12
+    A = synth.to_torch(synth.matrix(seedA, Mf, K, dtype="bf16", r0=row0, r1=row0 + M), "bf16").cuda()
+    B = synth.to_torch(synth.matrix(seedB, K, N, dtype="bf16"), "bf16").cuda()
+    C = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    with F.tile_class(full.bn, full.cta_group):
+        g = F.FTGemm("bf16", M, N, K)
+        plan = g.plan
+        assert (plan.bn, plan.cta_group, plan.check_tile_n) == (full.bn, full.cta_group, full.check_tile_n)
+        tiles = [(0, 0), (11, 60), (plan.tiles_m - 1, plan.tiles_n - 1), (20, 7)]
+        inj = [(ti * tm + min(3, M - ti * tm - 1), tj * tn + min(9, N - tj * tn - 1), 9000, 30, oracle.INJ_FLIP, 0, 0.0)
+               for ti, tj in tiles[:3]]                  # (the last tile column is 8 wide)
+        g.encode(A, B)
+        g.run(A, B, C, injections=inj)
+    counts, events = g.report()
+    assert counts["corrected"] == 3 and counts["tiles_detected"] == 3
+    assert counts["tiles_checked"] == plan.tiles_m * plan.tiles_n
+    for (ti, tj) in tiles:
+        r0, c0 = ti * tm, tj * tn
+        r1, c1 = min(M, r0 + tm), min(N, c0 + tn)
+        Ab = synth.matrix(seedA, Mf, K, dtype="bf16", r0=row0 + r0, r1=row0 + r1)
+        Bb = synth.matrix(seedB, K, N, dtype="bf16", c0=c0, c1=c1)
+        loc = [(r - r0, c - c0, k, b, m, tg, ad) for (r, c, k, b, m, tg, ad) in inj if r0 <= r < r1 and c0 <= c < c1]
+        ref = oracle.ftgemm(Ab, Bb, out="bf16", tile_m=tm, tile_n=tn, bk=plan.bk, u_acc=plan.u_acc,
+                            lambda1=plan.lambda1, lambda2=plan.lambda2, injections=loc)
+        assert ref.counts["corrected"] == len(loc)
+        blk = C[r0:r1, c0:c1].float().cpu().numpy().astype(np.float64)
+        assert np.linalg.norm(blk - ref.C) / np.linalg.norm(ref.C) < TOL["bf16"], (ti, tj)
+        mine = sorted((e["row"] - r0, e["col"] - c0) for e in events if e["tile_m"] == ti and e["tile_n"] == tj)
+        assert mine == sorted((e["row"], e["col"]) for e in ref.events)
+    del B, C
+
+
 def test_large_indexing_sampled():
     """C with more than 2^31 elements (65539 x 32768 BF16, 4.3 GB; ragged last
     check-tile row): 64-bit offsets in the encode, fused kernel and epilogue
