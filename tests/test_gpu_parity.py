@@ -636,6 +636,50 @@ def test_cfg5_rank_share_sampled():
     del B, C
 
 
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("shape", [(16384, 16384, 128), (128, 16384, 16384), (16384, 128, 16384)],
+                         ids=["wideC", "skinnyM", "skinnyN"])
+def test_cfg4_full_size_sampled(dtype, shape):
+    """cfg4 (BASELINE configs[3]) at full size in the plan's launch
+    configuration: faults in the first, an interior and the last check tile;
+    whole sampled tiles against the tile-local oracle."""
+    import torch
+    F = ftmod()
+    M, N, K = shape
+    plan = F.plan(dtype, M, N, K)
+    tm, tn = plan.check_tile_m, plan.check_tile_n
+    seedA, seedB = synth.BASE_SEED + 21, synth.BASE_SEED + 22
+    A = synth.to_torch(synth.matrix(seedA, M, K, dtype=odt(dtype)), odt(dtype)).cuda()
+    B = synth.to_torch(synth.matrix(seedB, K, N, dtype=odt(dtype)), odt(dtype)).cuda()
+    C = torch.empty(M, N, dtype=A.dtype, device="cuda")
+    last = (plan.tiles_m - 1, plan.tiles_n - 1)
+    tiles = [(0, 0), (plan.tiles_m // 2, plan.tiles_n // 2), last, (plan.tiles_m - 1, 0)]
+    tiles = list(dict.fromkeys(tiles))
+    inj = [(ti * tm + min(5, M - ti * tm - 1), tj * tn + min(6, N - tj * tn - 1), K // 2, 0, oracle.INJ_ADD, 0, 5000.0)
+           for ti, tj in tiles[:3]]
+    inj = list(dict.fromkeys(inj))
+    g = F.FTGemm(dtype, M, N, K)
+    g.encode(A, B)
+    g.run(A, B, C, injections=inj)
+    counts, events = g.report()
+    assert counts["corrected"] == len(inj) and counts["tiles_detected"] == len(inj), counts
+    assert counts["tiles_checked"] == plan.tiles_m * plan.tiles_n
+    for (ti, tj) in tiles:
+        r0, c0 = ti * tm, tj * tn
+        r1, c1 = min(M, r0 + tm), min(N, c0 + tn)
+        Ab = synth.matrix(seedA, M, K, dtype=odt(dtype), r0=r0, r1=r1)
+        Bb = synth.matrix(seedB, K, N, dtype=odt(dtype), c0=c0, c1=c1)
+        loc = [(r - r0, c - c0, k, b, m, tg, ad) for (r, c, k, b, m, tg, ad) in inj if r0 <= r < r1 and c0 <= c < c1]
+        ref = oracle.ftgemm(Ab, Bb, out=odt(dtype), tile_m=tm, tile_n=tn, bk=plan.bk, u_acc=plan.u_acc,
+                            lambda1=plan.lambda1, lambda2=plan.lambda2, injections=loc)
+        assert ref.counts["corrected"] == len(loc)
+        blk = C[r0:r1, c0:c1].float().cpu().numpy().astype(np.float64)
+        assert np.linalg.norm(blk - ref.C) / np.linalg.norm(ref.C) < TOL[dtype], (ti, tj)
+        mine = sorted((e["row"] - r0, e["col"] - c0) for e in events if e["tile_m"] == ti and e["tile_n"] == tj)
+        assert mine == sorted((e["row"], e["col"]) for e in ref.events)
+    del A, B, C
+
+
 def test_large_indexing_sampled():
     """C with more than 2^31 elements (65539 x 32768 BF16, 4.3 GB; ragged last
     check-tile row): 64-bit offsets in the encode, fused kernel and epilogue
