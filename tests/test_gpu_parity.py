@@ -680,6 +680,52 @@ def test_cfg4_full_size_sampled(dtype, shape):
     del A, B, C
 
 
+@pytest.mark.parametrize("dtype", ["f32_simt", "tf32"])
+def test_cfg2_full_size_sampled(dtype):
+    """cfg2 at its largest size (8192^3, FP32 operands) in the plan's launch
+    configuration, faults in 3 tiles; sampled whole tiles against the tile-local
+    oracle -- for the SIMT kernel in FP32SEQ mode, so every clean element must
+    be bit-identical (the paper's SGEMM numerics at full K)."""
+    import torch
+    F = ftmod()
+    M = N = K = 8192
+    plan = F.plan(dtype, M, N, K)
+    tm, tn = plan.check_tile_m, plan.check_tile_n
+    seedA, seedB = synth.BASE_SEED + 31, synth.BASE_SEED + 32
+    A = synth.to_torch(synth.matrix(seedA, M, K, dtype="f32"), "f32").cuda()
+    B = synth.to_torch(synth.matrix(seedB, K, N, dtype="f32"), "f32").cuda()
+    C = torch.empty(M, N, dtype=torch.float32, device="cuda")
+    tiles = [(0, 0), (plan.tiles_m // 3, plan.tiles_n // 2), (plan.tiles_m - 1, plan.tiles_n - 1), (5, plan.tiles_n - 1)]
+    inj = [(ti * tm + min(9, M - ti * tm - 1), tj * tn + min(4, N - tj * tn - 1), 5000, 0, oracle.INJ_ADD, 0, 700.0)
+           for ti, tj in tiles[:3]]
+    g = F.FTGemm(dtype, M, N, K)
+    g.encode(A, B)
+    g.run(A, B, C, injections=inj)
+    counts, events = g.report()
+    assert counts["corrected"] == 3 and counts["tiles_detected"] == 3, counts
+    acc = "fp32seq" if dtype == "f32_simt" else "fp64"
+    for (ti, tj) in tiles:
+        r0, c0 = ti * tm, tj * tn
+        r1, c1 = min(M, r0 + tm), min(N, c0 + tn)
+        Ab = synth.matrix(seedA, M, K, dtype="f32", r0=r0, r1=r1)
+        Bb = synth.matrix(seedB, K, N, dtype="f32", c0=c0, c1=c1)
+        loc = [(r - r0, c - c0, k, b, m, tg, ad) for (r, c, k, b, m, tg, ad) in inj if r0 <= r < r1 and c0 <= c < c1]
+        ref = oracle.ftgemm(Ab, Bb, out="f32", acc=acc, tile_m=tm, tile_n=tn, bk=plan.bk, u_acc=plan.u_acc,
+                            lambda1=plan.lambda1, lambda2=plan.lambda2, injections=loc)
+        assert ref.counts["corrected"] == len(loc)
+        blk = C[r0:r1, c0:c1].cpu().numpy()
+        if dtype == "f32_simt":
+            clean = np.ones(blk.shape, dtype=bool)
+            for (r, c, *_) in loc:
+                clean[r, c] = False                       # the corrected element: row-sum rounding
+            assert np.array_equal(blk[clean], ref.C[clean].astype(np.float32)), (ti, tj)
+        rel = np.linalg.norm(blk.astype(np.float64) - ref.C) / np.linalg.norm(ref.C)
+        assert rel < (2 * 2 ** -24 * math.sqrt(K) if dtype == "f32_simt" else TOL[dtype]), (ti, tj, rel)
+        mine = sorted((e["row"] - r0, e["col"] - c0) for e in events if e["tile_m"] == ti and e["tile_n"] == tj)
+        assert mine == sorted((e["row"], e["col"]) for e in ref.events)
+    del A, B, C
+
+
 def test_large_indexing_sampled():
     """C with more than 2^31 elements (65539 x 32768 BF16, 4.3 GB; ragged last
     check-tile row): 64-bit offsets in the encode, fused kernel and epilogue
