@@ -25,7 +25,7 @@
 namespace ftg {
 
 #ifndef FTGEMM_SIMT_SK
-#define FTGEMM_SIMT_SK 16
+#define FTGEMM_SIMT_SK 32
 #endif
 constexpr int SB = 128, SK = FTGEMM_SIMT_SK;       // tile, k-block (plan.bk)
 constexpr int NST = SK == 8 ? 4 : 3;                // smem pipeline stages

@@ -72,7 +72,7 @@ def test_struct_layouts(F, tmp_path):
 def test_plan_table(F, dtype):
     p = F.plan(dtype, 8192, 8192, 8192)
     if dtype == "f32_simt":
-        assert (p.bm, p.bn, p.bk, p.check_tile_m, p.check_tile_n) == (128, 128, 16, 128, 128)
+        assert (p.bm, p.bn, p.bk, p.check_tile_m, p.check_tile_n) == (128, 128, 32, 128, 128)
         assert p.u_acc == 2.0 ** -24
     else:
         assert (p.bm, p.bn) == (128, 256) and p.check_tile_m == 125 and p.check_tile_n == 252
