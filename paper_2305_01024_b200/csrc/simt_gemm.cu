@@ -28,7 +28,10 @@ namespace ftg {
 #define FTGEMM_SIMT_SK 32
 #endif
 constexpr int SB = 128, SK = FTGEMM_SIMT_SK;       // tile, k-block (plan.bk)
-constexpr int NST = SK == 8 ? 4 : 3;                // smem pipeline stages
+#ifndef FTGEMM_SIMT_NST
+#define FTGEMM_SIMT_NST (SK == 8 ? 4 : 3)
+#endif
+constexpr int NST = FTGEMM_SIMT_NST;                // smem pipeline stages
 // A tile rows padded by 4 floats: the row-reference FMAs read A[p][k] with one
 // thread per row, which at a 64-byte row pitch hit 2 banks (16-way conflicts);
 // at 80 bytes the 16-byte reads of 8 lanes cover all 32 banks
