@@ -60,6 +60,20 @@ extern "C" {
 #define FTGEMM_TF32     1   /* FP32 in/out, tcgen05.mma kind::tf32, FP32 accumulate in TMEM */
 #define FTGEMM_BF16     2   /* BF16 in/out, tcgen05.mma kind::f16 (bf16), FP32 accumulate in TMEM */
 
+/* Every `dtype` argument below is a dtype CODE: one of the precision variants
+ * above, optionally OR-ed with an explicit tensor-core tile class
+ *     FTGEMM_TF32 | FTGEMM_TILE(bn, cta_group),  bn in {128, 256}, cta_group in {1, 2}
+ * (check tile 125 x (bn - 4); cta_group 2 = a CTA pair issues one M = 256 MMA).
+ * Without a class the plan chooses one from the shape (north_star item 4).  The
+ * class travels with every call -- there is no process-wide tile-class state --
+ * so ftgemm_encode and ftgemm_run given the same code, M, N, K always derive the
+ * same encode layout; plan.dtype returns the fully explicit code of a plan
+ * (pass it to encode / run to reproduce exactly that plan, e.g. on every rank
+ * of an M-block partition: SURVEY.md 8(e)).  A class on F32_SIMT, an unknown
+ * class or other set bits: FTGEMM_ERR_INVALID_VALUE.                          */
+#define FTGEMM_TILE(bn, cta_group) ((((bn) / 128) << 8) | ((cta_group) << 12))
+#define FTGEMM_DTYPE_MASK 0xff
+
 /* ---- fault-tolerance level -------------------------------------------------- */
 #define FTGEMM_FT_OFF     0  /* same tile shape family, checksums compiled out (the overhead baseline) */
 #define FTGEMM_FT_DETECT  1  /* verify + locate, report, leave C as computed (detect-only flavour) */
@@ -209,7 +223,8 @@ typedef struct ftgemm_counts {
  * kernel serves (dtype, M, N, K), the check-tile geometry the verification
  * works on, and the workspace sizes.  Pure host function, no device access.  */
 typedef struct ftgemm_plan {
-    int32_t dtype;
+    int32_t dtype;               /* the fully explicit dtype code of this plan (tensor-core
+                                    dtypes: | FTGEMM_TILE(bn, cta_group)) */
     int32_t shape_class;         /* FTGEMM_SHAPE_* */
     int32_t bm, bn, bk;          /* MMA / CTA tile */
     int32_t check_tile_m;        /* data rows per check tile (FT on)    */
@@ -217,8 +232,7 @@ typedef struct ftgemm_plan {
     int32_t off_tile_m, off_tile_n; /* data tile with FT_OFF */
     int32_t stages;              /* smem pipeline depth */
     int32_t cta_group;           /* 1, or 2: a CTA pair issues one M = 256 tcgen05.mma (cta_group::2);
-                                    each CTA still owns one 128-row (125 + 3) check tile.  The
-                                    environment variable FTGEMM_CG=1|2 overrides (tuning/tests) */
+                                    each CTA still owns one 128-row (125 + 3) check tile */
     int32_t max_events, max_inject;
     int32_t pad0;
     int64_t tiles_m, tiles_n;    /* check-tile grid with FT on */
@@ -233,18 +247,8 @@ typedef struct ftgemm_plan {
 #define FTGEMM_SHAPE_SQUARE      0  /* 128 x 256 tcgen05 tile (128 x 128 SIMT) */
 #define FTGEMM_SHAPE_SMALL_N     1  /* 128 x 128 tcgen05 tile: narrow N or too few tiles for 148 SMs */
 
-/* Fill *out for a problem.  Errors: INVALID_VALUE (dims < 1, bad dtype, null out). */
+/* Fill *out for a problem.  Errors: INVALID_VALUE (dims < 1, bad dtype code, null out). */
 FTGEMM_API int ftgemm_plan(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* out);
-
-/* Force the tile class of the tensor-core paths (TF32, BF16) for every later
- * ftgemm_plan / ftgemm_encode / ftgemm_run* call in this process: bn in
- * {128, 256} (check tile 125 x (bn - 4)), cta_group in {1, 2}; (0, 0) restores
- * the plan's own choice (wave-quantised cost model, skinny-shape rules, which
- * are never overridden).  Used by M-block partitions so that every rank runs the
- * full problem's check tiles (concatenated C and event positions
- * identical to the one-GPU run).  Process-wide; not synchronised with calls in
- * flight on other host threads.  Errors: INVALID_VALUE.                        */
-FTGEMM_API int ftgemm_set_tile_class(int bn, int cta_group);
 
 /* ---- encode (Eq. 1 / Eq. 2) -------------------------
  * which = 1: encode A  ->  per check-tile i: Ac_i[k] = sum_{p in tile rows} A[p,k]

@@ -67,12 +67,26 @@ int fail_cuda(cudaError_t e, const char* where) {
 
 bool valid_dtype(int d) { return d == FTGEMM_F32_SIMT || d == FTGEMM_TF32 || d == FTGEMM_BF16; }
 
-// forced tile class of the tensor-core paths (0 = the plan's own choice)
-std::atomic<int> g_force_bn{0}, g_force_cg{0};
+// A dtype code is the precision variant (low byte) optionally OR-ed with an
+// explicit tensor-core tile class FTGEMM_TILE(bn, cta_group) (include/ftgemm.h).
+// The class is part of every call's arguments -- there is no ambient state --
+// so an encode and a run given the same code always derive the same layout.
+struct Code { int dtype, bn, cg; };
+bool parse_code(int code, Code* c) {
+    c->dtype = code & FTGEMM_DTYPE_MASK;
+    const int tb = (code >> 8) & 0xf, tcg = (code >> 12) & 0xf;
+    if (!valid_dtype(c->dtype) || (code & ~0xffff) != 0 || tb > 2 || tcg > 2 || (tb == 0) != (tcg == 0)) return false;
+    if (c->dtype == FTGEMM_F32_SIMT && tb) return false;       // the SIMT kernel has one tile class
+    c->bn = tb * 128; c->cg = tcg;
+    return true;
+}
 
 // The shape-class table (north_star item 4): compile-time instantiations
-// chosen per problem shape.
-void fill_plan(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* p) {
+// chosen per problem shape.  `code` must have passed parse_code.
+void fill_plan(int code, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* p) {
+    Code cc;
+    parse_code(code, &cc);
+    const int dtype = cc.dtype;
     std::memset(p, 0, sizeof(*p));
     p->dtype = dtype;
     p->max_events = kMaxEvents;
@@ -118,16 +132,14 @@ void fill_plan(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* p) {
             }
         }
         int bn = small ? 128 : 256;
-        // explicit class (ftgemm_set_tile_class: multi-GPU ranks use the full
-        // problem's class), then the tuning environment overrides
-        const int fbn = g_force_bn.load(std::memory_order_relaxed), fcg = g_force_cg.load(std::memory_order_relaxed);
-        if (fbn && !skinny_n && !skinny_m) { bn = fbn; cg = fcg; }
-        if (const char* e = getenv("FTGEMM_BN")) bn = atoi(e) == 128 ? 128 : 256;
+        // an explicit class in the code wins over every rule above (multi-GPU
+        // ranks pass the full problem's class, tests force each class)
+        if (cc.bn) { bn = cc.bn; cg = cc.cg; }
+        p->dtype = dtype | FTGEMM_TILE(bn, cg);      // the fully explicit code of this plan
         p->shape_class = bn == 128 ? FTGEMM_SHAPE_SMALL_N : FTGEMM_SHAPE_SQUARE;
         p->bm = 128; p->bn = bn; p->bk = bk;
         p->check_tile_m = 125; p->check_tile_n = bn - 4;
         p->off_tile_m = 128; p->off_tile_n = bn;
-        if (const char* e = getenv("FTGEMM_CG")) cg = atoi(e) == 2 ? 2 : 1;
         p->cta_group = cg;
         const int elt = dtype == FTGEMM_TF32 ? 4 : 2;
         const int stage = 128 * 128 + (bn / cg) * bk * elt;
@@ -140,41 +152,39 @@ void fill_plan(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* p) {
 
 Geometry geometry(const ftgemm_plan_t& p, int64_t K) {
     Geometry g{};
-    g.dtype = p.dtype;
+    g.dtype = p.dtype & FTGEMM_DTYPE_MASK;
     g.bm = p.bm; g.bn = p.bn; g.bk = p.bk;
     g.bmd = p.check_tile_m; g.bnd = p.check_tile_n;
     g.tiles_m = (int)p.tiles_m; g.tiles_n = (int)p.tiles_n;
     g.kp = (int)(((K + p.bk - 1) / p.bk) * p.bk);
     g.nkb = g.kp / p.bk;
-    g.elt = p.dtype == FTGEMM_BF16 ? 2 : 4;
+    g.elt = g.dtype == FTGEMM_BF16 ? 2 : 4;
     g.tc = p.dtype != FTGEMM_F32_SIMT;
     g.nkc_a = (g.kp + 512 / g.elt - 1) / (512 / g.elt);   // encode-A k chunks (512-byte rows)
     // encode B: 256 k-rows per block (measured best or equal against 64 / 128
     // for every profiled shape, profiles/r1_encode.md)
     g.enc_b_rows = kEncBRows;
-    {
-        if (const char* e = getenv("FTGEMM_ENC_B_ROWS")) {       // tuning override (32 .. 1024)
-            const int r = atoi(e);
-            if (r >= 32 && r <= 1024 && r % 32 == 0) g.enc_b_rows = r;
-        }
-    }
     g.nkc_b = (g.kp + g.enc_b_rows - 1) / g.enc_b_rows;
     return g;
 }
 
+// 1 if the CURRENT device is an sm_100 part (cached per device ordinal)
 int check_device() {
-    static int cached = -1;
     static std::mutex mu;
+    static signed char cached[kMaxDevices];
+    static bool init = false;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) { cudaGetLastError(); return 0; }
     std::lock_guard<std::mutex> lk(mu);
-    if (cached >= 0) return cached;
-    int dev = 0, major = 0, minor = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+    if (!init) { std::memset(cached, -1, sizeof(cached)); init = true; }
+    if (cached[dev] >= 0) return cached[dev];
+    int major = 0, minor = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
         cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess) {
         cudaGetLastError();
-        return cached = 0;
+        return 0;
     }
-    return cached = (major == 10 && minor == 0) ? 1 : 0;
+    return cached[dev] = (major == 10 && minor == 0) ? 1 : 0;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -227,8 +237,10 @@ int make_map_3d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-int check_dims(int dtype, int64_t M, int64_t N, int64_t K) {
-    if (!valid_dtype(dtype)) return fail(FTGEMM_ERR_INVALID_VALUE, "unknown dtype %d", dtype);
+int check_dims(int code, int64_t M, int64_t N, int64_t K) {
+    Code cc;
+    if (!parse_code(code, &cc))
+        return fail(FTGEMM_ERR_INVALID_VALUE, "bad dtype code 0x%x (dtype | FTGEMM_TILE(128|256, 1|2), tensor-core dtypes only)", code);
     if (M < 1 || N < 1 || K < 1) return fail(FTGEMM_ERR_INVALID_VALUE, "dims must be >= 1 (M=%lld N=%lld K=%lld)",
                                              (long long)M, (long long)N, (long long)K);
     if (M >= (1ll << 31) || N >= (1ll << 31) || K >= (1ll << 31))
@@ -239,7 +251,7 @@ int check_dims(int dtype, int64_t M, int64_t N, int64_t K) {
 // schedule key of a check tile (the order the kernel walks work units in; a
 // unit is cta_group check tiles stacked in M, one per CTA of the pair)
 int tile_key(const ftgemm_plan_t& p, int ti, int tj) {
-    if (p.dtype == FTGEMM_F32_SIMT) return ti * (int)p.tiles_n + tj;
+    if ((p.dtype & FTGEMM_DTYPE_MASK) == FTGEMM_F32_SIMT) return ti * (int)p.tiles_n + tj;
     const int cg = p.cta_group;
     const int units_m = ((int)p.tiles_m + cg - 1) / cg, tu = ti / cg;
     const int G = tc_group(units_m, cg);
@@ -254,27 +266,14 @@ extern "C" {
 
 int ftgemm_version(void) { return FTGEMM_ABI_VERSION; }
 
-int ftgemm_set_tile_class(int bn, int cta_group) {
-    if (bn == 0 && cta_group == 0) {
-        g_force_bn.store(0); g_force_cg.store(0);
-        g_err.clear();
-        return FTGEMM_OK;
-    }
-    if ((bn != 128 && bn != 256) || (cta_group != 1 && cta_group != 2))
-        return fail(FTGEMM_ERR_INVALID_VALUE, "tile class must be bn in {128, 256}, cta_group in {1, 2} (or 0, 0)");
-    g_force_cg.store(cta_group);
-    g_force_bn.store(bn);
-    g_err.clear();
-    return FTGEMM_OK;
-}
 int ftgemm_device_arch(void) { return 1000; }
 const char* ftgemm_last_error(void) { return g_err.c_str(); }
 
-int ftgemm_plan(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* out) {
+int ftgemm_plan(int code, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* out) {
     if (!out) return fail(FTGEMM_ERR_INVALID_VALUE, "null plan pointer");
-    int e = check_dims(dtype, M, N, K);
+    int e = check_dims(code, M, N, K);
     if (e) return e;
-    fill_plan(dtype, M, N, K, out);
+    fill_plan(code, M, N, K, out);
     const Geometry g = geometry(*out, K);
     const EncLayout L = enc_layout(g, M, N);
     out->enc_bytes = (int64_t)L.total;
@@ -285,12 +284,12 @@ int ftgemm_plan(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* out) 
     return FTGEMM_OK;
 }
 
-int ftgemm_encode_layout(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_enc_layout_t* out) {
+int ftgemm_encode_layout(int code, int64_t M, int64_t N, int64_t K, ftgemm_enc_layout_t* out) {
     if (!out) return fail(FTGEMM_ERR_INVALID_VALUE, "null layout pointer");
-    int e = check_dims(dtype, M, N, K);
+    int e = check_dims(code, M, N, K);
     if (e) return e;
     ftgemm_plan_t p;
-    fill_plan(dtype, M, N, K, &p);
+    fill_plan(code, M, N, K, &p);
     const Geometry g = geometry(p, K);
     const EncLayout L = enc_layout(g, M, N);
     out->ac = (int64_t)L.ac; out->br = (int64_t)L.br; out->bt = g.tc ? (int64_t)L.bt : -1;
@@ -302,10 +301,11 @@ int ftgemm_encode_layout(int dtype, int64_t M, int64_t N, int64_t K, ftgemm_enc_
     return FTGEMM_OK;
 }
 
-int ftgemm_encode(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B,
+int ftgemm_encode(int code, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B,
                   int64_t ldb, void* enc_ws, int which, void* stream) {
-    int e = check_dims(dtype, M, N, K);
+    int e = check_dims(code, M, N, K);
     if (e) return e;
+    const int dtype = code & FTGEMM_DTYPE_MASK;
     if ((which & 3) == 0 || which > 7) return fail(FTGEMM_ERR_INVALID_VALUE, "which must be 1, 2 or 3 (| 4)");
     if (!enc_ws) return fail(FTGEMM_ERR_INVALID_VALUE, "null enc_ws");
     if ((which & 1) && (!A || lda < K)) return fail(FTGEMM_ERR_INVALID_VALUE, "bad A / lda");
@@ -316,7 +316,7 @@ int ftgemm_encode(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int
     if ((reinterpret_cast<uintptr_t>(enc_ws) & 255) != 0) return fail(FTGEMM_ERR_INVALID_VALUE, "enc_ws must be 256-byte aligned");
     if (!check_device()) return fail(FTGEMM_ERR_UNSUPPORTED, "no sm_100 (B200) device");
     ftgemm_plan_t p;
-    fill_plan(dtype, M, N, K, &p);
+    fill_plan(code, M, N, K, &p);
     const Geometry g = geometry(p, K);
     const EncLayout L = enc_layout(g, M, N);
     cudaError_t ce = launch_encode(g, L, M, N, K, A, lda, B, ldb, enc_ws, which, (cudaStream_t)stream);
@@ -325,11 +325,12 @@ int ftgemm_encode(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int
     return FTGEMM_OK;
 }
 
-static int run_impl(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const void* A, int64_t lda,
+static int run_impl(int code, int64_t M, int64_t N, int64_t K, float alpha, const void* A, int64_t lda,
                     const void* B, int64_t ldb, float beta, void* C, int64_t ldc, const void* enc_ws, int ft_level,
                     int64_t ks, int fuse_a, const ftgemm_inject_t* inj, int32_t n_inj, void* report_ws, void* stream) {
-    int e = check_dims(dtype, M, N, K);
+    int e = check_dims(code, M, N, K);
     if (e) return e;
+    const int dtype = code & FTGEMM_DTYPE_MASK;
     if (ks < 0) return fail(FTGEMM_ERR_INVALID_VALUE, "ks must be >= 0");
     if (ks > 0 && dtype == FTGEMM_F32_SIMT) return fail(FTGEMM_ERR_UNSUPPORTED, "online-interval mode: tensor-core dtypes");
     if (ks > 0 && (ft_level == FTGEMM_FT_OFF || ft_level == FTGEMM_FT_DETECT_ROWS))
@@ -349,7 +350,7 @@ static int run_impl(int dtype, int64_t M, int64_t N, int64_t K, float alpha, con
     if (!check_device()) return fail(FTGEMM_ERR_UNSUPPORTED, "no sm_100 (B200) device");
 
     ftgemm_plan_t p;
-    fill_plan(dtype, M, N, K, &p);
+    fill_plan(code, M, N, K, &p);
     if (ks > 0 && ks % p.bk) return fail(FTGEMM_ERR_INVALID_VALUE, "ks must be a multiple of plan.bk (%d)", p.bk);
     // in-kernel encode: one CTA per MMA (a CTA pair would put a cluster-scope
     // release of the peer's split rows on every k-block's critical path)
@@ -431,7 +432,7 @@ static int run_impl(int dtype, int64_t M, int64_t N, int64_t K, float alpha, con
         // 2-D box per slice
         const CUtensorMapSwizzle bsw = tf32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
         const uint32_t nbox_cta = (uint32_t)(p.bn / boxn / p.cta_group);
-        bool b3d = !(getenv("FTGEMM_B3D") && atoi(getenv("FTGEMM_B3D")) == 0);
+        bool b3d = FTGEMM_B3D != 0;
 #if defined(FTGEMM_EXP_B_DIRECT)
         if (false) {
 #else
@@ -507,24 +508,26 @@ int ftgemm_run_online(int dtype, int64_t M, int64_t N, int64_t K, float alpha, c
                     stream);
 }
 
-int ftgemm_nonfused_workspace(int dtype, int64_t M, int64_t N, int64_t K, int64_t* bytes) {
-    int e = check_dims(dtype, M, N, K);
+int ftgemm_nonfused_workspace(int code, int64_t M, int64_t N, int64_t K, int64_t* bytes) {
+    int e = check_dims(code, M, N, K);
     if (e) return e;
+    const int dtype = code & FTGEMM_DTYPE_MASK;
     if (!bytes) return fail(FTGEMM_ERR_INVALID_VALUE, "null bytes");
     if (dtype == FTGEMM_TF32) return fail(FTGEMM_ERR_UNSUPPORTED, "non-fused baseline: BF16 and F32_SIMT only");
     ftgemm_plan_t p;
-    fill_plan(dtype, M, N, K, &p);
+    fill_plan(code, M, N, K, &p);
     *bytes = (int64_t)nonfused_ws_bytes(geometry(p, K), M, N);
     g_err.clear();
     return FTGEMM_OK;
 }
 
-int ftgemm_run_nonfused(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const void* A, int64_t lda,
+int ftgemm_run_nonfused(int code, int64_t M, int64_t N, int64_t K, float alpha, const void* A, int64_t lda,
                         const void* B, int64_t ldb, float beta, void* C, int64_t ldc, const void* enc_ws,
                         void* nf_ws, int ft_level, const ftgemm_inject_t* inj, int32_t n_inj, void* report_ws,
                         void* stream) {
-    int e = check_dims(dtype, M, N, K);
+    int e = check_dims(code, M, N, K);
     if (e) return e;
+    const int dtype = code & FTGEMM_DTYPE_MASK;
     if (dtype == FTGEMM_TF32) return fail(FTGEMM_ERR_UNSUPPORTED, "non-fused baseline: BF16 and F32_SIMT only");
     if (!A || !B || !C) return fail(FTGEMM_ERR_INVALID_VALUE, "null A, B or C");
     if (lda < K || ldb < N || ldc < N) return fail(FTGEMM_ERR_INVALID_VALUE, "leading dimension too small");
@@ -539,7 +542,7 @@ int ftgemm_run_nonfused(int dtype, int64_t M, int64_t N, int64_t K, float alpha,
         return fail(FTGEMM_ERR_UNSUPPORTED, "A, B, C must be 16-byte aligned with 16-byte row pitches");
     if (!check_device()) return fail(FTGEMM_ERR_UNSUPPORTED, "no sm_100 (B200) device");
     ftgemm_plan_t p;
-    fill_plan(dtype, M, N, K, &p);
+    fill_plan(code, M, N, K, &p);
     const Geometry g = geometry(p, K);
     const EncLayout L = enc_layout(g, M, N);
     cudaStream_t st = (cudaStream_t)stream;
@@ -580,7 +583,7 @@ int ftgemm_run_offline(int dtype, int64_t M, int64_t N, int64_t K, float alpha, 
         for (int i = 0; i < n_inj; ++i)
             if (inj_run[i] < 0 || inj_run[i] >= max_runs) return fail(FTGEMM_ERR_INVALID_VALUE, "inj_run[%d] out of range", i);
     cudaStream_t st = (cudaStream_t)stream;
-    const int elt = dtype == FTGEMM_BF16 ? 2 : 4;
+    const int elt = (dtype & FTGEMM_DTYPE_MASK) == FTGEMM_BF16 ? 2 : 4;
     const size_t pitch = (size_t)ldc * elt, width = (size_t)N * elt;
     cudaError_t ce;
     if (beta != 0.0f && (ce = cudaMemcpy2DAsync(c_backup, pitch, C, pitch, width, (size_t)M, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)

@@ -5,6 +5,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdlib>
+#include <mutex>
 
 #include "../../include/ftgemm.h"
 
@@ -14,6 +15,16 @@ constexpr int kNumSMsB200 = 148;
 constexpr int kMaxEvents = 4096;
 constexpr int kMaxInject = 65536;
 constexpr int kEncBRows = 256;     // k-rows of B per encode-B block
+constexpr int kMaxDevices = 64;    // per-device one-time state (kernel attributes, device checks)
+
+// Development / tuning knobs are compile-time only (-D...): the product path
+// reads no environment variables.
+#ifndef FTGEMM_B3D
+#define FTGEMM_B3D 1               // B tile in one 3-D TMA request per stage
+#endif
+#ifndef FTGEMM_GROUP
+#define FTGEMM_GROUP 16            // M-tiles per schedule group of the tensor-core kernel
+#endif
 
 // ---- report workspace (device) --------------------------------------------
 struct DevInject {        // one fault, resolved to (check tile, k-block, in-tile position)
@@ -67,11 +78,10 @@ struct SimtArgs {
     const DevInject* inj; int n_inj;
 };
 
-// M-tiles per schedule group of the tensor-core kernel: about 16, split evenly
-// so that no group is ragged (FTGEMM_GROUP overrides, for tuning)
+// M-tiles per schedule group of the tensor-core kernel: about FTGEMM_GROUP,
+// split evenly so that no group is ragged
 inline int tc_group(int units_m, int cg) {
-    int g0 = 16 / cg;
-    if (const char* e = getenv("FTGEMM_GROUP")) g0 = atoi(e) > 0 ? atoi(e) : g0;
+    const int g0 = FTGEMM_GROUP / cg > 0 ? FTGEMM_GROUP / cg : 1;
     const int ng = units_m / g0 > 0 ? (units_m + g0 / 2) / g0 : 1;
     return (units_m + ng - 1) / ng;
 }
@@ -130,6 +140,40 @@ inline EncLayout enc_layout(const Geometry& g, int64_t M, int64_t N) {
     L.b_bytes = o - L.b_off;
     L.total = o;
     return L;
+}
+
+// cudaFuncSetAttribute is a per-device setting: apply it once per (kernel,
+// device), thread-safely.  One instance per kernel (a function-local static).
+struct PerDeviceOnce {
+    std::mutex mu;
+    bool done[kMaxDevices] = {};
+    template <class Fn>
+    cudaError_t run(Fn fn) {
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return e;
+        if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+        std::lock_guard<std::mutex> lk(mu);
+        if (done[dev]) return cudaSuccess;
+        e = fn();
+        if (e == cudaSuccess) done[dev] = true;
+        return e;
+    }
+};
+
+// SMs of the current device (cached per device); the launch grids use it, the
+// plan's pure-host cost model assumes a full B200 (kNumSMsB200)
+inline int device_sms() {
+    static std::mutex mu;
+    static int sms[kMaxDevices] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return kNumSMsB200;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!sms[dev] && cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+        cudaGetLastError();
+        sms[dev] = kNumSMsB200;
+    }
+    return sms[dev];
 }
 
 // ---- operand conversions ---------------------------------------------------

@@ -297,7 +297,7 @@ cudaError_t launch_nonfused(const Geometry& g, const EncLayout& E, int64_t M, in
     if (bf) {
         uint16_t* Xs = reinterpret_cast<uint16_t*>(ws + L.xs);
         uint16_t* Ys = reinterpret_cast<uint16_t*>(ws + L.ys);
-        nf_split_kernel<<<2 * kNumSMsB200, 256, 0, st>>>(Ac, Br, tm, tn, g.kp, Ys, Xs);
+        nf_split_kernel<<<2 * device_sms(), 256, 0, st>>>(Ac, Br, tm, tn, g.kp, Ys, Xs);
         X = Xs; Y = Ys;
     }
     s = gemm_rm(h, true, M, (int64_t)S * tn, K, A, lda, X, g.kp, rrow, (int64_t)S * tn, tin, CUDA_R_32F, 0.0f);

@@ -442,14 +442,14 @@ __global__ void __launch_bounds__(256, FTGEMM_SIMT_MINB) simt_ftgemm_kernel(cons
 }
 
 cudaError_t launch_simt(bool ft, const SimtArgs& a, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(simt_ftgemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SIMT_DSMEM);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(simt_ftgemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SIMT_DSMEM);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static PerDeviceOnce attr;
+    cudaError_t e = attr.run([] {
+        cudaError_t r = cudaFuncSetAttribute(simt_ftgemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SIMT_DSMEM);
+        if (r == cudaSuccess)
+            r = cudaFuncSetAttribute(simt_ftgemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SIMT_DSMEM);
+        return r;
+    });
+    if (e != cudaSuccess) return e;
     const int grid = a.tiles_m * a.tiles_n;
     if (ft) simt_ftgemm_kernel<true><<<grid, 256, SIMT_DSMEM, st>>>(a);
     else simt_ftgemm_kernel<false><<<grid, 256, SIMT_DSMEM, st>>>(a);

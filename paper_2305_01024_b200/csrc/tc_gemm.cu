@@ -1010,14 +1010,14 @@ cudaError_t launch_tc_t(const CUtensorMap& mA, const CUtensorMap& mB, const CUte
                         const CUtensorMap& mY, const TcArgs& a, cudaStream_t st) {
     using Cfg = TcCfg<kTF32, BN, FT, CG>;
     auto kern = tc_ftgemm_kernel<kTF32, BN, FT, CG>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    static PerDeviceOnce smem_attr;
+    cudaError_t e = smem_attr.run([&] {
+        return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    });
+    if (e != cudaSuccess) return e;
     // persistent: one CTA (pair) per SM (pair of SMs)
-    const int clusters = a.num_units < kNumSMsB200 / CG ? a.num_units : kNumSMsB200 / CG;
+    const int slots = device_sms() / CG;
+    const int clusters = a.num_units < slots ? a.num_units : slots;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(clusters * CG, 1, 1);
     cfg.blockDim = dim3(Cfg::THREADS, 1, 1);

@@ -14,8 +14,6 @@ tests) with backend "nccl" on GPUs or "gloo" for the host-logic tests.
 """
 from __future__ import annotations
 
-import contextlib
-
 import torch
 import torch.distributed as dist
 
@@ -101,11 +99,10 @@ class PartitionedFTGemm:
         self.tile_row0 = self.row0 // full.check_tile_m
         self.M, self.N, self.K = M, N, K
         # every rank runs the full problem's tile class (its own, smaller M could
-        # make the plan's wave model pick another check-tile width)
-        self._cls = (full.bn, full.cta_group) if dtype not in ("f32_simt", F.F32_SIMT) else None
-        with self._tile_class():
-            self.g = F.FTGemm(dtype, max(self.rows, 1), N, K,
-                              device=device or torch.device("cuda", torch.cuda.current_device()))
+        # make the plan's wave model pick another check-tile width): full.dtype is
+        # the full plan's explicit dtype code (dtype | FTGEMM_TILE(bn, cta_group))
+        self.g = F.FTGemm(full.dtype, max(self.rows, 1), N, K,
+                          device=device or torch.device("cuda", torch.cuda.current_device()))
         # the B part of the workspace is only shareable when every rank has the same geometry
         sig = torch.tensor([self.g.plan.bn, self.g.plan.tiles_n, self.g.plan.enc_b_bytes], dtype=torch.int64,
                            device=self.g.enc_ws.device)
@@ -116,26 +113,20 @@ class PartitionedFTGemm:
         dist.all_reduce(agree, op=dist.ReduceOp.MIN, group=group)
         self.share_b = bool(agree.item())
 
-    def _tile_class(self):
-        from . import ftgemm as F
-        return F.tile_class(*self._cls) if self._cls else contextlib.nullcontext()
-
     def set_b(self, B: torch.Tensor, src: int = 0) -> float:
         """Broadcast B once (and its encode when all ranks share the geometry)."""
-        with self._tile_class():
-            if self.share_b:
-                return broadcast_b(self.g, B, src, self.group)
-            dist.broadcast(B, src, group=self.group)
-            self.g.encode(None, B, which=2)
-            return 0.0
+        if self.share_b:
+            return broadcast_b(self.g, B, src, self.group)
+        dist.broadcast(B, src, group=self.group)
+        self.g.encode(None, B, which=2)
+        return 0.0
 
     def run(self, A_local, B, C_local, **kw):
         if self.rows == 0:
             return
-        with self._tile_class():
-            if kw.get("ft_level", 2) != 0:
-                self.g.encode(A_local, None, which=1)
-            self.g.run(A_local, B, C_local, **kw)
+        if kw.get("ft_level", 2) != 0:
+            self.g.encode(A_local, None, which=1)
+        self.g.run(A_local, B, C_local, **kw)
 
     def report(self):
         counts, events = self.g.report()

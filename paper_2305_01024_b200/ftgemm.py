@@ -65,8 +65,14 @@ class Cost(C.Structure):
 
 SYMBOLS = ("ftgemm_plan", "ftgemm_encode", "ftgemm_encode_layout", "ftgemm_run", "ftgemm_run_fused", "ftgemm_run_online", "ftgemm_run_offline", "ftgemm_cost_model",
            "ftgemm_nonfused_workspace", "ftgemm_run_nonfused",
-           "ftgemm_report", "ftgemm_report_reset", "ftgemm_last_error", "ftgemm_version", "ftgemm_device_arch",
-           "ftgemm_set_tile_class")
+           "ftgemm_report", "ftgemm_report_reset", "ftgemm_last_error", "ftgemm_version", "ftgemm_device_arch")
+DTYPE_MASK = 0xFF
+
+
+def tile_code(dtype, bn: int, cta_group: int) -> int:
+    """dtype code with an explicit tensor-core tile class (FTGEMM_TILE in include/ftgemm.h)."""
+    tb = bn // 128 if bn in (128, 256) else 0xF           # anything else: rejected by the library
+    return _dt(dtype) | (tb << 8) | ((cta_group & 0xF) << 12)
 
 _lib = None
 
@@ -100,8 +106,6 @@ def lib():
         for n in SYMBOLS:
             if n != "ftgemm_last_error" and hasattr(L, n):
                 getattr(L, n).restype = C.c_int
-        if hasattr(L, "ftgemm_set_tile_class"):          # absent from development builds of older sources
-            L.ftgemm_set_tile_class.argtypes = [C.c_int, C.c_int]
         _lib = L
     return _lib
 
@@ -120,6 +124,34 @@ def _check(code: int, where: str):
 
 def _dt(dtype) -> int:
     return DTYPES[dtype] if isinstance(dtype, str) else int(dtype)
+
+
+_TORCH_DT = {F32_SIMT: torch.float32, TF32: torch.float32, BF16: torch.bfloat16}
+
+
+def _operand(name: str, t: torch.Tensor, dtype, rows: int | None = None, cols: int | None = None):
+    """Argument checks the C ABI cannot make (it sees only pointers): a CUDA
+    tensor of the dtype's operand type, 2-D, unit inner stride, given shape."""
+    want = _TORCH_DT[_dt(dtype) & DTYPE_MASK]
+    if not isinstance(t, torch.Tensor) or t.dim() != 2:
+        raise ValueError(f"{name}: expected a 2-D torch tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name}: must be a CUDA tensor (there is no CPU path)")
+    if t.dtype != want:
+        raise ValueError(f"{name}: dtype {t.dtype}, expected {want}")
+    if t.stride(1) != 1 or t.stride(0) < t.shape[1]:
+        raise ValueError(f"{name}: rows must be contiguous (stride(1) == 1, stride(0) >= cols)")
+    if (rows is not None and t.shape[0] != rows) or (cols is not None and t.shape[1] != cols):
+        raise ValueError(f"{name}: shape {tuple(t.shape)}, expected ({rows}, {cols})")
+
+
+def _gemm_operands(dtype, A, B, C_):
+    _operand("A", A, dtype)
+    M, K = A.shape
+    _operand("B", B, dtype, rows=K)
+    N = B.shape[1]
+    _operand("C", C_, dtype, rows=M, cols=N)
+    return M, N, K
 
 
 def _stream(stream) -> int:
@@ -154,31 +186,14 @@ class Plan:
     lambda2: float
 
 
-def plan(dtype, M: int, N: int, K: int) -> Plan:
+def plan(dtype, M: int, N: int, K: int, tile: tuple[int, int] | None = None) -> Plan:
+    """tile = (bn, cta_group): an explicit tensor-core tile class; plan.dtype is the
+    plan's fully explicit dtype code (pass it to encode / run)."""
+    if tile is not None:
+        dtype = tile_code(dtype, *tile)
     p = PlanStruct()
     _check(lib().ftgemm_plan(_dt(dtype), M, N, K, C.byref(p)), "ftgemm_plan")
     return Plan(**{f: getattr(p, f) for f in Plan.__dataclass_fields__})
-
-
-def set_tile_class(bn: int = 0, cta_group: int = 0) -> None:
-    """Force the tensor-core tile class (bn 128 | 256, cta_group 1 | 2) for later
-    calls in this process; (0, 0) restores the plan's own choice."""
-    _check(lib().ftgemm_set_tile_class(bn, cta_group), "ftgemm_set_tile_class")
-
-
-class tile_class:
-    """Context manager around set_tile_class (restores automatic choice on exit)."""
-
-    def __init__(self, bn: int, cta_group: int):
-        self.bn, self.cg = bn, cta_group
-
-    def __enter__(self):
-        set_tile_class(self.bn, self.cg)
-        return self
-
-    def __exit__(self, *exc):
-        set_tile_class(0, 0)
-        return False
 
 
 def encode_layout(dtype, M: int, N: int, K: int) -> dict:
@@ -197,6 +212,12 @@ def alloc_workspaces(pl: Plan, device="cuda"):
 
 def encode(dtype, A: torch.Tensor | None, B: torch.Tensor | None, enc_ws: torch.Tensor, *, M: int, N: int, K: int,
            which: int = 3, stream=None):
+    if which & 1:
+        _operand("A", A, dtype, rows=M, cols=K)
+    if which & 2:
+        _operand("B", B, dtype, rows=K, cols=N)
+    if enc_ws.numel() < plan(dtype, M, N, K).enc_bytes:
+        raise ValueError("enc_ws smaller than plan.enc_bytes")
     _check(lib().ftgemm_encode(_dt(dtype), M, N, K,
                                A.data_ptr() if A is not None else None, A.stride(0) if A is not None else K,
                                B.data_ptr() if B is not None else None, B.stride(0) if B is not None else N,
@@ -221,8 +242,7 @@ def run(dtype, A: torch.Tensor, B: torch.Tensor, C_: torch.Tensor, *, alpha: flo
         report_ws: torch.Tensor | None = None, stream=None, fuse_a: bool = False):
     """fuse_a: the A-side encode runs inside the GEMM kernel (ftgemm_run_fused);
     enc_ws then needs only the B part."""
-    M, K = A.shape
-    N = B.shape[1]
+    M, N, K = _gemm_operands(dtype, A, B, C_)
     arr, n = _inj_array(injections)
     fn = lib().ftgemm_run_fused if fuse_a else lib().ftgemm_run
     _check(fn(_dt(dtype), M, N, K, alpha, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0),
@@ -238,8 +258,7 @@ def run_offline(dtype, A: torch.Tensor, B: torch.Tensor, C_: torch.Tensor, *, al
                 max_runs: int = 4, c_backup: torch.Tensor | None = None, stream=None):
     """Offline (detect-only) ABFT with re-computation (PAPER.md:571-583).
     Returns (executions, clean).  inj_run[i]: the execution fault i strikes."""
-    M, K = A.shape
-    N = B.shape[1]
+    M, N, K = _gemm_operands(dtype, A, B, C_)
     arr, n = _inj_array(injections)
     runs = None
     if inj_run is not None:
@@ -267,8 +286,7 @@ def run_nonfused(dtype, A: torch.Tensor, B: torch.Tensor, C_: torch.Tensor, *, a
                  enc_ws: torch.Tensor | None = None, nf_ws: torch.Tensor | None = None, ft_level: int = FT_CORRECT,
                  injections=(), report_ws: torch.Tensor | None = None, stream=None):
     """The non-fused ABFT baseline (cuBLAS GEMMs + separate verification kernel)."""
-    M, K = A.shape
-    N = B.shape[1]
+    M, N, K = _gemm_operands(dtype, A, B, C_)
     arr, n = _inj_array(injections)
     _check(lib().ftgemm_run_nonfused(_dt(dtype), M, N, K, alpha, A.data_ptr(), A.stride(0), B.data_ptr(),
                                      B.stride(0), beta, C_.data_ptr(), C_.stride(0),
@@ -290,8 +308,7 @@ def run_online(dtype, A: torch.Tensor, B: torch.Tensor, C_: torch.Tensor, *, ks:
                beta: float = 0.0, enc_ws: torch.Tensor, ft_level: int = FT_CORRECT, injections=(),
                report_ws: torch.Tensor, stream=None):
     """Online ABFT verified after every ks of K."""
-    M, K = A.shape
-    N = B.shape[1]
+    M, N, K = _gemm_operands(dtype, A, B, C_)
     arr, n = _inj_array(injections)
     _check(lib().ftgemm_run_online(_dt(dtype), M, N, K, alpha, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0),
                                    beta, C_.data_ptr(), C_.stride(0), enc_ws.data_ptr(), ft_level, ks,
@@ -323,33 +340,48 @@ class FTGemm:
     """Convenience object: plan + workspaces for one (dtype, M, N, K).
 
     g = FTGemm("bf16", M, N, K); g.encode(A, B); g.run(A, B, C); counts, events = g.report()
+
+    tile = (bn, cta_group) fixes the tensor-core tile class (default: the plan's
+    choice).  Every call passes the plan's explicit dtype code, so the encode and
+    the run always agree on the layout of enc_ws.  With FT on, run() multiplies
+    by the copy of B inside enc_ws: re-encode B (which=2) after changing it.
     """
 
-    def __init__(self, dtype, M: int, N: int, K: int, device="cuda"):
-        self.dtype = _dt(dtype)
+    def __init__(self, dtype, M: int, N: int, K: int, device="cuda", tile: tuple[int, int] | None = None):
         self.M, self.N, self.K = M, N, K
-        self.plan = plan(self.dtype, M, N, K)
+        self.plan = plan(dtype, M, N, K, tile=tile)
+        self.dtype = self.plan.dtype                 # explicit code: dtype | tile class
         self.enc_ws, self.report_ws = alloc_workspaces(self.plan, device)
 
+    def _shape(self, A, B, C_=None):
+        for name, t, want in (("A", A, (self.M, self.K)), ("B", B, (self.K, self.N)), ("C", C_, (self.M, self.N))):
+            if t is not None and tuple(t.shape) != want:
+                raise ValueError(f"{name} shape {tuple(t.shape)} != {want} of this FTGemm")
+
     def encode(self, A=None, B=None, which: int = 3, stream=None):
+        self._shape(A, B)
         encode(self.dtype, A, B, self.enc_ws, M=self.M, N=self.N, K=self.K, which=which, stream=stream)
 
     def run(self, A, B, C_, *, alpha=1.0, beta=0.0, ft_level=FT_CORRECT, injections=(), stream=None, fuse_a=False):
+        self._shape(A, B, C_)
         run(self.dtype, A, B, C_, alpha=alpha, beta=beta, enc_ws=self.enc_ws, ft_level=ft_level,
             injections=injections, report_ws=self.report_ws, stream=stream, fuse_a=fuse_a)
 
     def run_online(self, A, B, C_, *, ks, alpha=1.0, beta=0.0, ft_level=FT_CORRECT, injections=(), stream=None):
+        self._shape(A, B, C_)
         run_online(self.dtype, A, B, C_, ks=ks, alpha=alpha, beta=beta, enc_ws=self.enc_ws, ft_level=ft_level,
                    injections=injections, report_ws=self.report_ws, stream=stream)
 
     def run_offline(self, A, B, C_, *, alpha=1.0, beta=0.0, injections=(), inj_run=None, max_runs=4,
                     c_backup=None, stream=None):
+        self._shape(A, B, C_)
         return run_offline(self.dtype, A, B, C_, alpha=alpha, beta=beta, enc_ws=self.enc_ws,
                            report_ws=self.report_ws, injections=injections, inj_run=inj_run, max_runs=max_runs,
                            c_backup=c_backup, stream=stream)
 
     def run_nonfused(self, A, B, C_, *, alpha=1.0, beta=0.0, ft_level=FT_CORRECT, injections=(), stream=None):
         """Non-fused baseline; encode first with encode(A, B, which=3 | 4)."""
+        self._shape(A, B, C_)
         if getattr(self, "nf_ws", None) is None:
             self.nf_ws = torch.empty(max(256, nonfused_workspace(self.dtype, self.M, self.N, self.K)),
                                      dtype=torch.uint8, device=self.enc_ws.device)

@@ -32,7 +32,7 @@ class HostPipeline:
             raise ValueError("depth must be >= 2 (double buffering)")
         self.g = g
         self.depth = depth
-        dt = {F.BF16: torch.bfloat16}.get(g.dtype, torch.float32)
+        dt = {F.BF16: torch.bfloat16}.get(g.dtype & F.DTYPE_MASK, torch.float32)
         M, N, K = g.M, g.N, g.K
         self.A = [torch.empty(M, K, dtype=dt, device=device) for _ in range(depth)]
         self.B = [torch.empty(K, N, dtype=dt, device=device) for _ in range(depth)]

@@ -196,22 +196,34 @@ def test_nonfused_host_checks(F):
     assert lib.ftgemm_run_nonfused(2, 64, 64, 64, 1.0, vp, 64, vp, 64, 0.0, vp, 64, None, None, 2, None, 0, vp, None) == 1
 
 
-def test_set_tile_class(F):
-    """ftgemm_set_tile_class forces the tensor-core class for later plans (the
-    multi-GPU partition runs every rank with the full problem's check tiles);
-    (0, 0) restores the plan's own choice; skinny shapes keep their rule."""
+def test_explicit_tile_class(F):
+    """An explicit class in the dtype code (FTGEMM_TILE(bn, cta_group)) fixes the
+    tensor-core plan for that call only -- there is no process-wide state --
+    and wins over every shape rule; plan.dtype is the plan's explicit code, so
+    re-planning with it reproduces the plan (the multi-GPU partition runs every
+    rank with the full problem's check tiles this way).  Invalid classes and a
+    class on F32_SIMT are argument errors."""
     auto = F.plan("bf16", 8192, 8192, 8192)
     assert (auto.bn, auto.cta_group) == (256, 2)
-    with F.tile_class(128, 1):
-        p = F.plan("bf16", 8192, 8192, 8192)
-        assert (p.bn, p.cta_group, p.check_tile_n) == (128, 1, 124)
-        sn = F.plan("bf16", 16384, 128, 16384)
-        assert sn.bn == 256 and sn.tiles_n == 1
-        s = F.plan("f32_simt", 1024, 1024, 1024)
-        assert s.bn == 128 and s.check_tile_n == 128
-    back = F.plan("bf16", 8192, 8192, 8192)
-    assert (back.bn, back.cta_group) == (256, 2)
-    with pytest.raises(F.FtgemmError):
-        F.set_tile_class(192, 1)
-    with pytest.raises(F.FtgemmError):
-        F.set_tile_class(256, 3)
+    assert auto.dtype == F.tile_code("bf16", 256, 2) == (2 | 2 << 8 | 2 << 12)
+    p = F.plan("bf16", 8192, 8192, 8192, tile=(128, 1))
+    assert (p.bn, p.cta_group, p.check_tile_n) == (128, 1, 124)
+    assert F.plan(p.dtype, 8192, 8192, 8192) == p
+    assert F.plan("bf16", 8192, 8192, 8192) == auto            # nothing ambient changed
+    sn = F.plan("bf16", 16384, 128, 16384)
+    assert sn.bn == 256 and sn.tiles_n == 1
+    sn2 = F.plan("bf16", 16384, 128, 16384, tile=(128, 2))
+    assert (sn2.bn, sn2.cta_group, sn2.tiles_n) == (128, 2, 2)
+    s = F.plan("f32_simt", 1024, 1024, 1024)
+    assert s.bn == 128 and s.check_tile_n == 128 and s.dtype == F.F32_SIMT
+    for bad in ((192, 1), (256, 3)):
+        with pytest.raises(F.FtgemmError) as e:
+            F.plan("bf16", 64, 64, 64, tile=bad)
+        assert e.value.code == 1
+    for code in (F.tile_code("f32_simt", 128, 1), F.BF16 | (1 << 8), F.BF16 | (1 << 20)):
+        with pytest.raises(F.FtgemmError) as e:
+            F.plan(code, 64, 64, 64)
+        assert e.value.code == 1
+    # encode and run with different codes must not be mixed: the layouts differ
+    a, b = F.encode_layout(auto.dtype, 8192, 8192, 8192), F.encode_layout(p.dtype, 8192, 8192, 8192)
+    assert a["bt_ld"] == 33 * 256 and b["bt_ld"] == 67 * 128

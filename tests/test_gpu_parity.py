@@ -11,7 +11,14 @@ import pytest
 
 import oracle
 import synth
-from gpu_util import TOL, Case, detectable_sites, frob, odt
+from gpu_util import TOL, Case, detectable_sites, elementwise_ratio, frob, odt, oracle_operand, uncorrectable_mask
+
+
+def simt_tol(K: int) -> float:
+    """FP32 SIMT relative Frobenius bound (R14): the north_star 1e-6
+    for K <= 2048; beyond, max(1e-6, 2 u sqrt(K)) with clean elements bit-exact
+    against the oracle's FP32SEQ mode (test_cfg2_full_size_sampled)."""
+    return 1e-6 if K <= 2048 else max(1e-6, 2 * 2 ** -24 * math.sqrt(K))
 
 pytestmark = pytest.mark.gpu
 
@@ -66,8 +73,9 @@ SHAPES = [
 def test_clean_parity(dtype, shape):
     M, N, K, lda, ldb, ldc = shape
     c = Case(dtype, M, N, K, lda=lda, ldb=ldb, ldc=ldc, alpha=1.5, beta=-0.5)
-    tol = TOL[dtype] if dtype != "f32_simt" else max(1e-6, 2 * 2 ** -24 * math.sqrt(K))
+    tol = TOL[dtype] if dtype != "f32_simt" else simt_tol(K)
     assert c.fro() < tol, c.fro()
+    assert c.elementwise() <= 1.0
     assert c.counts["tiles_checked"] == c.plan.tiles_m * c.plan.tiles_n
     assert c.counts["tiles_detected"] == 0 and c.counts_match() and c.events_match()
 
@@ -95,10 +103,7 @@ def test_ft_off_matches_ft_on_clean(dtype):
     F = ftmod()
     on = Case(dtype, 640, 760, 512, run_oracle=False)
     off = Case(dtype, 640, 760, 512, ft=F.FT_OFF, run_oracle=False)
-    if dtype == "f32_simt":
-        assert np.array_equal(on.C, off.C)
-    else:
-        assert np.abs(on.C - off.C).max() <= 1e-6 * np.abs(off.C).max()
+    assert np.array_equal(on.C.view(np.uint32), off.C.view(np.uint32))
 
 
 def test_determinism():
@@ -123,7 +128,8 @@ def test_injected_single_faults_parity(dtype, dist):
     c = Case(dtype, M, N, K, dist=dist, injections=inj, alpha=1.0, beta=0.0)
     assert c.counts["corrected"] == len(inj), (c.counts, c.ref.counts)
     assert c.events_match() and c.counts_match()
-    assert c.fro() < TOL[dtype] if dtype != "f32_simt" else c.fro() < 5e-6
+    assert c.fro() < (TOL[dtype] if dtype != "f32_simt" else simt_tol(K))
+    assert c.elementwise() <= 1.0
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
@@ -138,6 +144,7 @@ def test_cfg1_one_flip(dtype):
         c = Case(dtype, M, N, K, dist=dist, injections=inj, alpha=1.5, beta=-0.5)
         assert c.counts["corrected"] == 1 and c.events_match()
         assert c.fro() < (TOL[dtype] if dtype != "f32_simt" else 1e-6)
+        assert c.elementwise() <= 1.0
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
@@ -162,7 +169,8 @@ def test_add_mode_and_nonfinite(dtype):
     c = Case(dtype, M, N, K, dist="unit", injections=inj)
     assert c.counts["corrected"] == 3 and c.events_match()
     assert np.all(np.isfinite(c.C))
-    assert c.fro() < (TOL[dtype] if dtype != "f32_simt" else 5e-6)
+    assert c.fro() < (TOL[dtype] if dtype != "f32_simt" else 1e-6)
+    assert c.elementwise() <= 1.0
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
@@ -182,7 +190,8 @@ def test_seu_violation_and_checksum_faults(dtype):
     bad = np.zeros((M, N), bool)
     bad[[1, 7], :] = True
     bad[:, [2, 9]] = True
-    assert c.fro(~bad) < (TOL[dtype] if dtype != "f32_simt" else 5e-6)
+    assert c.fro(~bad) < (TOL[dtype] if dtype != "f32_simt" else 1e-6)
+    assert c.elementwise(skip=bad) <= 1.0
     assert abs(c.C[1, 2] - c.ref.C[1, 2]) <= 1e-2 * abs(c.ref.C[1, 2]) + 1.0
 
 
@@ -204,6 +213,7 @@ def test_stress_one_fault_per_tile():
     inj = detectable_sites("bf16", plan.tiles_m * plan.tiles_n, M, N, K, plan, A, B, seed=99)
     c = Case("bf16", M, N, K, injections=inj)
     assert c.counts["corrected"] == len(inj) and c.events_match() and c.fro() < TOL["bf16"]
+    assert c.elementwise() <= 1.0
 
 
 @pytest.mark.parametrize("dtype", ["tf32", "bf16"])
@@ -221,23 +231,23 @@ def test_false_positive_sweep(dtype):
 @pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("dtype", ["tf32", "bf16"])
 @pytest.mark.parametrize("shape", [(845, 600, 1000), (1000, 10896, 2048)], ids=["bn128", "bn256"])
-def test_fused_encode_parity(dtype, cg, shape, monkeypatch):
+def test_fused_encode_parity(dtype, cg, shape):
     """ftgemm_run_fused: with only B encoded,
     the kernel derives e^T A, its split rows and the row / tile norms itself;
     events, counts and C as the oracle; C bit-identical to the separately
     encoded run except at corrected elements (same tiles, same k order)."""
     import torch
-    monkeypatch.setenv("FTGEMM_CG", str(cg))
     F = ftmod()
     M, N, K = shape
     A, B, Cin = synth.problem(M, N, K, dtype=odt(dtype))
-    plan = F.plan(dtype, M, N, K)
+    plan = F.plan(dtype, M, N, K, tile=(F.plan(dtype, M, N, K).bn, cg))
     assert plan.cta_group == cg
+    dtype_c = plan.dtype
     tm, tn = plan.check_tile_m, plan.check_tile_n
     inj = detectable_sites(dtype, 8, M, N, K, plan, A, B, seed=61)
     inj.append((plan.tiles_m * tm - tm + 2, 3, 40, 0, oracle.INJ_ADD, 0, 800.0))          # last (ragged) tile row
     Ad, Bd = synth.to_torch(A, odt(dtype)).cuda(), synth.to_torch(B, odt(dtype)).cuda()
-    g = F.FTGemm(dtype, M, N, K)
+    g = F.FTGemm(dtype_c, M, N, K)
     g.enc_ws.fill_(0xFF)                          # the A part must not be read
     g.encode(None, Bd, which=2)
     Cf = synth.to_torch(Cin, odt(dtype)).cuda()
@@ -253,7 +263,7 @@ def test_fused_encode_parity(dtype, cg, shape, monkeypatch):
     assert ek(events) == ek(ref.events)
     assert frob(Cf.float().cpu().numpy(), ref.C) < TOL[dtype]
     # against the separately encoded run: identical away from the corrected elements
-    g2 = F.FTGemm(dtype, M, N, K)
+    g2 = F.FTGemm(dtype_c, M, N, K)
     g2.encode(Ad, Bd)
     C2 = synth.to_torch(Cin, odt(dtype)).cuda()
     g2.run(Ad, Bd, C2, alpha=1.5, beta=-0.5, injections=inj)
@@ -299,18 +309,17 @@ def test_partition_invariance(dtype, shape):
         parts = row_partition(M, world, tm)
         Cp, evs = [], []
         for row0, rows in parts:
-            # a rank runs the full problem's tile class (as distributed.PartitionedFTGemm does)
-            cls = F.tile_class(full_plan.bn, full_plan.cta_group) if dtype != "f32_simt" else contextlib.nullcontext()
-            with cls:
-                gp = F.FTGemm(dtype, rows, N, K)
-                assert (gp.plan.bn, gp.plan.cta_group, gp.plan.check_tile_m, gp.plan.check_tile_n) == \
-                    (full_plan.bn, full_plan.cta_group, full_plan.check_tile_m, full_plan.check_tile_n)
-                mine = [(r - row0, c, k, b, m, tg, ad) for (r, c, k, b, m, tg, ad) in inj if row0 <= r < row0 + rows]
-                Cd = synth.to_torch(Cin[row0:row0 + rows], odt(dtype)).cuda()
-                Ar = Ad[row0:row0 + rows].contiguous()
-                gp.encode(Ar, Bd)
-                gp.run(Ar, Bd, Cd, alpha=1.0, beta=0.5, injections=mine)
-                torch.cuda.synchronize()
+            # a rank runs the full problem's tile class (as distributed.PartitionedFTGemm
+            # does: full_plan.dtype is the full plan's explicit dtype code)
+            gp = F.FTGemm(full_plan.dtype, rows, N, K)
+            assert (gp.plan.bn, gp.plan.cta_group, gp.plan.check_tile_m, gp.plan.check_tile_n) == \
+                (full_plan.bn, full_plan.cta_group, full_plan.check_tile_m, full_plan.check_tile_n)
+            mine = [(r - row0, c, k, b, m, tg, ad) for (r, c, k, b, m, tg, ad) in inj if row0 <= r < row0 + rows]
+            Cd = synth.to_torch(Cin[row0:row0 + rows], odt(dtype)).cuda()
+            Ar = Ad[row0:row0 + rows].contiguous()
+            gp.encode(Ar, Bd)
+            gp.run(Ar, Bd, Cd, alpha=1.0, beta=0.5, injections=mine)
+            torch.cuda.synchronize()
             _, e = gp.report()
             for x in e:
                 x = dict(x)
@@ -348,18 +357,17 @@ def test_skinny_shapes(dtype, shape):
 
 @pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("dtype", ["tf32", "bf16"])
-def test_online_interval_parity(dtype, cg, monkeypatch):
+def test_online_interval_parity(dtype, cg):
     """ftgemm_run_online: the fused kernel verifies
     after every K_s step and corrects in TMEM.  Several faults per tile in
     different steps are all corrected; a double fault within one step is
     uncorrectable at that step and after; a reference fault is reported at
     every later check; events (with k_checked) and counts as in the oracle."""
     import torch
-    monkeypatch.setenv("FTGEMM_CG", str(cg))
     F = ftmod()
     M, N, K = 845, 600, 1024
     A, B, Cin = synth.problem(M, N, K, dtype=odt(dtype))
-    plan = F.plan(dtype, M, N, K)
+    plan = F.plan(dtype, M, N, K, tile=(F.plan(dtype, M, N, K).bn, cg))
     tm, tn = plan.check_tile_m, plan.check_tile_n
     ks = 256
     inj = [(5, 7, 40, 0, oracle.INJ_ADD, 0, 1000.0), (5, 90, 300, 0, oracle.INJ_ADD, 0, -800.0),      # tile (0,0)
@@ -368,7 +376,7 @@ def test_online_interval_parity(dtype, cg, monkeypatch):
            (3 * tm + 1, 2, 520, 0, oracle.INJ_ADD, 0, 700.0), (3 * tm + 8, 9, 600, 0, oracle.INJ_ADD, 0, -700.0),  # same step
            (4 * tm + 2, tn + 1, 300, 0, oracle.INJ_ADD, oracle.TGT_ROW_REF, 600.0),
            (6 * tm + 1, 3, 10, 0, oracle.INJ_ADD, 0, 900.0), (6 * tm + 2, 4, 900, 0, oracle.INJ_ADD, 0, 900.0)]
-    g = F.FTGemm(dtype, M, N, K)
+    g = F.FTGemm(plan.dtype, M, N, K)
     assert g.plan.cta_group == cg
     Ad, Bd = synth.to_torch(A, odt(dtype)).cuda(), synth.to_torch(B, odt(dtype)).cuda()
     Cd = synth.to_torch(Cin, odt(dtype)).cuda()
@@ -470,7 +478,8 @@ def test_detect_rows_parity(dtype):
     for r, col, _, _, _, tgt, _ in inj:
         if tgt == 0:
             bad[r, col] = True
-    assert c.fro(~bad) < (TOL[dtype] if dtype != "f32_simt" else 5e-6)
+    assert c.fro(~bad) < (TOL[dtype] if dtype != "f32_simt" else 1e-6)
+    assert c.elementwise(skip=bad) <= 1.0
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
@@ -491,7 +500,7 @@ def test_run_offline_recompute(dtype):
     g.encode(Ad, Bd)
     faults = [(5, 7, 40, 0, oracle.INJ_ADD, 0, 1000.0), (tm + 3, tn + 4, 200, 0, oracle.INJ_ADD, 0, -1000.0),
               (3 * tm + 1, 2 * tn + 9, 300, 0, oracle.INJ_ADD, 0, 5000.0)]
-    tol = TOL[dtype] if dtype != "f32_simt" else 5e-6
+    tol = TOL[dtype] if dtype != "f32_simt" else 1e-6
 
     def go(inj_run, max_runs, beta=-0.5):
         Cd = synth.to_torch(Cin, odt(dtype)).cuda()
@@ -520,16 +529,16 @@ def test_run_offline_recompute(dtype):
 @pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("dtype", ["tf32", "bf16"])
 @pytest.mark.parametrize("shape", [(845, 600, 320), (845, 10896, 256)], ids=["bn128", "bn256"])
-def test_cta_pair_modes(dtype, cg, shape, monkeypatch):
+def test_cta_pair_modes(dtype, cg, shape):
     """Both tensor-core launch modes (one CTA per MMA, or a cta_group::2 pair with
     M = 256) give the oracle's C, events and counts.  7 check-tile rows: the last
     pair's second tile lies beyond M.  Faults in both CTAs of a pair (even and
     odd tile rows), in the carried references, and an SEU violation."""
-    monkeypatch.setenv("FTGEMM_CG", str(cg))
     F = ftmod()
     M, N, K = shape
     A, B, _ = synth.problem(M, N, K, dtype=odt(dtype))
-    plan = F.plan(dtype, M, N, K)
+    tile = (F.plan(dtype, M, N, K).bn, cg)
+    plan = F.plan(dtype, M, N, K, tile=tile)
     assert plan.cta_group == cg and plan.tiles_m == 7
     tm, tn = plan.check_tile_m, plan.check_tile_n
     inj = detectable_sites(dtype, 8, M, N, K, plan, A, B, seed=21)
@@ -539,7 +548,7 @@ def test_cta_pair_modes(dtype, cg, shape, monkeypatch):
              (6 * tm + 1, 4, 10, 0, oracle.INJ_ADD, 0, 900.0),                            # last (unpaired) row
              (6 * tm + 2, 8, 200, 0, oracle.INJ_ADD, 0, -900.0)]                          # ... twice: SEU violation
     inj += [f for f in extra if (f[0] // tm, f[1] // tn) not in used]
-    c = Case(dtype, M, N, K, injections=inj, alpha=1.25, beta=0.5)
+    c = Case(dtype, M, N, K, injections=inj, alpha=1.25, beta=0.5, tile=tile)
     assert c.counts_match() and c.events_match(), (c.counts, c.ref.counts)
     assert c.counts["tiles_checked"] == plan.tiles_m * plan.tiles_n
     bad = np.zeros((M, N), bool)
@@ -547,7 +556,7 @@ def test_cta_pair_modes(dtype, cg, shape, monkeypatch):
         if e["kind"] == oracle.EV_UNCORRECTABLE:
             bad[e["tile_m"] * tm:(e["tile_m"] + 1) * tm, e["tile_n"] * tn:(e["tile_n"] + 1) * tn] = True
     assert c.fro(~bad) < TOL[dtype]
-    off = Case(dtype, M, N, K, ft=F.FT_OFF, alpha=1.25, beta=0.5)
+    off = Case(dtype, M, N, K, ft=F.FT_OFF, alpha=1.25, beta=0.5, tile=tile)
     assert off.fro() < TOL[dtype]
 
 
@@ -587,6 +596,7 @@ def test_cfg3_full_size_sampled():
         blk = Ch[r0:r1, c0:c1].astype(np.float64)
         rel = np.linalg.norm(blk - ref.C) / np.linalg.norm(ref.C)
         assert rel < TOL["bf16"], (ti, tj, rel)
+        assert elementwise_ratio(blk, ref, Ab, Bb, plan=plan, out="bf16") <= 1.0, (ti, tj)
         mine = sorted((e["row"] - r0, e["col"] - c0) for e in events if e["tile_m"] == ti and e["tile_n"] == tj)
         assert mine == sorted((e["row"], e["col"]) for e in ref.events)
 
@@ -608,15 +618,14 @@ def test_cfg5_rank_share_sampled():
     A = synth.to_torch(synth.matrix(seedA, Mf, K, dtype="bf16", r0=row0, r1=row0 + M), "bf16").cuda()
     B = synth.to_torch(synth.matrix(seedB, K, N, dtype="bf16"), "bf16").cuda()
     C = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
-    with F.tile_class(full.bn, full.cta_group):
-        g = F.FTGemm("bf16", M, N, K)
-        plan = g.plan
-        assert (plan.bn, plan.cta_group, plan.check_tile_n) == (full.bn, full.cta_group, full.check_tile_n)
-        tiles = [(0, 0), (11, 60), (plan.tiles_m - 1, plan.tiles_n - 1), (20, 7)]
-        inj = [(ti * tm + min(3, M - ti * tm - 1), tj * tn + min(9, N - tj * tn - 1), 9000, 30, oracle.INJ_FLIP, 0, 0.0)
-               for ti, tj in tiles[:3]]                  # (the last tile column is 8 wide)
-        g.encode(A, B)
-        g.run(A, B, C, injections=inj)
+    g = F.FTGemm(full.dtype, M, N, K)
+    plan = g.plan
+    assert (plan.bn, plan.cta_group, plan.check_tile_n) == (full.bn, full.cta_group, full.check_tile_n)
+    tiles = [(0, 0), (11, 60), (plan.tiles_m - 1, plan.tiles_n - 1), (20, 7)]
+    inj = [(ti * tm + min(3, M - ti * tm - 1), tj * tn + min(9, N - tj * tn - 1), 9000, 30, oracle.INJ_FLIP, 0, 0.0)
+           for ti, tj in tiles[:3]]                  # (the last tile column is 8 wide)
+    g.encode(A, B)
+    g.run(A, B, C, injections=inj)
     counts, events = g.report()
     assert counts["corrected"] == 3 and counts["tiles_detected"] == 3
     assert counts["tiles_checked"] == plan.tiles_m * plan.tiles_n
@@ -631,6 +640,7 @@ def test_cfg5_rank_share_sampled():
         assert ref.counts["corrected"] == len(loc)
         blk = C[r0:r1, c0:c1].float().cpu().numpy().astype(np.float64)
         assert np.linalg.norm(blk - ref.C) / np.linalg.norm(ref.C) < TOL["bf16"], (ti, tj)
+        assert elementwise_ratio(blk, ref, Ab, Bb, plan=plan, out="bf16") <= 1.0, (ti, tj)
         mine = sorted((e["row"] - r0, e["col"] - c0) for e in events if e["tile_m"] == ti and e["tile_n"] == tj)
         assert mine == sorted((e["row"], e["col"]) for e in ref.events)
     del B, C
@@ -667,14 +677,15 @@ def test_cfg4_full_size_sampled(dtype, shape):
     for (ti, tj) in tiles:
         r0, c0 = ti * tm, tj * tn
         r1, c1 = min(M, r0 + tm), min(N, c0 + tn)
-        Ab = synth.matrix(seedA, M, K, dtype=odt(dtype), r0=r0, r1=r1)
-        Bb = synth.matrix(seedB, K, N, dtype=odt(dtype), c0=c0, c1=c1)
+        Ab = oracle_operand(synth.matrix(seedA, M, K, dtype=odt(dtype), r0=r0, r1=r1), dtype)
+        Bb = oracle_operand(synth.matrix(seedB, K, N, dtype=odt(dtype), c0=c0, c1=c1), dtype)
         loc = [(r - r0, c - c0, k, b, m, tg, ad) for (r, c, k, b, m, tg, ad) in inj if r0 <= r < r1 and c0 <= c < c1]
         ref = oracle.ftgemm(Ab, Bb, out=odt(dtype), tile_m=tm, tile_n=tn, bk=plan.bk, u_acc=plan.u_acc,
                             lambda1=plan.lambda1, lambda2=plan.lambda2, injections=loc)
         assert ref.counts["corrected"] == len(loc)
         blk = C[r0:r1, c0:c1].float().cpu().numpy().astype(np.float64)
         assert np.linalg.norm(blk - ref.C) / np.linalg.norm(ref.C) < TOL[dtype], (ti, tj)
+        assert elementwise_ratio(blk, ref, Ab, Bb, plan=plan, out=odt(dtype)) <= 1.0, (ti, tj)
         mine = sorted((e["row"] - r0, e["col"] - c0) for e in events if e["tile_m"] == ti and e["tile_n"] == tj)
         assert mine == sorted((e["row"], e["col"]) for e in ref.events)
     del A, B, C
@@ -707,8 +718,8 @@ def test_cfg2_full_size_sampled(dtype):
     for (ti, tj) in tiles:
         r0, c0 = ti * tm, tj * tn
         r1, c1 = min(M, r0 + tm), min(N, c0 + tn)
-        Ab = synth.matrix(seedA, M, K, dtype="f32", r0=r0, r1=r1)
-        Bb = synth.matrix(seedB, K, N, dtype="f32", c0=c0, c1=c1)
+        Ab = oracle_operand(synth.matrix(seedA, M, K, dtype="f32", r0=r0, r1=r1), dtype)
+        Bb = oracle_operand(synth.matrix(seedB, K, N, dtype="f32", c0=c0, c1=c1), dtype)
         loc = [(r - r0, c - c0, k, b, m, tg, ad) for (r, c, k, b, m, tg, ad) in inj if r0 <= r < r1 and c0 <= c < c1]
         ref = oracle.ftgemm(Ab, Bb, out="f32", acc=acc, tile_m=tm, tile_n=tn, bk=plan.bk, u_acc=plan.u_acc,
                             lambda1=plan.lambda1, lambda2=plan.lambda2, injections=loc)
@@ -721,6 +732,9 @@ def test_cfg2_full_size_sampled(dtype):
             assert np.array_equal(blk[clean], ref.C[clean].astype(np.float32)), (ti, tj)
         rel = np.linalg.norm(blk.astype(np.float64) - ref.C) / np.linalg.norm(ref.C)
         assert rel < (2 * 2 ** -24 * math.sqrt(K) if dtype == "f32_simt" else TOL[dtype]), (ti, tj, rel)
+        if dtype != "f32_simt":       # (SIMT: every clean element is bit-exact above; the FP32SEQ
+            # reference has no FP64 accumulator to bound against)
+            assert elementwise_ratio(blk, ref, Ab, Bb, plan=plan, out="f32") <= 1.0, (ti, tj)
         mine = sorted((e["row"] - r0, e["col"] - c0) for e in events if e["tile_m"] == ti and e["tile_n"] == tj)
         assert mine == sorted((e["row"], e["col"]) for e in ref.events)
     del A, B, C
@@ -761,6 +775,7 @@ def test_large_indexing_sampled():
                             lambda1=plan.lambda1, lambda2=plan.lambda2, injections=loc)
         blk = C[r0:r1, c0:c1].float().cpu().numpy().astype(np.float64)
         assert np.linalg.norm(blk - ref.C) / np.linalg.norm(ref.C) < TOL["bf16"], (ti, tj)
+        assert elementwise_ratio(blk, ref, Ab, Bb, plan=plan, out="bf16") <= 1.0, (ti, tj)
         mine = sorted((e["row"] - r0, e["col"] - c0) for e in events if e["tile_m"] == ti and e["tile_n"] == tj)
         assert mine == sorted((e["row"], e["col"]) for e in ref.events)
     del C
@@ -774,7 +789,7 @@ def test_device_argument_errors():
     A = torch.zeros(64, 64, dtype=torch.bfloat16, device="cuda")
     C = torch.zeros(64, 64, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(F.FtgemmError) as e:
-        F.run("bf16", A[:, 1:], A[1:, :], C[:, 1:], ft_level=F.FT_OFF)     # misaligned base
+        F.run("bf16", A[:, 1:], A[1:, 1:], C[:, 1:], ft_level=F.FT_OFF)    # misaligned base
     assert e.value.code == 2
     g = F.FTGemm("bf16", 64, 64, 64)
     with pytest.raises(F.FtgemmError) as e:
@@ -862,17 +877,17 @@ def test_host_pipeline_matches_isolated_steps(dtype, beta):
 @pytest.mark.parametrize("cls", [(256, 2), (256, 1), (128, 1), (128, 2)], ids=lambda c: f"bn{c[0]}cg{c[1]}")
 def test_forced_tile_classes_parity(dtype, cls):
     """Every tensor-core tile class the plan's cost model can choose (and
-    ftgemm_set_tile_class can force) gives the oracle's C, events and counts,
+    an explicit FTGEMM_TILE class in the dtype code can force) gives the oracle's C, events and counts,
     with detectable flips in several tiles, including the ragged last ones."""
     F = ftmod()
     M, N, K = 1000, 2016, 1024
-    with F.tile_class(*cls):
-        plan = F.plan(dtype, M, N, K)
-        assert (plan.bn, plan.cta_group) == cls
-        A, B, _ = synth.problem(M, N, K, dtype=odt(dtype))
-        inj = detectable_sites(dtype, 8, M, N, K, plan, A, B, seed=71)
-        assert len(inj) >= 5
-        c = Case(dtype, M, N, K, injections=inj, alpha=1.0, beta=0.25)
+    plan = F.plan(dtype, M, N, K, tile=cls)
+    assert (plan.bn, plan.cta_group) == cls
+    A, B, _ = synth.problem(M, N, K, dtype=odt(dtype))
+    inj = detectable_sites(dtype, 8, M, N, K, plan, A, B, seed=71)
+    assert len(inj) >= 5
+    c = Case(dtype, M, N, K, injections=inj, alpha=1.0, beta=0.25, tile=cls)
     assert c.counts["corrected"] == len(inj), (c.counts, c.ref.counts)
     assert c.events_match() and c.counts_match()
     assert c.fro() < TOL[dtype]
+    assert c.elementwise() <= 1.0
