@@ -3,24 +3,33 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Workload (BASELINE.json configs[2], "cfg3"): BF16 tcgen05 ABFT GEMM 8192^3,
-C = A B (alpha 1, beta 0), inputs U[-1,1) rounded to BF16 (synthetic, seeded).
-One STEP = the whole hot path of SURVEY.md §8(a): encode A (a1), encode B (a2),
-the fused FT GEMM with verify / locate / correct (a3-a7) at ft_level CORRECT,
-with faults injected by a seeded schedule at ERRORS_PER_MIN (a4); the report
-counters (a8) accumulate on the device and are read and checked after the timed
-region.  N > 1 (torchrun): M-block partition (weak scaling): every rank owns an
-8192 x 8192 block of A and C, B (8192 x 8192) is generated on rank 0 and
-broadcast ONCE over NCCL before timing; each rank's step is the same as the
-1-GPU step.  Timing: W warm-up steps, then K steps bracketed by a barrier +
+N = 1 (BASELINE.json configs[2], "cfg3"): BF16 tcgen05 ABFT GEMM 8192^3,
+C = A B (alpha 1, beta 0), inputs U[-1,1) rounded to BF16 (synthetic, seeded,
+generated on the device by the counter-based generator of synth/).  One STEP =
+the whole hot path of SURVEY.md 8(a): encode A (a1), encode B (a2), the fused
+FT GEMM with verify / locate / correct (a3-a7) at ft_level CORRECT, with faults
+injected by a seeded schedule (a4; at least one fault inside every timed
+region); the report counters (a8) accumulate on the device and are read and
+checked after the timed region.  Inputs (A + B = 256 MiB) exceed the 126 MB L2.
+
+N > 1 (torchrun; BASELINE.json configs[4], "cfg5"): BF16 32768 x 32768 x 16384
+M-block-partitioned over the N GPUs (strong scaling) through
+paper_2305_01024_b200.distributed.PartitionedFTGemm: B is generated on rank 0,
+encoded once and broadcast once with its encode (NCCL); a steady-state STEP on
+every rank = encode of its A block + its fused FT GEMM (B resident and
+pre-encoded, weight-like); the one-shot time (encode B + broadcast + step) is
+reported beside it.
+
+Timing: W warm-up steps, then K steps bracketed by a barrier +
 cuda.synchronize on both sides, CUDA events on the launch stream, max over
-ranks.  Inputs (A + B = 256 MiB per rank) are larger than the 126 MB L2.
+ranks.  Comparators are timed call by call in one interleaved loop whose order
+is a fresh random permutation every call, so that all see the same clock /
+power state and no fixed predecessor.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -31,29 +40,38 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "FT-GEMM TFLOPS & % overhead vs non-FT/cuBLAS at 0..N errors/min, 1-8 B200"
-M_PER_RANK, N_DIM, K_DIM = 8192, 8192, 8192
-ERRORS_PER_MIN = 500.0           # "hundreds of errors per minute" (north_star)
+M3 = N3 = K3 = 8192                       # cfg3
+M5, N5, K5 = 32768, 32768, 16384          # cfg5
+ERRORS_PER_MIN = 500.0                    # "hundreds of errors per minute" (north_star)
 SWEEP_RATES = (0.0, 1.0, 10.0, 100.0, 500.0)
-OFFLINE_GAMMA0 = (1e-5, 1e-4, 2e-4)   # per-tile error probability per execution (online vs offline)
+FAULTS_PER_CALL = (0, 1, 10, 100, -1)     # -1: one fault in every check tile
+OFFLINE_GAMMA0 = (1e-5, 1e-4, 2e-4)       # per-tile error probability per execution (online vs offline)
+BURST_WINDOW_S = 0.25                     # timed regions shorter than this run at burst clocks
+SIMT_FFMA_PEAK = 148 * 128 * 2 * 1.965e9 / 1e12   # FP32 FFMA: SMs x FMA lanes x 2 x max clock
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=400)   # ~0.35 s timed: several clock samples, ~3 faults at 500/min
+    ap.add_argument("--steps", type=int, default=400)   # ~0.35 s timed: several clock samples
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-sweep", action="store_true", help="skip the injection-rate sweep and comparators")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the comparators and side workloads")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-oracle sample budget")
+    ap.add_argument("--backend", default="nccl", help="process-group backend for N > 1 (gloo: host-logic check)")
     return ap.parse_args()
 
 
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
-        d = json.load(open(p))
-        return d, "measured"
+        return json.load(open(p)), "measured"
+    # /opt/skills/guides/B200_PROFILING.md fallbacks
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def tflops(flops: float, ms: float) -> float:
+    return flops / (ms * 1e-3) / 1e12
 
 
 # ----------------------------------------------------------- CPU oracle leg ---
@@ -64,13 +82,13 @@ def cpu_oracle_sample(budget_s: float):
     import oracle
     import synth
     oracle.build()
-    tm, tn, K = 125, 252, K_DIM                # the plan's BF16 check tile
+    tm, tn, K = 125, 252, K3                   # the plan's BF16 check tile
     done_tiles, flops, t_spent = 0, 0.0, 0.0
     ti = tj = 0
     t0 = time.time()
     while True:
-        A = synth.matrix(synth.BASE_SEED + synth.SEED_A, M_PER_RANK, K, dtype="bf16", r0=ti * tm, r1=ti * tm + tm)
-        B = synth.matrix(synth.BASE_SEED + synth.SEED_B, K, N_DIM, dtype="bf16", c0=tj * tn, c1=tj * tn + tn)
+        A = synth.matrix(synth.BASE_SEED + synth.SEED_A, M3, K, dtype="bf16", r0=ti * tm, r1=ti * tm + tm)
+        B = synth.matrix(synth.BASE_SEED + synth.SEED_B, K, N3, dtype="bf16", c0=tj * tn, c1=tj * tn + tn)
         t1 = time.time()
         oracle.ftgemm(A, B, out="bf16", tile_m=tm, tile_n=tn, bk=64, u_acc=2.0 ** -23, lambda1=8.0, lambda2=16.0)
         t_spent += time.time() - t1
@@ -79,25 +97,24 @@ def cpu_oracle_sample(budget_s: float):
         ti, tj = (ti + 7) % 65, (tj + 5) % 32
         if time.time() - t0 > budget_s or done_tiles >= 4096:
             break
-    tflops = flops / t_spent / 1e12
-    return tflops, oracle.num_threads(), (f"{done_tiles} check tiles of 125x252x8192 (BF16 values, FP64 oracle incl. "
-                                           f"encode/verify), {flops / 1e9:.1f} GFLOP in {t_spent:.1f}s")
+    return flops / t_spent / 1e12, oracle.num_threads(), (
+        f"{done_tiles} check tiles of 125x252x8192 (BF16 values, FP64 oracle incl. encode/verify), "
+        f"{flops / 1e9:.1f} GFLOP in {t_spent:.1f}s")
 
 
 def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """The reference arm: the paper-derived CPU oracle (no reference
+    implementation exists), timed on a bounded tile sample of cfg3."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return 0
-    tflops, cores, desc = cpu_oracle_sample(min(args.cpu_seconds, 60.0))
-    steps = args.steps
-    ms = 2.0 * M_PER_RANK * N_DIM * K_DIM / (tflops * 1e12) * 1e3
-    line = {"impl": "reference", "metric": METRIC, "value": tflops, "unit": "TFLOPS", "n_gpus": args.gpus,
-            "steps": steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+    tfl, cores, desc = cpu_oracle_sample(min(args.cpu_seconds, 60.0))
+    ms = 2.0 * M3 * N3 * K3 / (tfl * 1e12) * 1e3
+    line = {"impl": "reference", "metric": METRIC, "value": tfl, "unit": "TFLOPS", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "cfg3: BF16 ABFT GEMM 8192^3 (tile-sampled CPU oracle)", "M": M_PER_RANK,
-                       "N": N_DIM, "K": K_DIM},
-            "cpu_baseline": {"value": tflops, "unit": "TFLOPS", "cores": cores, "kind": "oracle", "sample": desc},
-            "e2e": {"value": tflops, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "config": {"workload": "cfg3: BF16 ABFT GEMM 8192^3 (tile-sampled CPU oracle)", "M": M3, "N": N3, "K": K3},
+            "cpu_baseline": {"value": tfl, "unit": "TFLOPS", "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": {"value": tfl, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "note": "the reference arm is the paper-derived CPU oracle (no reference implementation exists)"}
     print(json.dumps(line), flush=True)
     return 0
@@ -113,14 +130,14 @@ class ClockSampler:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                          "-lms", "50"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                                          "-lms", "20"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.12)
+        time.sleep(0.05)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -149,112 +166,193 @@ class ClockSampler:
                 "samples": len(loaded), "power_w_max": max(r[2] for r in rows), "reasons": sorted(reasons)}
 
 
-# ------------------------------------------------------------------ ours ---
-def run_ours(args):
+# ------------------------------------------------------------- harness ---
+class Harness:
+    """Process group, barrier, max over ranks, and the timing loops."""
+
+    def __init__(self, backend: str):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        ndev = torch.cuda.device_count()
+        # backend gloo: validate the N > 1 host logic with several ranks on one GPU
+        torch.cuda.set_device(self.local % ndev)
+        self.dev = torch.device("cuda", self.local % ndev)
+        if self.world > 1:
+            kw = {"device_id": self.dev} if backend == "nccl" else {}
+            dist.init_process_group(backend, **kw)
+        self.backend = backend
+        self.stream = torch.cuda.current_stream()
+
+    def barrier(self):
+        if self.world > 1:
+            if self.backend == "nccl":
+                self.dist.barrier(device_ids=[self.dev.index])
+            else:
+                self.dist.barrier()
+
+    def max_over_ranks(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device=self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def ev(self):
+        return self.torch.cuda.Event(enable_timing=True)
+
+    def timed(self, fn_list, warm: int = 0) -> float:
+        """ms per call of fn_list (run in order), max over ranks."""
+        torch = self.torch
+        for i in range(warm):
+            fn_list[i % len(fn_list)]()
+        self.barrier(); torch.cuda.synchronize()
+        e0, e1 = self.ev(), self.ev()
+        e0.record(self.stream)
+        for fn in fn_list:
+            fn()
+        e1.record(self.stream)
+        e1.synchronize()
+        self.barrier(); torch.cuda.synchronize()
+        return self.max_over_ranks(e0.elapsed_time(e1) / len(fn_list))
+
+    def interleave(self, configs: dict, n_calls: int, after_warmup=None) -> dict:
+        """Every configuration timed CALL BY CALL in one loop (one event pair per
+        call on the launch stream, median per configuration) in a fresh seeded
+        random order every call, so no configuration keeps a fixed position or a
+        fixed predecessor (under the B200's power cap, back-to-back blocks of one
+        configuration drift apart by tens of percent, and a call right after a
+        long, power-hungry one runs at lower clocks)."""
+        import random
+        torch = self.torch
+        names = list(configs)
+        rnd = random.Random(230501024)
+        evs = {k: [(self.ev(), self.ev()) for _ in range(n_calls)] for k in names}
+        for k in names:
+            configs[k](0)
+        self.barrier(); torch.cuda.synchronize()
+        if after_warmup is not None:
+            after_warmup()
+        for i in range(n_calls):
+            order = names[:]
+            rnd.shuffle(order)
+            for k in order:
+                evs[k][i][0].record(self.stream)
+                configs[k](i)
+                evs[k][i][1].record(self.stream)
+        torch.cuda.synchronize()
+        return {k: self.max_over_ranks(statistics.median(a.elapsed_time(b) for a, b in evs[k])) for k in names}
+
+
+class Faults:
+    """Seeded fault sites (bit 30 of the FP32 accumulator: a flip that is always
+    far above the threshold) over the check tiles of a plan."""
+
+    def __init__(self, plan, M, N, K, seed):
+        import numpy as np
+        from paper_2305_01024_b200 import ftgemm as F
+        self.F, self.p, self.M, self.N, self.K = F, plan, M, N, K
+        self.rng = np.random.default_rng(seed)
+        self.tiles = plan.tiles_m * plan.tiles_n
+
+    def _in_tile(self, t: int, salt: int = 0):
+        p = self.p
+        ti, tj = divmod(int(t), p.tiles_n)
+        bm = min(p.check_tile_m, self.M - ti * p.check_tile_m)
+        bn = min(p.check_tile_n, self.N - tj * p.check_tile_n)
+        return (ti * p.check_tile_m + int(self.rng.integers(bm)), tj * p.check_tile_n + int(self.rng.integers(bn)),
+                int(self.rng.integers(self.K)), 30, self.F.INJ_FLIP, self.F.TGT_ACC, 0.0)
+
+    def site(self):
+        return self._in_tile(int(self.rng.integers(self.tiles)))
+
+    def per_call(self, n: int):
+        """n faults in n distinct check tiles (n = -1: one in every tile)."""
+        tiles = range(self.tiles) if n < 0 else self.rng.choice(self.tiles, size=n, replace=False)
+        return [self._in_tile(t) for t in tiles]
+
+    def schedule(self, rate: float, nsteps: int, step_ms: float, at_least_one: bool = False):
+        """rate errors/min over nsteps steps of step_ms: round(rate x time)
+        faults (at least one if asked) at evenly spaced steps."""
+        n = int(round(rate * nsteps * step_ms / 60000.0))
+        if at_least_one:
+            n = max(1, n)
+        out = [[] for _ in range(nsteps)]
+        for i in range(n):
+            out[int((i + 0.5) * nsteps / n)].append(self.site())
+        return out, n
+
+
+def roofline(peaks, kind, achieved_tflops, window_s, clk, traffic, kernel, flops_launch, tf32=False):
+    """Tensor-bound roofline of the fused kernel.  The peak is the measured
+    figure of the clock regime the timed region ran in: burst (best-of-10
+    cuBLAS) for a region shorter than BURST_WINDOW_S, sustained (cuBLAS back to
+    back, power-capped) for a longer one; both fractions are reported."""
+    scale = 0.5 if tf32 else 1.0                        # TF32 dense = BF16 x 1/2 (guide's nominal ratio)
+    burst = peaks["bf16_tflops"] * scale
+    sus = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) * scale
+    regime = "burst" if window_s < BURST_WINDOW_S else "sustained"
+    peak = burst if regime == "burst" else sus
+    return {"bound": "tensor", "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved_tflops / peak, "traffic": traffic, "kernel": kernel,
+            "peak_kind": f"{kind} {'tf32 (bf16 x 1/2)' if tf32 else 'bf16'} {regime} "
+                         f"(timed region {window_s * 1e3:.0f} ms, median SM clock {clk.get('sm_mhz')} MHz)",
+            "algorithmic_flops_per_launch": flops_launch,
+            "peak_burst": burst, "frac_burst": achieved_tflops / burst,
+            "peak_sustained": sus, "frac_sustained": achieved_tflops / sus}
+
+
+def ncu_traffic(key: str):
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            return json.load(open(tp)).get(key)
+        except Exception:
+            return None
+    return None
+
+
+# ----------------------------------------------------------- N = 1: cfg3 ---
+def run_single(args, H):
     import numpy as np
     import torch
-    import torch.distributed as dist
 
     import synth
     from paper_2305_01024_b200 import ftgemm as F
-    from paper_2305_01024_b200 import distributed as D
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    stream = torch.cuda.current_stream()
-    Mr, N, K = M_PER_RANK, N_DIM, K_DIM
-    flops_rank = 2.0 * Mr * N * K
-
-    # ---- inputs: A block by global row index, B on rank 0 + one broadcast ----
-    A_h = synth.matrix(synth.BASE_SEED + synth.SEED_A, Mr * world, K, dtype="bf16", r0=rank * Mr, r1=(rank + 1) * Mr)
-    A = synth.to_torch(A_h, "bf16").to(dev)
-    del A_h
-    g = F.FTGemm("bf16", Mr, N, K, device=dev)
+    dev, stream = H.dev, H.stream
+    M, N, K = M3, N3, K3
+    flops = 2.0 * M * N * K
+    A = synth.matrix_torch(synth.BASE_SEED + synth.SEED_A, M, K, dtype="bf16", device=dev)
+    B = synth.matrix_torch(synth.BASE_SEED + synth.SEED_B, K, N, dtype="bf16", device=dev)
+    C = torch.empty(M, N, dtype=torch.bfloat16, device=dev)
+    g = F.FTGemm("bf16", M, N, K, device=dev)
     pl = g.plan
-    bcast_ms = 0.0
-    if rank == 0:
-        B = synth.to_torch(synth.matrix(synth.BASE_SEED + synth.SEED_B, K, N, dtype="bf16"), "bf16").to(dev)
-    else:
-        B = torch.empty(K, N, dtype=torch.bfloat16, device=dev)
-    if world > 1:
-        bcast_ms = D.broadcast_b(g, B, src=0)
-    C = torch.empty(Mr, N, dtype=torch.bfloat16, device=dev)
-
-    # ---- seeded fault schedule at a rate (errors / minute) ----
-    rng = np.random.default_rng(synth.BASE_SEED + synth.SEED_PLAN + rank)
-    tiles_total = pl.tiles_m * pl.tiles_n
-
-    def site():
-        t = int(rng.integers(tiles_total))
-        ti, tj = divmod(t, pl.tiles_n)
-        bm = min(pl.check_tile_m, Mr - ti * pl.check_tile_m)
-        bn = min(pl.check_tile_n, N - tj * pl.check_tile_n)
-        return (ti * pl.check_tile_m + int(rng.integers(bm)), tj * pl.check_tile_n + int(rng.integers(bn)),
-                int(rng.integers(K)), 30, F.INJ_FLIP, F.TGT_ACC, 0.0)
-
-    def schedule(rate, nsteps, step_ms):
-        """rate errors/min over nsteps steps of step_ms: round(rate x time)
-        faults at evenly spaced steps, seeded sites"""
-        n = int(round(rate * nsteps * step_ms / 60000.0))
-        out = [[] for _ in range(nsteps)]
-        for i in range(n):
-            out[int((i + 0.5) * nsteps / n)].append(site())
-        return out
+    fl = Faults(pl, M, N, K, synth.BASE_SEED + synth.SEED_PLAN)
 
     def step(inj=()):
         g.encode(A, B)
         g.run(A, B, C, ft_level=F.FT_CORRECT, injections=inj)
 
-    def barrier():
-        if world > 1:
-            dist.barrier(device_ids=[local])
-
-    def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    def timed(fn_list, warm: int):
-        """fn_list: per-step callables; returns ms/step (max over ranks)."""
-        for i in range(warm):
-            fn_list[i % len(fn_list)]()
-        barrier(); torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for fn in fn_list:
-            fn()
-        e1.record(stream)
-        e1.synchronize()
-        barrier(); torch.cuda.synchronize()
-        return max_over_ranks(e0.elapsed_time(e1) / len(fn_list))
-
-    # ---- warm-up + rough step time for the schedule ----
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
-    g.reset()
-    est = timed([step] * 5, 0)
+    est = H.timed([step] * 5)
 
-    # ---- main timed region: K steps at ERRORS_PER_MIN, kernel events per step ----
-    sched = schedule(ERRORS_PER_MIN, args.steps, est)
-    n_injected = sum(len(s) for s in sched)
-    g.reset()
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    # ---- main timed region: K steps, faults at ERRORS_PER_MIN (>= 1), kernel events ----
+    sched, n_injected = fl.schedule(ERRORS_PER_MIN, args.steps, est, at_least_one=True)
+    kev = [(H.ev(), H.ev()) for _ in range(args.steps)]
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     g.reset()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
-    barrier(); torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(dev.index)
+    H.barrier(); torch.cuda.synchronize()
+    e0, e1 = H.ev(), H.ev()
     e0.record(stream)
     for i in range(args.steps):
         g.encode(A, B)
@@ -263,232 +361,423 @@ def run_ours(args):
         kev[i][1].record(stream)
     e1.record(stream)
     e1.synchronize()
-    barrier(); torch.cuda.synchronize()
+    H.barrier(); torch.cuda.synchronize()
     clk = clocks.stop()
-    ms_step = max_over_ranks(e0.elapsed_time(e1) / args.steps)
-    ms_kernel = max_over_ranks(sum(a.elapsed_time(b) for a, b in kev) / args.steps)
-    counts, events = g.report()
+    ms_step = e0.elapsed_time(e1) / args.steps
+    ms_kernel = sum(a.elapsed_time(b) for a, b in kev) / args.steps
+    counts, _ = g.report()
     ok_faults = counts["corrected"] == n_injected and counts["uncorrectable"] == 0 and counts["checksum_only"] == 0
-    value = flops_rank * world / (ms_step * 1e-3) / 1e12
-    launches_per_step = 2   # encode_ab (both operands, one launch), fused GEMM (tickets reset by cudaMemsetAsync, not kernels)
+    window_s = ms_step * args.steps * 1e-3
+    peaks, kind = load_peaks()
+    roof = roofline(peaks, kind, tflops(flops, ms_kernel), window_s, clk,
+                    ncu_traffic("fused_gemm_bf16_8192_bytes_per_launch"), "tc_ftgemm_kernel<bf16,256,FT,2>", flops)
+    roof["kernel_share_of_step"] = ms_kernel / ms_step
 
     extra = {}
     if not args.no_sweep:
-        reps, rounds = max(20, args.steps), 3
-        stress = []
-        for ti in range(pl.tiles_m):
-            for tj in range(pl.tiles_n):
-                r = ti * pl.check_tile_m + (ti * 7 + tj) % min(pl.check_tile_m, Mr - ti * pl.check_tile_m)
-                c = tj * pl.check_tile_n + (tj * 5 + ti) % min(pl.check_tile_n, N - tj * pl.check_tile_n)
-                stress.append((r, c, (ti * 131 + tj * 17) % K, 30, F.INJ_FLIP, F.TGT_ACC, 0.0))
-        one = [site()]
-        n_calls = reps * rounds
-        # the injection-rate sweep: one seeded schedule per rate, call i of that
-        # rate's configuration uses step i of its schedule
-        rate_sched = {str(int(r)): schedule(r, n_calls, est) for r in SWEEP_RATES}
-        configs = {
-            "ft_off": lambda i: g.run(A, B, C, ft_level=F.FT_OFF),
-            "cublas": lambda i: torch.matmul(A, B, out=C),
-            "ft_run": lambda i: g.run(A, B, C, ft_level=F.FT_CORRECT),
-            "ft_step": lambda i: step(),
-            "encode": lambda i: g.encode(A, B),
-            "encode_a": lambda i: g.encode(A, None, which=1),
-            "one_fault_run": lambda i: g.run(A, B, C, ft_level=F.FT_CORRECT, injections=one),
-            # the paper's comparison scheme (Ding 2011): cuBLAS GEMMs + separate verification
-            "nonfused_step": lambda i: (g.encode(A, B, which=3 | 4), g.run_nonfused(A, B, C, ft_level=F.FT_CORRECT)),
-            "nonfused_run": lambda i: g.run_nonfused(A, B, C, ft_level=F.FT_CORRECT),
-            # online verification after every K_s = 256 step: 32 checks per tile
-            "online_ks256_run": lambda i: g.run_online(A, B, C, ks=256),
-            "online_ks2048_run": lambda i: g.run_online(A, B, C, ks=2048),
-        }
-        for key, sc in rate_sched.items():
-            configs["rate_" + key] = (lambda sc_: (lambda i: step(sc_[i])))(sc)
-        # every configuration timed CALL BY CALL in one interleaved loop (one event
-        # pair per call on the launch stream, median per configuration), so all
-        # of them -- the rate sweep included -- see the same clock / power state:
-        # under the B200's power cap, back-to-back blocks of one configuration
-        # drift apart by tens of percent
-        names = list(configs)
-        evs = {k: [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                   for _ in range(n_calls)] for k in names}
-        for k in names:
-            if not k.startswith("rate_"):
-                configs[k](0)
-        barrier(); torch.cuda.synchronize()
-        g.reset()
-        for i in range(n_calls):
-            for k in names:
-                evs[k][i][0].record(stream)
-                configs[k](i)
-                evs[k][i][1].record(stream)
-        torch.cuda.synchronize()
-        samples = {k: [a.elapsed_time(b) for a, b in evs[k]] for k in names}
-        cs_sweep, _ = g.report(0)
-        rate_inj = {k: sum(len(x) for x in sc) for k, sc in rate_sched.items()}
-        med = {k: max_over_ranks(statistics.median(v)) for k, v in samples.items()}
-        g.reset()
-        t_stress = timed([lambda: g.run(A, B, C, ft_level=F.FT_CORRECT, injections=stress)] * 3, 1)
-        cs, _ = g.report(0)
-        stress_ok = cs["corrected"] == 4 * len(stress) and cs["uncorrectable"] == 0
-        t_off, t_cub = med["ft_off"], med["cublas"]
-        sweep = {}
-        for rate in SWEEP_RATES:
-            key = str(int(rate))
-            t = med["rate_" + key]
-            sweep[key] = {"ms_per_step": t, "tflops": flops_rank * world / (t * 1e-3) / 1e12,
-                          "steps": n_calls, "injected": rate_inj[key],
-                          "overhead_vs_ft_off_pct": 100.0 * (t - t_off) / t_off,
-                          "overhead_vs_cublas_pct": 100.0 * (t - t_cub) / t_cub,
-                          "run_only_overhead_vs_ft_off_pct": 100.0 * (t - med["encode"] - t_off) / t_off}
-        # every injected fault of the sweep (and of the one-fault comparator) corrected
-        n_sweep_inj = sum(rate_inj.values()) + n_calls
-        sweep_ok = (cs_sweep["corrected"] == n_sweep_inj and cs_sweep["uncorrectable"] == 0
-                    and cs_sweep["checksum_only"] == 0)
-        # ---- online vs offline ABFT: per-tile error rate gamma0 ----
-        offline = {}
-        t_rows = timed([lambda: g.run(A, B, C, ft_level=F.FT_DETECT_ROWS)] * reps, 2)
-
-        def draw(g0):
-            hit = np.nonzero(rng.random(tiles_total) < g0)[0]
-            out = []
-            for t in hit:
-                ti, tj = divmod(int(t), pl.tiles_n)
-                out.append((ti * pl.check_tile_m + int(rng.integers(min(pl.check_tile_m, Mr - ti * pl.check_tile_m))),
-                            tj * pl.check_tile_n + int(rng.integers(min(pl.check_tile_n, N - tj * pl.check_tile_n))),
-                            int(rng.integers(K)), 30, F.INJ_FLIP, F.TGT_ACC, 0.0))
-            return out
-        calls, max_runs = 20, 8
-        for g0 in OFFLINE_GAMMA0:
-            cm = F.cost_model(g0, tiles_total)
-            on_inj = [draw(g0) for _ in range(calls)]
-            t_on = timed([(lambda inj: (lambda: step(inj)))(x) for x in on_inj], 2)
-            execs = []
-            e0o, e1o = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            e0o.record(stream)
-            for _ in range(calls):
-                inj, run_of = [], []
-                for r in range(max_runs):
-                    d = draw(g0)
-                    inj += d
-                    run_of += [r] * len(d)
-                g.encode(A, B)
-                n_exec, clean = g.run_offline(A, B, C, injections=inj, inj_run=run_of, max_runs=max_runs)
-                execs.append(n_exec)
-            e1o.record(stream)
-            e1o.synchronize()
-            t_off_call = e0o.elapsed_time(e1o) / calls
-            offline[f"{g0:g}"] = {
-                "gamma": cm["gamma"], "tiles": tiles_total, "calls": calls,
-                "online_ms_per_call": t_on, "online_faults": sum(len(x) for x in on_inj),
-                "offline_ms_per_call": t_off_call, "offline_mean_executions": float(np.mean(execs)),
-                "offline_restart_model_executions": 1.0 / (1.0 - cm["gamma"]),
-                "paper_model_offline_expected_runs": cm["offline_expected_runs"],
-                "paper_model_offline_ms": med["encode"] + cm["offline_expected_runs"] * t_rows,
-                "offline_vs_online_pct": 100.0 * (t_off_call - t_on) / t_on}
-        g.reset()
-        g.encode(A, B)                               # restore the fused path's encoded operand
-        extra = {
-            "nonfused_step_ms": med["nonfused_step"], "nonfused_run_ms": med["nonfused_run"],
-            "online_ks256_run_ms": med["online_ks256_run"], "online_ks2048_run_ms": med["online_ks2048_run"],
-            "fused_speedup_vs_nonfused_pct": 100.0 * (med["nonfused_step"] - med["ft_step"]) / med["ft_step"],
-            "detect_rows_run_ms": t_rows,
-            "detect_rows_overhead_vs_ft_off_pct": 100.0 * (t_rows - med["ft_off"]) / med["ft_off"],
-            "online_vs_offline": offline,
-            "ft_off_ms": t_off, "ft_off_tflops": flops_rank * world / (t_off * 1e-3) / 1e12,
-            "cublas_ms": t_cub, "cublas_tflops": flops_rank * world / (t_cub * 1e-3) / 1e12,
-            "ft_step_ms": med["ft_step"], "ft_run_only_ms": med["ft_run"],
-            "encode_ms": med["encode"], "encode_a_ms": med["encode_a"],
-            "encode_gbs": (2 * Mr * K + 2 * K * N + 2 * K * pl.tiles_n * pl.bn) / (med["encode"] * 1e-3) / 1e9,
-            "encode_hbm_frac": (2 * Mr * K + 2 * K * N + 2 * K * pl.tiles_n * pl.bn) / (med["encode"] * 1e-3) / 1e9
-            / load_peaks()[0]["hbm_gbs"],
-            "overhead_vs_ft_off_pct": 100.0 * (med["ft_step"] - t_off) / t_off,
-            "overhead_vs_cublas_pct": 100.0 * (med["ft_step"] - t_cub) / t_cub,
-            "overhead_run_only_vs_ft_off_pct": 100.0 * (med["ft_run"] - t_off) / t_off,
-            "overhead_pre_encoded_B_vs_ft_off_pct": 100.0 * (med["ft_run"] + med["encode_a"] - t_off) / t_off,
-            "one_fault_call_ms": med["one_fault_run"], "stress_one_fault_per_tile_ms": t_stress,
-            "stress_faults": len(stress), "stress_all_corrected": bool(stress_ok),
-            "rate_sweep_errors_per_min": sweep, "rate_sweep_all_corrected": bool(sweep_ok),
-            "comparator_rounds": rounds, "comparator_reps": reps,
-        }
+        extra.update(cfg3_comparators(args, H, g, A, B, C, fl, est, step))
+        del C
+        extra["cfg2_8192"] = cfg2_section(args, H, peaks)
+        extra["cfg4_shapes"] = cfg4_section(args, H, peaks)
+        extra["cfg5_1gpu_steady_state"] = cfg5_one_gpu(args, H)
+        C = torch.empty(M, N, dtype=torch.bfloat16, device=dev)
 
     # ---- e2e: public API with host buffers, H2D inputs + D2H result per step ----
-    A_pin = A.cpu().pin_memory(); B_pin = B.cpu().pin_memory()
-    C_pin = torch.empty(Mr, N, dtype=torch.bfloat16).pin_memory()
-    e2e_steps = max(3, min(args.steps, 10))
+    e2e = e2e_pipeline(H, g, A, B, C, args.steps, flops)
 
-    def e2e_step():
-        A.copy_(A_pin, non_blocking=True)
-        B.copy_(B_pin, non_blocking=True)
+    tfl, cores, desc = cpu_oracle_sample(args.cpu_seconds)
+    line = {"metric": METRIC, "value": tflops(flops, ms_step), "unit": "TFLOPS", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "cfg3: BF16 tcgen05 ABFT GEMM 8192^3 (encode A + encode B + fused FT GEMM, CORRECT)",
+                       "M": M, "N": N, "K": K, "alpha": 1.0, "beta": 0.0, "ft_level": "CORRECT",
+                       "errors_per_min_target": ERRORS_PER_MIN,
+                       "errors_per_min_effective": n_injected / (window_s / 60.0),
+                       "check_tile": [pl.check_tile_m, pl.check_tile_n], "mma_tile": [pl.bm, pl.bn, pl.bk],
+                       "cta_group": pl.cta_group, "l2": "inputs larger than L2 (A+B 256 MiB), no flush",
+                       "parallelism": "single"},
+            "faults": {"injected": n_injected, **{k: v for k, v in counts.items() if v}, "all_corrected": ok_faults},
+            "roofline": roof,
+            "cpu_baseline": {"value": tfl, "unit": "TFLOPS", "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": e2e, "gpu_launches": 2 * args.steps, "clocks": clk, "kernel_ms": ms_kernel, **extra}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cfg3_comparators(args, H, g, A, B, C, fl, est, step):
+    """Comparators of the cfg3 step, the injection-rate and faults-per-call
+    sweeps, all timed call by call in one rotating interleaved loop."""
+    import numpy as np
+    import torch
+    from paper_2305_01024_b200 import ftgemm as F
+    M, N, K = M3, N3, K3
+    flops = 2.0 * M * N * K
+    pl = g.plan
+    reps, rounds = max(20, args.steps), 3
+    n_calls = reps * rounds
+    rate_sched = {str(int(r)): fl.schedule(r, n_calls, est)[0] for r in SWEEP_RATES}
+    fpc_lists = {str(n) if n >= 0 else "all_tiles": [fl.per_call(n) for _ in range(4 if n >= 0 else 1)]
+                 for n in FAULTS_PER_CALL}
+    configs = {
+        "ft_off": lambda i: g.run(A, B, C, ft_level=F.FT_OFF),
+        "cublas": lambda i: torch.matmul(A, B, out=C),
+        "ft_run": lambda i: g.run(A, B, C, ft_level=F.FT_CORRECT),
+        "ft_step": lambda i: step(),
+        "ft_step_dup": lambda i: step(),            # identical to ft_step: the loop's noise floor
+        "encode": lambda i: g.encode(A, B),
+        "encode_a": lambda i: g.encode(A, None, which=1),
+        "step_b_resident": lambda i: (g.encode(A, None, which=1), g.run(A, B, C, ft_level=F.FT_CORRECT)),
+        "detect_rows_run": lambda i: g.run(A, B, C, ft_level=F.FT_DETECT_ROWS),
+        # the paper's comparison scheme (Ding 2011): cuBLAS GEMMs + separate verification
+        "nonfused_step": lambda i: (g.encode(A, B, which=3 | 4), g.run_nonfused(A, B, C, ft_level=F.FT_CORRECT)),
+        "nonfused_run": lambda i: g.run_nonfused(A, B, C, ft_level=F.FT_CORRECT),
+        # online verification after every K_s = 256 step (PAPER.md:515): 32 checks per tile
+        "online_ks256_run": lambda i: g.run_online(A, B, C, ks=256),
+        "online_ks2048_run": lambda i: g.run_online(A, B, C, ks=2048),
+    }
+    for key, sc in rate_sched.items():
+        configs["rate_" + key] = (lambda sc_: (lambda i: step(sc_[i])))(sc)
+    for key, lists in fpc_lists.items():
+        configs["fpc_" + key] = (lambda ls: (lambda i: step(ls[i % len(ls)])))(lists)
+    med = H.interleave(configs, n_calls, after_warmup=g.reset)
+    cs_sweep, _ = g.report(0)
+    g.reset()
+    g.encode(A, B)                               # restore the fused path's encoded operand (nonfused re-encodes)
+    n_expect = sum(sum(len(x) for x in sc) for sc in rate_sched.values())
+    n_expect += sum(sum(len(ls[i % len(ls)]) for i in range(n_calls)) for ls in fpc_lists.values())
+    sweep_ok = (cs_sweep["corrected"] == n_expect and cs_sweep["uncorrectable"] == 0 and cs_sweep["checksum_only"] == 0)
+    t_off, t_cub = med["ft_off"], med["cublas"]
+    ov = lambda t, base: 100.0 * (t - base) / base            # noqa: E731
+    sweep = {}
+    for rate in SWEEP_RATES:
+        key = str(int(rate))
+        t = med["rate_" + key]
+        sweep[key] = {"ms_per_step": t, "tflops": tflops(flops, t), "calls": n_calls,
+                      "injected": sum(len(x) for x in rate_sched[key]),
+                      "overhead_vs_ft_off_pct": ov(t, t_off), "overhead_vs_cublas_pct": ov(t, t_cub)}
+    fpc = {}
+    for key, lists in fpc_lists.items():
+        t = med["fpc_" + key]
+        n = len(lists[0])
+        fpc[key] = {"faults_per_call": n, "ms_per_step": t, "tflops": tflops(flops, t),
+                    "errors_per_min_at_this_step_time": n * 60000.0 / t,
+                    "overhead_vs_ft_off_pct": ov(t, t_off), "overhead_vs_cublas_pct": ov(t, t_cub),
+                    "overhead_vs_0_faults_pct": ov(t, med["fpc_0"])}
+    # ---- online vs offline ABFT (PAPER.md:571-583): per-tile error rate gamma0 ----
+    offline = {}
+    rng = np.random.default_rng(synth_seed(7))
+    tiles_total = pl.tiles_m * pl.tiles_n
+
+    def draw(g0):
+        hit = np.nonzero(rng.random(tiles_total) < g0)[0]
+        return [fl._in_tile(int(t)) for t in hit]
+    calls, max_runs = 20, 8
+    for g0 in OFFLINE_GAMMA0:
+        cm = F.cost_model(g0, tiles_total)
+        on_inj = [draw(g0) for _ in range(calls)]
+        t_on = H.timed([(lambda inj: (lambda: step(inj)))(x) for x in on_inj], 2)
+        execs = []
+        e0, e1 = H.ev(), H.ev()
+        torch.cuda.synchronize()
+        e0.record(H.stream)
+        for _ in range(calls):
+            inj, run_of = [], []
+            for r in range(max_runs):
+                d = draw(g0)
+                inj += d
+                run_of += [r] * len(d)
+            g.encode(A, B)
+            n_exec, _clean = g.run_offline(A, B, C, injections=inj, inj_run=run_of, max_runs=max_runs)
+            execs.append(n_exec)
+        e1.record(H.stream)
+        e1.synchronize()
+        t_off_call = e0.elapsed_time(e1) / calls
+        offline[f"{g0:g}"] = {
+            "gamma": cm["gamma"], "tiles": tiles_total, "calls": calls,
+            "online_ms_per_call": t_on, "online_faults": sum(len(x) for x in on_inj),
+            "offline_ms_per_call": t_off_call, "offline_mean_executions": float(np.mean(execs)),
+            "offline_restart_model_executions": 1.0 / (1.0 - cm["gamma"]),
+            "paper_model_offline_expected_runs": cm["offline_expected_runs"],
+            "paper_model_offline_ms": med["encode"] + cm["offline_expected_runs"] * med["detect_rows_run"],
+            "offline_vs_online_pct": ov(t_off_call, t_on)}
+    g.reset()
+    enc_bytes = 2 * M * K + 2 * K * N + 2 * K * pl.tiles_n * pl.bn      # A, B read; B^r written
+    peaks, _ = load_peaks()
+    return {
+        "comparators_ms": med, "comparator_calls": n_calls, "comparator_order": "seeded random permutation per call",
+        "identical_config_spread_pct": 100.0 * abs(med["ft_step"] - med["ft_step_dup"]) /
+                                       (0.5 * (med["ft_step"] + med["ft_step_dup"])),
+        "ft_off_tflops": tflops(flops, t_off), "cublas_tflops": tflops(flops, t_cub),
+        "ft_step_tflops": tflops(flops, med["ft_step"]),
+        "overhead_vs_ft_off_pct": ov(med["ft_step"], t_off),
+        "overhead_vs_cublas_pct": ov(med["ft_step"], t_cub),
+        "overhead_b_resident_vs_ft_off_pct": ov(med["step_b_resident"], t_off),
+        "overhead_run_only_vs_ft_off_pct": ov(med["ft_run"], t_off),
+        "encode_gbs": enc_bytes / (med["encode"] * 1e-3) / 1e9,
+        "encode_hbm_frac": enc_bytes / (med["encode"] * 1e-3) / 1e9 / peaks["hbm_gbs"],
+        "encode_algorithmic_hbm_frac": (2 * M * K + 2 * K * N) / (med["encode"] * 1e-3) / 1e9 / peaks["hbm_gbs"],
+        "fused_speedup_vs_nonfused_pct": ov(med["nonfused_step"], med["ft_step"]),
+        "detect_rows_overhead_vs_ft_off_pct": ov(med["detect_rows_run"], t_off),
+        "rate_sweep_errors_per_min": sweep, "faults_per_call_sweep": fpc,
+        "sweeps_all_corrected": bool(sweep_ok), "online_vs_offline": offline,
+    }
+
+
+def synth_seed(k: int) -> int:
+    import synth
+    return synth.BASE_SEED + synth.SEED_PLAN + 100 + k
+
+
+def cfg2_section(args, H, peaks):
+    """cfg2 at 8192^3 with FP32 operands: the paper's precision (FP32 SIMT, one
+    fmaf per k) and TF32 tcgen05 -- FT step, FT run, FT off, cuBLAS."""
+    import torch
+
+    import synth
+    from paper_2305_01024_b200 import ftgemm as F
+    M = N = K = 8192
+    flops = 2.0 * M * N * K
+    A = synth.matrix_torch(synth.BASE_SEED + 31, M, K, device=H.dev)
+    B = synth.matrix_torch(synth.BASE_SEED + 32, K, N, device=H.dev)
+    C = torch.empty(M, N, device=H.dev)
+    out = {}
+    for dt, reps in (("f32_simt", 6), ("tf32", 30)):
+        g = F.FTGemm(dt, M, N, K, device=H.dev)
+        tf32 = dt == "tf32"
+
+        def cub(i, tf32=tf32):
+            torch.backends.cuda.matmul.allow_tf32 = tf32
+            torch.matmul(A, B, out=C)
+        cfg = {"ft_step": lambda i, g=g: (g.encode(A, B), g.run(A, B, C)),
+               "ft_run": lambda i, g=g: g.run(A, B, C),
+               "ft_off": lambda i, g=g: g.run(A, B, C, ft_level=F.FT_OFF),
+               "cublas": cub}
         g.encode(A, B)
+        med = H.interleave(cfg, reps)
+        torch.backends.cuda.matmul.allow_tf32 = False
+        cnt, _ = g.report(0)
+        peak = SIMT_FFMA_PEAK if not tf32 else peaks["bf16_tflops"] / 2
+        out[dt] = {k + "_ms": v for k, v in med.items()}
+        out[dt].update({k + "_tflops": tflops(flops, v) for k, v in med.items()})
+        out[dt].update({"overhead_step_vs_ft_off_pct": 100.0 * (med["ft_step"] - med["ft_off"]) / med["ft_off"],
+                        "overhead_run_vs_ft_off_pct": 100.0 * (med["ft_run"] - med["ft_off"]) / med["ft_off"],
+                        "overhead_step_vs_cublas_pct": 100.0 * (med["ft_step"] - med["cublas"]) / med["cublas"],
+                        "ft_run_frac_of_peak": tflops(flops, med["ft_run"]) / peak,
+                        "peak_tflops": peak, "peak_kind": "FP32 FFMA (148 SM x 128 lanes x 2 x 1.965 GHz)" if not tf32
+                        else "measured bf16 burst x 1/2", "tiles_detected_fault_free": cnt["tiles_detected"],
+                        "calls": reps})
+        del g
+    return out
+
+
+def cfg4_section(args, H, peaks):
+    """cfg4 irregular shapes (BF16; HBM-bound): FT run / FT off / cuBLAS and the
+    HBM fraction of the FT run on the algorithmic bytes (MK + KN + MN) x 2."""
+    import torch
+
+    import synth
+    from paper_2305_01024_b200 import ftgemm as F
+    out = {}
+    shapes = {"16384x16384x128": (16384, 16384, 128), "128x16384x16384": (128, 16384, 16384),
+              "16384x128x16384": (16384, 128, 16384)}
+    for name, (M, N, K) in shapes.items():
+        A = synth.matrix_torch(synth.BASE_SEED + 21, M, K, dtype="bf16", device=H.dev)
+        B = synth.matrix_torch(synth.BASE_SEED + 22, K, N, dtype="bf16", device=H.dev)
+        C = torch.empty(M, N, dtype=torch.bfloat16, device=H.dev)
+        g = F.FTGemm("bf16", M, N, K, device=H.dev)
+        g.encode(A, B)
+        med = H.interleave({"ft_step": lambda i: (g.encode(A, B), g.run(A, B, C)),
+                            "ft_run": lambda i: g.run(A, B, C),
+                            "ft_off": lambda i: g.run(A, B, C, ft_level=F.FT_OFF),
+                            "cublas": lambda i: torch.matmul(A, B, out=C)}, 30)
+        byts = 2.0 * (M * K + K * N + M * N)
+        out[name] = {**{k + "_ms": v for k, v in med.items()},
+                     "ft_run_hbm_frac": byts / (med["ft_run"] * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                     "ft_off_hbm_frac": byts / (med["ft_off"] * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                     "cublas_hbm_frac": byts / (med["cublas"] * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                     "run_over_off": med["ft_run"] / med["ft_off"], "step_over_run": med["ft_step"] / med["ft_run"],
+                     "tile_class": [g.plan.bn, g.plan.cta_group]}
+        del A, B, C, g
+    return out
+
+
+def cfg5_one_gpu(args, H):
+    """The full cfg5 problem on this one GPU in the steady state of the
+    partitioned runs (B resident and pre-encoded; step = encode A + FT GEMM):
+    the N = 1 point of the cfg5 strong-scaling curve."""
+    import torch
+
+    import synth
+    from paper_2305_01024_b200 import ftgemm as F
+    flops = 2.0 * M5 * N5 * K5
+    A = synth.matrix_torch(synth.BASE_SEED + 11, M5, K5, dtype="bf16", device=H.dev)
+    B = synth.matrix_torch(synth.BASE_SEED + 12, K5, N5, dtype="bf16", device=H.dev)
+    C = torch.empty(M5, N5, dtype=torch.bfloat16, device=H.dev)
+    g = F.FTGemm("bf16", M5, N5, K5, device=H.dev)
+    g.encode(None, B, which=2)
+    med = H.interleave({"step": lambda i: (g.encode(A, None, which=1), g.run(A, B, C)),
+                        "ft_off": lambda i: g.run(A, B, C, ft_level=F.FT_OFF),
+                        "cublas": lambda i: torch.matmul(A, B, out=C)}, 5)
+    cnt, _ = g.report(0)
+    out = {**{k + "_ms": v for k, v in med.items()}, "step_tflops": tflops(flops, med["step"]),
+           "overhead_vs_ft_off_pct": 100.0 * (med["step"] - med["ft_off"]) / med["ft_off"],
+           "overhead_vs_cublas_pct": 100.0 * (med["step"] - med["cublas"]) / med["cublas"],
+           "tiles_detected_fault_free": cnt["tiles_detected"], "M": M5, "N": N5, "K": K5}
+    del A, B, C, g
+    torch.cuda.empty_cache()
+    return out
+
+
+def e2e_pipeline(H, g, A, B, C, steps, flops, b_resident=False):
+    """The same step through the public host-buffer API
+    (paper_2305_01024_b200.pipeline.HostPipeline): H2D of step s+1, kernels of
+    step s and D2H of step s-1 overlap on three streams."""
+    import torch
+    from paper_2305_01024_b200 import ftgemm as F
+    from paper_2305_01024_b200.pipeline import HostPipeline
+    A_pin = A.cpu().pin_memory()
+    B_pin = None if b_resident else B.cpu().pin_memory()
+    C_pin = torch.empty(C.shape, dtype=C.dtype).pin_memory()
+    n = max(3, min(steps, 10))
+
+    def serial():
+        A.copy_(A_pin, non_blocking=True)
+        if not b_resident:
+            B.copy_(B_pin, non_blocking=True)
+            g.encode(A, B)
+        else:
+            g.encode(A, None, which=1)
         g.run(A, B, C, ft_level=F.FT_CORRECT)
         C_pin.copy_(C, non_blocking=True)
-    t_e2e_serial = timed([e2e_step] * e2e_steps, 2)
-    # the same steps through paper_2305_01024_b200.pipeline.HostPipeline: H2D of
-    # step s+1, kernels of step s and D2H of step s-1 overlap on three streams
-    from paper_2305_01024_b200.pipeline import HostPipeline
-    pipe = HostPipeline(g)
-    C_pins = [torch.empty(Mr, N, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
-    for i in range(2):                                    # warm-up
+    t_serial = H.timed([serial] * n, 2)
+    pipe = HostPipeline(g, device=H.dev, b_resident=B if b_resident else None)
+    C_pins = [torch.empty(C.shape, dtype=C.dtype).pin_memory() for _ in range(2)]
+    for i in range(2):
         pipe.submit(A_pin, B_pin, C_pins[i % 2])
     pipe.synchronize()
-    barrier(); torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    pipe.begin(stream)
-    for i in range(e2e_steps):
+    H.barrier(); torch.cuda.synchronize()
+    e0, e1 = H.ev(), H.ev()
+    e0.record(H.stream)
+    pipe.begin(H.stream)
+    for i in range(n):
         pipe.submit(A_pin, B_pin, C_pins[i % 2])
-    pipe.join(stream)
+    pipe.join(H.stream)
+    e1.record(H.stream)
+    e1.synchronize()
+    H.barrier(); torch.cuda.synchronize()
+    t = H.max_over_ranks(e0.elapsed_time(e1) / n)
+    same = bool(torch.equal(C_pins[(n - 1) % 2], C_pin))
+    esz = A.element_size()
+    return {"value": tflops(flops, t), "unit": "TFLOPS",
+            "h2d_bytes_per_step": A.numel() * esz + (0 if b_resident else B.numel() * esz),
+            "d2h_bytes_per_step": C.numel() * esz, "ms_per_step": t,
+            "api": "paper_2305_01024_b200.pipeline.HostPipeline (3 streams, 2 slots"
+                   + (", B resident)" if b_resident else ")"),
+            "serial_ms_per_step": t_serial, "pipelined_equals_serial": same}
+
+
+# --------------------------------------------------------- N > 1: cfg5 ---
+def run_multi(args, H):
+    import torch
+
+    import synth
+    from paper_2305_01024_b200 import ftgemm as F
+    from paper_2305_01024_b200.distributed import PartitionedFTGemm
+
+    dev, stream = H.dev, H.stream
+    flops_total = 2.0 * M5 * N5 * K5
+    P = PartitionedFTGemm("bf16", M5, N5, K5, device=dev)
+    g, pl = P.g, P.g.plan
+    rows = P.rows
+    A = synth.matrix_torch(synth.BASE_SEED + 11, M5, K5, dtype="bf16", r0=P.row0, r1=P.row0 + rows, device=dev)
+    if H.rank == 0:
+        B = synth.matrix_torch(synth.BASE_SEED + 12, K5, N5, dtype="bf16", device=dev)
+    else:
+        B = torch.empty(K5, N5, dtype=torch.bfloat16, device=dev)
+    C = torch.empty(rows, N5, dtype=torch.bfloat16, device=dev)
+    fl = Faults(pl, rows, N5, K5, synth.BASE_SEED + synth.SEED_PLAN + 1000 + H.rank)
+
+    def step(inj=()):
+        P.run(A, B, C, ft_level=F.FT_CORRECT, injections=inj)
+
+    # ---- one-shot: encode B on rank 0 + broadcast of B and its encode + one step ----
+    P.set_b(B)                                            # warm-up (communicator setup)
+    torch.cuda.synchronize()
+    H.barrier(); torch.cuda.synchronize()
+    e0, e1, e2 = H.ev(), H.ev(), H.ev()
+    e0.record(stream)
+    bcast_ms = P.set_b(B)
+    e1.record(stream)
+    step()
+    e2.record(stream)
+    e2.synchronize()
+    H.barrier(); torch.cuda.synchronize()
+    oneshot_ms = H.max_over_ranks(e0.elapsed_time(e2))
+    bcast_ms = H.max_over_ranks(e0.elapsed_time(e1))
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    est = H.timed([step] * 3)
+    sched, n_injected = fl.schedule(ERRORS_PER_MIN, args.steps, est, at_least_one=True)
+    kev = [(H.ev(), H.ev()) for _ in range(args.steps)]
+    g.reset()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(dev.index)
+    H.barrier(); torch.cuda.synchronize()
+    e0, e1 = H.ev(), H.ev()
+    e0.record(stream)
+    for i in range(args.steps):
+        g.encode(A, None, which=1)
+        kev[i][0].record(stream)
+        g.run(A, B, C, ft_level=F.FT_CORRECT, injections=sched[i])
+        kev[i][1].record(stream)
     e1.record(stream)
     e1.synchronize()
-    barrier(); torch.cuda.synchronize()
-    t_e2e = max_over_ranks(e0.elapsed_time(e1) / e2e_steps)
-    pipe_ok = bool(torch.equal(C_pins[(e2e_steps - 1) % 2], C_pin))      # same bits as the serial step
-    e2e = {"value": flops_rank * world / (t_e2e * 1e-3) / 1e12, "unit": "TFLOPS",
-           "h2d_bytes_per_step": A.numel() * 2 + B.numel() * 2, "d2h_bytes_per_step": C.numel() * 2,
-           "ms_per_step": t_e2e, "api": "paper_2305_01024_b200.pipeline.HostPipeline (3 streams, 2 slots)",
-           "serial_ms_per_step": t_e2e_serial, "pipelined_equals_serial": pipe_ok}
-
+    H.barrier(); torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms_step = H.max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    ms_kernel = H.max_over_ranks(sum(a.elapsed_time(b) for a, b in kev) / args.steps)
+    counts, events = P.report()                          # all-reduced counters, gathered events
+    inj_total = torch.tensor([n_injected], dtype=torch.int64, device=dev)
+    if H.world > 1:
+        H.dist.all_reduce(inj_total)
+    n_inj_all = int(inj_total.item())
+    ok = counts["corrected"] == n_inj_all and counts["uncorrectable"] == 0 and counts["checksum_only"] == 0
+    flops_rank = 2.0 * rows * N5 * K5
+    window_s = ms_step * args.steps * 1e-3
     peaks, kind = load_peaks()
-    # the kernel is timed inside ~0.4 s of back-to-back steps (power-capped,
-    # sustained regime): the sustained cuBLAS figure is its peak; the burst
-    # figure is reported beside it
-    sustained = peaks.get("bf16_tflops_sustained")
-    peak = sustained or peaks["bf16_tflops"]
-    achieved = flops_rank / (ms_kernel * 1e-3) / 1e12
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get("fused_gemm_bf16_8192_bytes_per_launch")
-        except Exception:
-            traffic = None
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "tc_ftgemm_kernel<bf16,256,FT>",
-                "peak_kind": f"{kind} bf16 {'sustained (cuBLAS back to back, power-capped)' if sustained else 'burst'}",
-                "algorithmic_flops_per_launch": flops_rank,
-                "peak_burst": peaks["bf16_tflops"], "frac_burst": achieved / peaks["bf16_tflops"]}
-
-    if rank == 0:
-        cpu = None
-        if world == 1:
-            tfl, cores, desc = cpu_oracle_sample(args.cpu_seconds)
-            cpu = {"value": tfl, "unit": "TFLOPS", "cores": cores, "kind": "oracle", "sample": desc}
-        line = {"metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-                "config": {"workload": "cfg3: BF16 tcgen05 ABFT GEMM 8192^3 per GPU (M-block partition for N>1)",
-                           "M": Mr * world, "N": N, "K": K, "alpha": 1.0, "beta": 0.0, "ft_level": "CORRECT",
-                           "errors_per_min": ERRORS_PER_MIN, "check_tile": [pl.check_tile_m, pl.check_tile_n],
-                           "mma_tile": [pl.bm, pl.bn, pl.bk], "l2": "inputs larger than L2 (A+B 256 MiB/rank)",
-                           "parallelism": f"mblock{world}" if world > 1 else "single"},
-                "faults": {"injected": n_injected, **{k: v for k, v in counts.items() if v}, "all_corrected": ok_faults},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
-                "clocks": clk, "kernel_ms": ms_kernel, "b_broadcast_ms": bcast_ms, **extra}
+    roof = roofline(peaks, kind, tflops(flops_rank, ms_kernel), window_s, clk, None,
+                    f"tc_ftgemm_kernel<bf16,{pl.bn},FT,{pl.cta_group}>", flops_rank)
+    extra = {}
+    if not args.no_sweep:
+        med = H.interleave({"step": lambda i: step(),
+                            "ft_off": lambda i: g.run(A, B, C, ft_level=F.FT_OFF),
+                            "cublas": lambda i: torch.matmul(A, B, out=C)}, 10)
+        extra = {"comparators_ms": med,
+                 "overhead_vs_ft_off_pct": 100.0 * (med["step"] - med["ft_off"]) / med["ft_off"],
+                 "overhead_vs_cublas_pct": 100.0 * (med["step"] - med["cublas"]) / med["cublas"]}
+    e2e = e2e_pipeline(H, g, A, B, C, args.steps, flops_total, b_resident=True)
+    if H.rank == 0:
+        line = {"metric": METRIC, "value": tflops(flops_total, ms_step), "unit": "TFLOPS", "n_gpus": H.world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": {"workload": f"cfg5: BF16 ABFT GEMM {M5}x{N5}x{K5} M-block-partitioned over {H.world} "
+                                       "GPUs; B encoded once and broadcast once (NCCL) with its encode; step = "
+                                       "encode A block + fused FT GEMM (CORRECT) per rank",
+                           "M": M5, "N": N5, "K": K5, "rows_per_rank": [r for _, r in P.parts],
+                           "errors_per_min_target_per_rank": ERRORS_PER_MIN,
+                           "check_tile": [pl.check_tile_m, pl.check_tile_n], "mma_tile": [pl.bm, pl.bn, pl.bk],
+                           "cta_group": pl.cta_group, "l2": "inputs larger than L2, no flush",
+                           "parallelism": f"mblock{H.world}", "backend": H.backend},
+                "faults": {"injected": n_inj_all, **{k: v for k, v in counts.items() if v}, "all_corrected": ok},
+                "roofline": roof, "cpu_baseline": None, "e2e": e2e, "gpu_launches": 2 * args.steps,
+                "clocks": clk, "kernel_ms": ms_kernel,
+                "one_shot_ms": oneshot_ms, "one_shot_tflops": tflops(flops_total, oneshot_ms),
+                "b_encode_and_broadcast_ms": bcast_ms, **extra}
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier(device_ids=[local])
-        dist.destroy_process_group()
+    H.barrier()
+    H.dist.destroy_process_group()
     return 0
 
 
@@ -496,7 +785,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
-    return run_ours(args)
+    H = Harness(args.backend)
+    return run_single(args, H) if H.world == 1 else run_multi(args, H)
 
 
 if __name__ == "__main__":

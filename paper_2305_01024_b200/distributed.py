@@ -88,7 +88,10 @@ def gather_events(events: list, row0: int, tile_row0: int, group=None) -> list:
 class PartitionedFTGemm:
     """The local share of an M-block-partitioned FT GEMM on this rank."""
 
-    def __init__(self, dtype, M: int, N: int, K: int, device=None, group=None):
+    def __init__(self, dtype, M: int, N: int, K: int, device=None, group=None, gemm_factory=None):
+        """gemm_factory(code, rows, N, K, device=...) builds the per-rank GEMM
+        object (default: ftgemm.FTGemm; tests substitute a host stand-in to
+        drive this logic over gloo on CPU)."""
         from . import ftgemm as F
         self.group = group
         self.world = dist.get_world_size(group)
@@ -101,8 +104,8 @@ class PartitionedFTGemm:
         # every rank runs the full problem's tile class (its own, smaller M could
         # make the plan's wave model pick another check-tile width): full.dtype is
         # the full plan's explicit dtype code (dtype | FTGEMM_TILE(bn, cta_group))
-        self.g = F.FTGemm(full.dtype, max(self.rows, 1), N, K,
-                          device=device or torch.device("cuda", torch.cuda.current_device()))
+        self.g = (gemm_factory or F.FTGemm)(full.dtype, max(self.rows, 1), N, K,
+                                            device=device or torch.device("cuda", torch.cuda.current_device()))
         # the B part of the workspace is only shareable when every rank has the same geometry
         sig = torch.tensor([self.g.plan.bn, self.g.plan.tiles_n, self.g.plan.enc_b_bytes], dtype=torch.int64,
                            device=self.g.enc_ws.device)

@@ -10,7 +10,9 @@ them across steps on three CUDA streams with double-buffered device operands:
     compute stream   ftgemm_encode + ftgemm_run on slot s  (waits: H2D of s, D2H of s-2)
     copy-out stream  D2H C_s from slot s % 2               (waits: compute of s)
 
-so a step costs max(H2D, compute, D2H) instead of their sum: H2D and D2H use
+so a step costs max(H2D, compute, D2H) instead of their sum (with a resident,
+pre-encoded B -- weights, or the broadcast B of an M-block partition -- only A
+travels and only A is encoded per step): H2D and D2H use
 separate copy engines (opposite PCIe directions) and the kernels run beside
 them.  Every slot's reuse is ordered by CUDA events, so the results are the
 same bits as isolated steps (tests/test_gpu_parity.py).  The workspaces of the
@@ -27,7 +29,9 @@ from . import ftgemm as F
 class HostPipeline:
     """Pipelined FT GEMM steps over pinned host buffers for one (dtype, M, N, K)."""
 
-    def __init__(self, g: "F.FTGemm", *, depth: int = 2, device="cuda"):
+    def __init__(self, g: "F.FTGemm", *, depth: int = 2, device="cuda", b_resident: torch.Tensor | None = None):
+        """b_resident: a device B already encoded into g (ftgemm_encode which=2);
+        steps then upload and encode only A (submit(A_host, None, C_host))."""
         if depth < 2:
             raise ValueError("depth must be >= 2 (double buffering)")
         self.g = g
@@ -35,7 +39,9 @@ class HostPipeline:
         dt = {F.BF16: torch.bfloat16}.get(g.dtype & F.DTYPE_MASK, torch.float32)
         M, N, K = g.M, g.N, g.K
         self.A = [torch.empty(M, K, dtype=dt, device=device) for _ in range(depth)]
-        self.B = [torch.empty(K, N, dtype=dt, device=device) for _ in range(depth)]
+        self.b_resident = b_resident
+        self.B = [b_resident] * depth if b_resident is not None else \
+            [torch.empty(K, N, dtype=dt, device=device) for _ in range(depth)]
         self.C = [torch.empty(M, N, dtype=dt, device=device) for _ in range(depth)]
         self.s_in = torch.cuda.Stream(device=device)
         self.s_cmp = torch.cuda.Stream(device=device)
@@ -63,7 +69,8 @@ class HostPipeline:
             self.s_in.wait_event(self.cmp_done[s])
         with torch.cuda.stream(self.s_in):
             self.A[s].copy_(A_host, non_blocking=True)
-            self.B[s].copy_(B_host, non_blocking=True)
+            if self.b_resident is None:
+                self.B[s].copy_(B_host, non_blocking=True)
             if beta != 0.0:
                 if k >= self.depth:
                     self.s_in.wait_event(self.out_done[s])
@@ -74,7 +81,10 @@ class HostPipeline:
             self.s_cmp.wait_event(self.out_done[s])  # C slot read back before it is overwritten
         g, st = self.g, self.s_cmp
         if ft_level != F.FT_OFF:
-            g.encode(self.A[s], self.B[s], stream=st)
+            if self.b_resident is None:
+                g.encode(self.A[s], self.B[s], stream=st)
+            else:
+                g.encode(self.A[s], None, which=1, stream=st)
         g.run(self.A[s], self.B[s], self.C[s], alpha=alpha, beta=beta, ft_level=ft_level, injections=injections,
               stream=st)
         self.cmp_done[s].record(st)

@@ -132,3 +132,47 @@ def injection_sites(n: int, M: int, N: int, K: int, tile_m: int, tile_n: int, bk
         used.add(t)
         sites.append((ti * tile_m + p, tj * tile_n + q, k))
     return sites
+
+
+# ---- the same generator in torch (device-side generation of large inputs) ----
+def _u64(v: int):
+    """uint64 constant as the int64 torch arithmetic wraps it."""
+    return v - (1 << 64) if v >= (1 << 63) else v
+
+
+def _srl(x, s: int):
+    """logical right shift of int64 tensors (as uint64)."""
+    return (x >> s) & ((1 << (64 - s)) - 1)
+
+
+def splitmix64_torch(x):
+    """splitmix64 on an int64 torch tensor, bit-identical to splitmix64() (the
+    int64 multiply wraps modulo 2^64 like the uint64 one)."""
+    z = x + _u64(0x9E3779B97F4A7C15)
+    z = (z ^ _srl(z, 30)) * _u64(0xBF58476D1CE4E5B9)
+    z = (z ^ _srl(z, 27)) * _u64(0x94D049BB133111EB)
+    return z ^ _srl(z, 31)
+
+
+def matrix_torch(seed: int, rows: int, cols: int, *, dist: str = "signed", dtype: str = "f32",
+                 r0: int = 0, r1: int | None = None, device="cuda", chunk_rows: int = 2048):
+    """Rows [r0, r1) of matrix(seed, rows, cols) generated on `device` (torch),
+    element-for-element identical to the numpy generator (tests/test_synth.py).
+    Used for inputs too large to generate on the host in time (bench cfg5)."""
+    import torch
+    r1 = rows if r1 is None else r1
+    key = int(splitmix64(np.array([seed & 0xFFFFFFFFFFFFFFFF], dtype=np.uint64))[0])
+    out = torch.empty(r1 - r0, cols, dtype=torch.bfloat16 if dtype == "bf16" else torch.float32, device=device)
+    c = torch.arange(cols, dtype=torch.int64, device=device)[None, :]
+    for a in range(r0, r1, chunk_rows):
+        b = min(r1, a + chunk_rows)
+        r = torch.arange(a, b, dtype=torch.int64, device=device)[:, None]
+        z = splitmix64_torch(r * cols + c + _u64(key))
+        top = _srl(z, 40).to(torch.float64)
+        if dist == "int":
+            v = torch.remainder(top, 9.0) - 4.0
+        else:
+            lo, hi = (-1.0, 1.0) if dist == "signed" else (0.0, 1.0)
+            v = lo + (hi - lo) * (top * 2.0 ** -24)
+        out[a - r0:b - r0] = v.to(torch.float32).to(out.dtype)
+    return out
