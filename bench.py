@@ -598,6 +598,26 @@ def cfg4_section(args, H, peaks):
                      "run_over_off": med["ft_run"] / med["ft_off"], "step_over_run": med["ft_step"] / med["ft_run"],
                      "tile_class": [g.plan.bn, g.plan.cta_group]}
         del A, B, C, g
+    # tall-skinny batch: 32 x (4096, 128, 4096) in one persistent launch (ftgemm_run_batched)
+    batch, M, N, K = 32, 4096, 128, 4096
+    A = torch.stack([synth.matrix_torch(synth.BASE_SEED + 41 + b, M, K, dtype="bf16", device=H.dev) for b in range(batch)])
+    B = torch.stack([synth.matrix_torch(synth.BASE_SEED + 141 + b, K, N, dtype="bf16", device=H.dev) for b in range(batch)])
+    C = torch.empty(batch, M, N, dtype=torch.bfloat16, device=H.dev)
+    g = F.FTGemmBatched("bf16", batch, M, N, K, device=H.dev)
+    g.encode(A, B)
+    med = H.interleave({"ft_step": lambda i: (g.encode(A, B), g.run(A, B, C)),
+                        "ft_run": lambda i: g.run(A, B, C),
+                        "ft_off": lambda i: g.run(A, B, C, ft_level=F.FT_OFF),
+                        "cublas": lambda i: torch.bmm(A, B, out=C)}, 30)
+    byts = 2.0 * batch * (M * K + K * N + M * N)
+    out["batch32x4096x128x4096"] = {
+        **{k + "_ms": v for k, v in med.items()},
+        "ft_run_hbm_frac": byts / (med["ft_run"] * 1e-3) / 1e9 / peaks["hbm_gbs"],
+        "ft_off_hbm_frac": byts / (med["ft_off"] * 1e-3) / 1e9 / peaks["hbm_gbs"],
+        "cublas_hbm_frac": byts / (med["cublas"] * 1e-3) / 1e9 / peaks["hbm_gbs"],
+        "run_over_off": med["ft_run"] / med["ft_off"], "step_over_run": med["ft_step"] / med["ft_run"],
+        "tile_class": [g.plan.bn, g.plan.cta_group], "launches_per_run": 1}
+    del A, B, C, g
     return out
 
 

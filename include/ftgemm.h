@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define FTGEMM_ABI_VERSION 1
+#define FTGEMM_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define FTGEMM_API __attribute__((visibility("default")))
@@ -216,7 +216,11 @@ typedef struct ftgemm_counts {
     int64_t corrected, checksum_only, uncorrectable, located;
     int64_t events;              /* events recorded or dropped */
     int64_t dropped;             /* events that did not fit the ring */
-} ftgemm_counts_t;
+    float   max_resid_ratio;     /* threshold margin telemetry: the largest |residual| / tau over every
+                                    residual that was NOT flagged (fused kernels; 0 if none) -- a
+                                    fault-free run's distance from a false positive */
+    int32_t pad;
+} ftgemm_counts_t;                /* 72 bytes */
 
 /* ---- plan --------------------------------------------------------------------
  * The host-side instantiation table (north_star item 4): which compile-time
@@ -310,6 +314,31 @@ FTGEMM_API int ftgemm_run(int dtype, int64_t M, int64_t N, int64_t K, float alph
                const void* enc_ws, int ft_level,
                const ftgemm_inject_t* inj, int32_t n_inj,
                void* report_ws, void* stream);
+
+/* ---- batched runs (cfg4 "tall-skinny batches") ---------------------------------
+ * `batch` independent problems of one shape in ONE persistent launch (PAPER.md
+ * :450, :501 evaluate irregular and tall-skinny shapes; 32 launches of a
+ * 4096 x 128 x 4096 GEMM leave most of the 148 SMs idle).  Problem b reads
+ * A + b stride_a, B + b stride_b and writes C + b stride_c (strides in
+ * ELEMENTS, multiples of 16 bytes; stride_b may be 0 for a shared B; C problems
+ * must not overlap: stride_c >= M ldc), and uses its own encode at
+ * enc_ws + b enc_stride (BYTES, a multiple of 256, >= plan.enc_bytes of
+ * ftgemm_plan_batched).  Every problem is planned, encoded, verified and
+ * corrected exactly as the single-problem call would do it with the batched
+ * plan's tile class.  Faults and events use the stacked (batch x M) x N view:
+ * inj.row and event.row in [0, batch M), event.tile_m = b tiles_m + ti.
+ * Tensor-core dtypes only (F32_SIMT -> UNSUPPORTED); ftgemm_encode_batched's
+ * `which` as ftgemm_encode.  ftgemm_plan_batched: the tile-class choice counts
+ * all problems' work units (explicit FTGEMM_TILE classes are honoured).
+ * Errors: as ftgemm_run / ftgemm_encode, INVALID_VALUE (batch < 1, bad strides). */
+FTGEMM_API int ftgemm_plan_batched(int dtype, int64_t batch, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* out);
+FTGEMM_API int ftgemm_encode_batched(int dtype, int64_t batch, int64_t M, int64_t N, int64_t K,
+               const void* A, int64_t lda, int64_t stride_a, const void* B, int64_t ldb, int64_t stride_b,
+               void* enc_ws, int64_t enc_stride, int which, void* stream);
+FTGEMM_API int ftgemm_run_batched(int dtype, int64_t batch, int64_t M, int64_t N, int64_t K, float alpha,
+               const void* A, int64_t lda, int64_t stride_a, const void* B, int64_t ldb, int64_t stride_b,
+               float beta, void* C, int64_t ldc, int64_t stride_c, const void* enc_ws, int64_t enc_stride,
+               int ft_level, const ftgemm_inject_t* inj, int32_t n_inj, void* report_ws, void* stream);
 
 /* ---- report ------------------------------------------------------------------
  * Synchronises `stream`, then copies the counters into *counts (host) and up

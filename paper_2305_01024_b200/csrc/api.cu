@@ -24,7 +24,7 @@
 namespace ftg {
 cudaError_t launch_encode(const Geometry& g, const EncLayout& L, int64_t M, int64_t N, int64_t K,
                           const void* A, int64_t lda, const void* B, int64_t ldb, void* enc, int which,
-                          cudaStream_t st);
+                          cudaStream_t st, int batch, int64_t sA, int64_t sB, int64_t sE);
 }  // namespace ftg
 
 namespace ftg {
@@ -83,7 +83,7 @@ bool parse_code(int code, Code* c) {
 
 // The shape-class table (north_star item 4): compile-time instantiations
 // chosen per problem shape.  `code` must have passed parse_code.
-void fill_plan(int code, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* p) {
+void fill_plan(int code, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* p, int64_t batch = 1) {
     Code cc;
     parse_code(code, &cc);
     const int dtype = cc.dtype;
@@ -107,7 +107,7 @@ void fill_plan(int code, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* p) {
         const bool skinny_n = N <= 252;
         const bool skinny_m = M <= 250 && !skinny_n;
         const int64_t tiles_m125 = (M + 124) / 125;
-        bool small = !skinny_n && !skinny_m && (tiles256 < 2 * kNumSMsB200 || N <= 512);
+        bool small = !skinny_n && !skinny_m && (tiles256 * batch < 2 * kNumSMsB200 || N <= 512);
         // CTA pairs (cta_group::2, M = 256 per MMA) halve the B tile each SM
         // loads; they lose on K = 128 shapes (epilogue-bound) and skinny M
         int cg = (!small && ((tiles_m125 >= 4 && (K >= 2048 || (dtype == FTGEMM_TF32 && K >= 1024))) ||
@@ -125,7 +125,7 @@ void fill_plan(int code, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* p) {
             double best = 1e300;
             for (const Cls& c : cls) {
                 const int64_t tn = (N + c.bn - 5) / (c.bn - 4);
-                const int64_t units = ((tiles_m125 + c.cg - 1) / c.cg) * tn;
+                const int64_t units = ((tiles_m125 + c.cg - 1) / c.cg) * tn * batch;
                 const int64_t slots = kNumSMsB200 / c.cg;
                 const double t = (double)((units + slots - 1) / slots) * (dtype == FTGEMM_TF32 ? c.c_tf32 : c.c_bf16);
                 if (t < best * (1.0 - 1e-9)) { best = t; small = c.bn == 128; cg = c.cg; }
@@ -200,16 +200,29 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return fn;
 }
 
+// Every map carries a trailing batch dimension (size `batch`, stride
+// `batch_bytes`; 1 and any valid stride for a single problem), so one kernel
+// instantiation serves single and batched launches (ftgemm_run_batched).
+struct Batch {
+    uint64_t n = 1, bytes = 0;
+};
+uint64_t batch_stride(const Batch& bt, uint64_t fallback) {
+    // a size-1 dimension still needs a legal stride (a multiple of 16 below 2^40)
+    if (bt.n > 1) return bt.bytes;
+    const uint64_t s = (fallback + 15) & ~(uint64_t)15;
+    return s > 0 && s < (1ull << 40) ? s : 16;
+}
+
 int make_map(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t outer,
              uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
-             CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
+             CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B, Batch bt = Batch{}) {
     auto enc = tensor_map_encoder();
     if (!enc) return fail(FTGEMM_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
-    cuuint64_t dims[2] = {inner, outer};
-    cuuint64_t strides[1] = {row_bytes};
-    cuuint32_t box[2] = {box_inner, box_outer};
-    cuuint32_t es[2] = {1, 1};
-    CUresult r = enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    cuuint64_t dims[3] = {inner, outer, bt.n};
+    cuuint64_t strides[2] = {row_bytes, batch_stride(bt, row_bytes * outer)};
+    cuuint32_t box[3] = {box_inner, box_outer, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(m, dt, 3, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(FTGEMM_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -221,15 +234,16 @@ int make_map(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t 
 // landing as nblk stacked [bk][128 B] SWIZZLE_128B atoms -- the smem layout of
 // the N-major B tile (cols must be a multiple of the slice width)
 int make_map_3d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t slice, uint64_t rows,
-                uint64_t nblocks, uint64_t row_bytes, uint32_t box_rows, uint32_t box_blocks, CUtensorMapSwizzle sw) {
+                uint64_t nblocks, uint64_t row_bytes, uint32_t box_rows, uint32_t box_blocks, CUtensorMapSwizzle sw,
+                Batch bt = Batch{}) {
     auto enc = tensor_map_encoder();
     if (!enc) return fail(FTGEMM_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
     const uint64_t elt = (dt == CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) ? 2 : 4;
-    cuuint64_t dims[3] = {slice, rows, nblocks};
-    cuuint64_t strides[2] = {row_bytes, slice * elt};
-    cuuint32_t box[3] = {(cuuint32_t)slice, box_rows, box_blocks};
-    cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = enc(m, dt, 3, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+    cuuint64_t dims[4] = {slice, rows, nblocks, bt.n};
+    cuuint64_t strides[3] = {row_bytes, slice * elt, batch_stride(bt, row_bytes * rows)};
+    cuuint32_t box[4] = {(cuuint32_t)slice, box_rows, box_blocks, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = enc(m, dt, 4, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(FTGEMM_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled (3-D) failed (%d)", (int)r);
     return FTGEMM_OK;
@@ -301,8 +315,9 @@ int ftgemm_encode_layout(int code, int64_t M, int64_t N, int64_t K, ftgemm_enc_l
     return FTGEMM_OK;
 }
 
-int ftgemm_encode(int code, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B,
-                  int64_t ldb, void* enc_ws, int which, void* stream) {
+static int encode_impl(int code, int64_t batch, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                       int64_t sA, const void* B, int64_t ldb, int64_t sB, void* enc_ws, int64_t enc_stride, int which,
+                       void* stream) {
     int e = check_dims(code, M, N, K);
     if (e) return e;
     const int dtype = code & FTGEMM_DTYPE_MASK;
@@ -310,27 +325,45 @@ int ftgemm_encode(int code, int64_t M, int64_t N, int64_t K, const void* A, int6
     if (!enc_ws) return fail(FTGEMM_ERR_INVALID_VALUE, "null enc_ws");
     if ((which & 1) && (!A || lda < K)) return fail(FTGEMM_ERR_INVALID_VALUE, "bad A / lda");
     if ((which & 2) && (!B || ldb < N)) return fail(FTGEMM_ERR_INVALID_VALUE, "bad B / ldb");
+    if (batch < 1 || batch >= 65536) return fail(FTGEMM_ERR_INVALID_VALUE, "batch must be in [1, 65536)");
+    if (batch > 1 && dtype == FTGEMM_F32_SIMT) return fail(FTGEMM_ERR_UNSUPPORTED, "batched: tensor-core dtypes");
+    if (sA < 0 || sB < 0) return fail(FTGEMM_ERR_INVALID_VALUE, "negative batch stride");
     const int elt = dtype == FTGEMM_BF16 ? 2 : 4;
-    if ((which & 1) && (!aligned16(A) || (lda * elt) % 16)) return fail(FTGEMM_ERR_UNSUPPORTED, "A must be 16-byte aligned with 16-byte row pitch");
-    if ((which & 2) && (!aligned16(B) || (ldb * elt) % 16)) return fail(FTGEMM_ERR_UNSUPPORTED, "B must be 16-byte aligned with 16-byte row pitch");
+    if ((which & 1) && (!aligned16(A) || (lda * elt) % 16 || (sA * elt) % 16)) return fail(FTGEMM_ERR_UNSUPPORTED, "A must be 16-byte aligned with 16-byte row pitch");
+    if ((which & 2) && (!aligned16(B) || (ldb * elt) % 16 || (sB * elt) % 16)) return fail(FTGEMM_ERR_UNSUPPORTED, "B must be 16-byte aligned with 16-byte row pitch");
     if ((reinterpret_cast<uintptr_t>(enc_ws) & 255) != 0) return fail(FTGEMM_ERR_INVALID_VALUE, "enc_ws must be 256-byte aligned");
     if (!check_device()) return fail(FTGEMM_ERR_UNSUPPORTED, "no sm_100 (B200) device");
     ftgemm_plan_t p;
-    fill_plan(code, M, N, K, &p);
+    fill_plan(code, M, N, K, &p, batch);
     const Geometry g = geometry(p, K);
     const EncLayout L = enc_layout(g, M, N);
-    cudaError_t ce = launch_encode(g, L, M, N, K, A, lda, B, ldb, enc_ws, which, (cudaStream_t)stream);
+    if (batch > 1 && (enc_stride < (int64_t)L.total || enc_stride % 256))
+        return fail(FTGEMM_ERR_INVALID_VALUE, "enc_stride must be >= plan.enc_bytes and a multiple of 256");
+    cudaError_t ce = launch_encode(g, L, M, N, K, A, lda, B, ldb, enc_ws, which, (cudaStream_t)stream, (int)batch,
+                                   sA * elt, sB * elt, batch > 1 ? enc_stride : (int64_t)L.total);
     if (ce != cudaSuccess) return fail_cuda(ce, "encode launch");
     g_err.clear();
     return FTGEMM_OK;
 }
 
+// batched launches (ftgemm_run_batched): problem b's operands at A + b sA,
+// B + b sB, C + b sC (elements), its encode at enc_ws + b enc_stride (bytes)
+struct BatchArgs {
+    int64_t n = 1, sA = 0, sB = 0, sC = 0, enc_stride = 0;
+};
+
 static int run_impl(int code, int64_t M, int64_t N, int64_t K, float alpha, const void* A, int64_t lda,
                     const void* B, int64_t ldb, float beta, void* C, int64_t ldc, const void* enc_ws, int ft_level,
-                    int64_t ks, int fuse_a, const ftgemm_inject_t* inj, int32_t n_inj, void* report_ws, void* stream) {
+                    int64_t ks, int fuse_a, const ftgemm_inject_t* inj, int32_t n_inj, void* report_ws, void* stream,
+                    const BatchArgs& bt = BatchArgs{}) {
     int e = check_dims(code, M, N, K);
     if (e) return e;
     const int dtype = code & FTGEMM_DTYPE_MASK;
+    if (bt.n < 1 || bt.n >= (1 << 20)) return fail(FTGEMM_ERR_INVALID_VALUE, "batch must be in [1, 2^20)");
+    if (bt.n > 1 && (dtype == FTGEMM_F32_SIMT || ks > 0 || fuse_a))
+        return fail(FTGEMM_ERR_UNSUPPORTED, "batched runs: tensor-core dtypes, end-of-K verification, separate encode");
+    if (bt.sA < 0 || bt.sB < 0 || bt.sC < 0 || bt.enc_stride < 0)
+        return fail(FTGEMM_ERR_INVALID_VALUE, "negative batch stride");
     if (ks < 0) return fail(FTGEMM_ERR_INVALID_VALUE, "ks must be >= 0");
     if (ks > 0 && dtype == FTGEMM_F32_SIMT) return fail(FTGEMM_ERR_UNSUPPORTED, "online-interval mode: tensor-core dtypes");
     if (ks > 0 && (ft_level == FTGEMM_FT_OFF || ft_level == FTGEMM_FT_DETECT_ROWS))
@@ -347,10 +380,13 @@ static int run_impl(int code, int64_t M, int64_t N, int64_t K, float alpha, cons
     const int elt = dtype == FTGEMM_BF16 ? 2 : 4;
     if (!aligned16(A) || !aligned16(B) || !aligned16(C) || (lda * elt) % 16 || (ldb * elt) % 16 || (ldc * elt) % 16)
         return fail(FTGEMM_ERR_UNSUPPORTED, "A, B, C must be 16-byte aligned with 16-byte row pitches");
+    if (bt.n > 1 && ((bt.sA * elt) % 16 || (bt.sB * elt) % 16 || (bt.sC * elt) % 16))
+        return fail(FTGEMM_ERR_UNSUPPORTED, "batch strides must be multiples of 16 bytes");
+    if (bt.n > 1 && bt.sC < M * ldc) return fail(FTGEMM_ERR_INVALID_VALUE, "C problems overlap (stride_c < M * ldc)");
     if (!check_device()) return fail(FTGEMM_ERR_UNSUPPORTED, "no sm_100 (B200) device");
 
     ftgemm_plan_t p;
-    fill_plan(code, M, N, K, &p);
+    fill_plan(code, M, N, K, &p, bt.n);
     if (ks > 0 && ks % p.bk) return fail(FTGEMM_ERR_INVALID_VALUE, "ks must be a multiple of plan.bk (%d)", p.bk);
     // in-kernel encode: one CTA per MMA (a CTA pair would put a cluster-scope
     // release of the peer's split rows on every k-block's critical path)
@@ -358,6 +394,12 @@ static int run_impl(int code, int64_t M, int64_t N, int64_t K, float alpha, cons
     const bool ft = ft_level != FTGEMM_FT_OFF;
     const Geometry g = geometry(p, K);
     const EncLayout L = enc_layout(g, M, N);
+    const int64_t enc_stride = bt.n > 1 ? bt.enc_stride : (int64_t)L.total;
+    if (ft && bt.n > 1 && (enc_stride < (int64_t)L.total || enc_stride % 256))
+        return fail(FTGEMM_ERR_INVALID_VALUE, "enc_stride must be >= plan.enc_bytes and a multiple of 256");
+    const int64_t units_m_h = (p.tiles_m + p.cta_group - 1) / p.cta_group;     // tensor-core units per problem
+    const int64_t units_pb = dtype == FTGEMM_F32_SIMT ? 0 : units_m_h * p.tiles_n;
+    if (units_pb * bt.n >= (1ll << 31)) return fail(FTGEMM_ERR_UNSUPPORTED, "too many tiles in one launch");
     cudaStream_t st = (cudaStream_t)stream;
     const int num_kb = (int)((K + p.bk - 1) / p.bk);
 
@@ -368,14 +410,16 @@ static int run_impl(int code, int64_t M, int64_t N, int64_t K, float alpha, cons
         std::vector<int> per_tile;
         for (int i = 0; i < n_inj; ++i) {
             const ftgemm_inject_t& f = inj[i];
-            if (f.row < 0 || f.row >= M || f.col < 0 || f.col >= N || f.k_elem < 0 ||
+            // batched: rows of the stacked (batch x M) x N view
+            if (f.row < 0 || f.row >= M * bt.n || f.col < 0 || f.col >= N || f.k_elem < 0 ||
                 f.bit < 0 || f.bit > 31 || f.mode < 0 || f.mode > 1 || f.target < 0 || f.target > 2)
                 return fail(FTGEMM_ERR_INVALID_VALUE, "injection %d out of range", i);
-            const int ti = (int)(f.row / p.check_tile_m), tj = (int)(f.col / p.check_tile_n);
+            const int64_t pb = f.row / M, row = f.row - pb * M;
+            const int ti = (int)(row / p.check_tile_m), tj = (int)(f.col / p.check_tile_n);
             DevInject d;
-            d.tile = tile_key(p, ti, tj);
+            d.tile = (int)(pb * units_pb) + tile_key(p, ti, tj);
             d.kb = (int)std::min<int64_t>(f.k_elem / p.bk, num_kb - 1);
-            d.p = (int)(f.row - (int64_t)ti * p.check_tile_m);
+            d.p = (int)(row - (int64_t)ti * p.check_tile_m);
             d.q = (int)(f.col - (int64_t)tj * p.check_tile_n);
             d.bit = f.bit; d.mode = f.mode; d.addend = f.addend;
             // CTA of the pair that owns the tile in bits 8+ (the epilogue filters on it)
@@ -425,8 +469,10 @@ static int run_impl(int code, int64_t M, int64_t N, int64_t K, float alpha, cons
 #if defined(FTGEMM_EXP_A128)
         if ((e = make_map(&mA, dt, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * elt, (uint32_t)p.bk, 128u))) return e;
 #else
-        if ((e = make_map(&mA, dt, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * elt, (uint32_t)p.bk, (uint32_t)bmd))) return e;
+        if ((e = make_map(&mA, dt, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * elt, (uint32_t)p.bk, (uint32_t)bmd,
+                          CU_TENSOR_MAP_SWIZZLE_128B, Batch{(uint64_t)bt.n, (uint64_t)(bt.sA * elt)}))) return e;
 #endif
+        const Batch benc{(uint64_t)bt.n, (uint64_t)enc_stride};
         // B (N-major, 128-byte column slices): one 3-D request per stage when the
         // column count is a whole number of slices (B^r always is), else one
         // 2-D box per slice
@@ -441,28 +487,35 @@ static int run_impl(int code, int64_t M, int64_t N, int64_t K, float alpha, cons
             // the encoded operand B^r (N-major, kp rows of tiles_n * bn) from the encode workspace
             const uint64_t ldt = (uint64_t)g.tiles_n * p.bn;
             if (b3d) e = make_map_3d(&mB, dt, enc + L.bt, boxn, (uint64_t)g.kp, ldt / boxn, ldt * elt, (uint32_t)p.bk,
-                                     nbox_cta, bsw);
-            else e = make_map(&mB, dt, enc + L.bt, ldt, (uint64_t)g.kp, ldt * elt, boxn, (uint32_t)p.bk, bsw);
+                                     nbox_cta, bsw, benc);
+            else e = make_map(&mB, dt, enc + L.bt, ldt, (uint64_t)g.kp, ldt * elt, boxn, (uint32_t)p.bk, bsw, benc);
             if (e) return e;
         } else {
             b3d = b3d && (N % boxn) == 0;
+            const Batch bb{(uint64_t)bt.n, (uint64_t)(bt.sB * elt)};
             if (b3d) e = make_map_3d(&mB, dt, B, boxn, (uint64_t)K, (uint64_t)N / boxn, (uint64_t)ldb * elt,
-                                     (uint32_t)p.bk, nbox_cta, bsw);
-            else e = make_map(&mB, dt, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb * elt, boxn, (uint32_t)p.bk, bsw);
+                                     (uint32_t)p.bk, nbox_cta, bsw, bb);
+            else e = make_map(&mB, dt, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb * elt, boxn, (uint32_t)p.bk, bsw, bb);
             if (e) return e;
         }
         // C: 128-byte rows of output per thread, 32-row boxes (29 rows for the
         // last epilogue warp of a 125-row check tile)
         CUtensorMap mC, mC29;
         const CUtensorMapDataType dc = tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-        if ((e = make_map(&mC, dc, C, (uint64_t)N, (uint64_t)M, (uint64_t)ldc * elt, boxn, 32))) return e;
-        if ((e = make_map(&mC29, dc, C, (uint64_t)N, (uint64_t)M, (uint64_t)ldc * elt, boxn, ft ? 29 : 32))) return e;
+        const Batch bc{(uint64_t)bt.n, (uint64_t)(bt.sC * elt)};
+        if ((e = make_map(&mC, dc, C, (uint64_t)N, (uint64_t)M, (uint64_t)ldc * elt, boxn, 32, CU_TENSOR_MAP_SWIZZLE_128B,
+                          bc))) return e;
+        if ((e = make_map(&mC29, dc, C, (uint64_t)N, (uint64_t)M, (uint64_t)ldc * elt, boxn, ft ? 29 : 32,
+                          CU_TENSOR_MAP_SWIZZLE_128B, bc))) return e;
         TcArgs a{};
         a.M = (int)M; a.N = (int)N; a.K = (int)K; a.num_kb = num_kb;
         a.tiles_m = (int)((M + bmd - 1) / bmd); a.tiles_n = (int)((N + bnd - 1) / bnd);
         a.num_tiles = a.tiles_m * a.tiles_n;
         a.units_m = (a.tiles_m + p.cta_group - 1) / p.cta_group;
-        a.num_units = a.units_m * a.tiles_n;
+        a.units_pb = a.units_m * a.tiles_n;
+        a.num_units = (int)(a.units_pb * bt.n);
+        a.enc_bs = enc_stride / 4;
+        a.c_bs = bt.sC;
         a.group = tc_group(a.units_m, p.cta_group);
         a.ft_level = ft_level; a.alpha = alpha; a.beta = beta; a.C = C; a.ldc = ldc;
         a.ks_kb = ks > 0 ? (int)std::min<int64_t>(ks / p.bk, num_kb) : 0;
@@ -478,12 +531,49 @@ static int run_impl(int code, int64_t M, int64_t N, int64_t K, float alpha, cons
         // pre-swizzled split rows of A^c: one 384-byte row per (check tile, k-block)
         CUtensorMap mY{};
         if (ft && (e = make_map(&mY, CU_TENSOR_MAP_DATA_TYPE_UINT32, enc + L.y, 96, (uint64_t)g.tiles_m * g.nkb, 384,
-                                96, 1, CU_TENSOR_MAP_SWIZZLE_NONE))) return e;
+                                96, 1, CU_TENSOR_MAP_SWIZZLE_NONE, benc))) return e;
         ce = launch_tc(tf32, p.bn, ft, p.cta_group, mA, mB, mC, mC29, mY, a, st);
     }
     if (ce != cudaSuccess) return fail_cuda(ce, "kernel launch");
     g_err.clear();
     return FTGEMM_OK;
+}
+
+int ftgemm_encode(int code, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B,
+                  int64_t ldb, void* enc_ws, int which, void* stream) {
+    return encode_impl(code, 1, M, N, K, A, lda, 0, B, ldb, 0, enc_ws, 0, which, stream);
+}
+
+int ftgemm_encode_batched(int code, int64_t batch, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                          int64_t stride_a, const void* B, int64_t ldb, int64_t stride_b, void* enc_ws,
+                          int64_t enc_stride, int which, void* stream) {
+    return encode_impl(code, batch, M, N, K, A, lda, stride_a, B, ldb, stride_b, enc_ws, enc_stride, which, stream);
+}
+
+int ftgemm_plan_batched(int code, int64_t batch, int64_t M, int64_t N, int64_t K, ftgemm_plan_t* out) {
+    if (!out) return fail(FTGEMM_ERR_INVALID_VALUE, "null plan pointer");
+    int e = check_dims(code, M, N, K);
+    if (e) return e;
+    if (batch < 1) return fail(FTGEMM_ERR_INVALID_VALUE, "batch must be >= 1");
+    fill_plan(code, M, N, K, out, batch);
+    const Geometry g = geometry(*out, K);
+    const EncLayout L = enc_layout(g, M, N);
+    out->enc_bytes = (int64_t)L.total;
+    out->enc_b_offset = (int64_t)L.b_off;
+    out->enc_b_bytes = (int64_t)L.b_bytes;
+    out->report_bytes = (int64_t)report_bytes();
+    g_err.clear();
+    return FTGEMM_OK;
+}
+
+int ftgemm_run_batched(int code, int64_t batch, int64_t M, int64_t N, int64_t K, float alpha, const void* A,
+                       int64_t lda, int64_t stride_a, const void* B, int64_t ldb, int64_t stride_b, float beta, void* C,
+                       int64_t ldc, int64_t stride_c, const void* enc_ws, int64_t enc_stride, int ft_level,
+                       const ftgemm_inject_t* inj, int32_t n_inj, void* report_ws, void* stream) {
+    BatchArgs bt;
+    bt.n = batch; bt.sA = stride_a; bt.sB = stride_b; bt.sC = stride_c; bt.enc_stride = enc_stride;
+    return run_impl(code, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, enc_ws, ft_level, 0, 0, inj, n_inj, report_ws,
+                    stream, bt);
 }
 
 int ftgemm_run(int dtype, int64_t M, int64_t N, int64_t K, float alpha, const void* A, int64_t lda,
@@ -651,6 +741,12 @@ int ftgemm_report(const void* report_ws, ftgemm_counts_t* counts, ftgemm_event_t
     counts->located = (int64_t)c[CNT_LOCATED];
     counts->events = (int64_t)c[CNT_EVENTS];
     counts->dropped = (int64_t)c[CNT_DROPPED];
+    unsigned int mr = 0;
+    ce = cudaMemcpy(&mr, reinterpret_cast<const char*>(report_ws) + offsetof(ReportDev, max_ratio_bits), sizeof(mr),
+                    cudaMemcpyDeviceToHost);
+    if (ce != cudaSuccess) return fail_cuda(ce, "report copy");
+    std::memcpy(&counts->max_resid_ratio, &mr, sizeof(float));
+    counts->pad = 0;
     const int64_t stored = std::min<int64_t>(counts->events, kMaxEvents);
     const int64_t n = std::min<int64_t>(stored, max_events);
     if (n > 0) {

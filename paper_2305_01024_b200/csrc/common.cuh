@@ -36,7 +36,9 @@ static_assert(sizeof(DevInject) == 32, "DevInject layout");
 
 struct ReportDev {
     unsigned long long counts[8];     // order of ftgemm_counts_t
-    unsigned long long pad[8];
+    unsigned int max_ratio_bits;      // max |residual| / tau over unflagged residuals (FP32 bits; >= 0)
+    unsigned int pad32;
+    unsigned long long pad[7];
     ftgemm_event_t events[kMaxEvents];
 };
 enum { CNT_CHECKED = 0, CNT_DETECTED, CNT_CORRECTED, CNT_CHECKSUM_ONLY, CNT_UNCORRECTABLE,
@@ -49,7 +51,10 @@ inline size_t report_inject_offset() { return sizeof(ReportDev); }
 struct TcArgs {
     int M, N, K, num_kb;
     int tiles_m, tiles_n, num_tiles;
-    int units_m, num_units;   // work units: CG check tiles stacked in M (CG = CTAs per MMA)
+    int units_m, num_units;   // work units: CG check tiles stacked in M (CG = CTAs per MMA); all problems
+    int units_pb;             // units per problem (batched launches: num_units = batch x units_pb)
+    int64_t enc_bs;           // encode-workspace stride between problems, in floats
+    int64_t c_bs;             // C stride between problems, in elements
     int group;            // M-units per schedule group (tile_coords)
     int ft_level;
     int ks_kb;            // > 0: verify after every ks_kb k-blocks too (online-interval mode)

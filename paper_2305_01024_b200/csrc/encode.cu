@@ -78,11 +78,37 @@ __device__ __forceinline__ bool last_block(int* ticket, int idx, int nblocks, in
 struct EncAP {
     const void* A; int64_t lda; int M, K, bmd, kp, bk, nkc;
     float* Ac; uint8_t* Y; float* rn2; float* acn2; int* ticket; float* rownorm; float* acnorm;
+    int64_t sA, sE;        // batched encode: bytes between problems (A, encode workspace)
 };
 struct EncBP {
     const void* B; int64_t ldb; int N, K, bnd, bn, kp, ldt, nkc, rpb;
     float* Br; uint8_t* Bt; float* cn2; float* brn2; int* ticket; float* colnorm; float* brnorm;
+    int64_t sB, sE;
 };
+
+// the parameters of problem b of a batched encode (every output lives in that
+// problem's copy of the encode workspace)
+template <class T> __device__ __forceinline__ T* boff(T* p, int64_t bytes) {
+    return p ? reinterpret_cast<T*>(reinterpret_cast<char*>(const_cast<std::remove_const_t<T>*>(p)) + bytes) : p;
+}
+__device__ __forceinline__ EncAP at_batch(const EncAP& P, int b) {
+    if (b == 0) return P;
+    EncAP Q = P;
+    const int64_t e = (int64_t)b * P.sE;
+    Q.A = boff(P.A, (int64_t)b * P.sA);
+    Q.Ac = boff(P.Ac, e); Q.Y = boff(P.Y, e); Q.rn2 = boff(P.rn2, e); Q.acn2 = boff(P.acn2, e);
+    Q.ticket = boff(P.ticket, e); Q.rownorm = boff(P.rownorm, e); Q.acnorm = boff(P.acnorm, e);
+    return Q;
+}
+__device__ __forceinline__ EncBP at_batch(const EncBP& P, int b) {
+    if (b == 0) return P;
+    EncBP Q = P;
+    const int64_t e = (int64_t)b * P.sE;
+    Q.B = boff(P.B, (int64_t)b * P.sB);
+    Q.Br = boff(P.Br, e); Q.Bt = boff(P.Bt, e); Q.cn2 = boff(P.cn2, e); Q.brn2 = boff(P.brn2, e);
+    Q.ticket = boff(P.ticket, e); Q.colnorm = boff(P.colnorm, e); Q.brnorm = boff(P.brnorm, e);
+    return Q;
+}
 
 // ------------------------------------------ encode A (register streaming) --
 // grid (nkc = ceil(kp/KC), tiles_m); block 256.  Same outputs as the TMA-fed
@@ -643,25 +669,27 @@ __device__ __forceinline__ void encode_b_tc_body(const int kc, const int tj, con
 // as every block has started.
 template <int MODE>
 __global__ void __launch_bounds__(256, ENC_A_MINB) encode_a_kernel(const EncAP P) {
-    encode_a_body<MODE>(blockIdx.x, blockIdx.y, P);
+    encode_a_body<MODE>(blockIdx.x, blockIdx.y, at_batch(P, blockIdx.z));
 }
 template <int MODE>
 __global__ void __launch_bounds__(256) encode_b_tc_kernel(const EncBP P) {
-    encode_b_tc_body<MODE>(blockIdx.x, blockIdx.y, P);
+    encode_b_tc_body<MODE>(blockIdx.x, blockIdx.y, at_batch(P, blockIdx.z));
 }
 __global__ void __launch_bounds__(256) encode_b_simt_kernel(const EncBP P) {
-    encode_b_simt_body(blockIdx.x, blockIdx.y, P);
+    encode_b_simt_body(blockIdx.x, blockIdx.y, at_batch(P, blockIdx.z));
 }
 template <int MODE>
 __global__ void __launch_bounds__(256, 4) encode_ab_kernel(const EncAP PA, const EncBP PB, const int nblk_b) {
     griddep_launch_dependents();
     const int i = blockIdx.x;
     if (i < nblk_b) {
-        if constexpr (MODE == 2) encode_b_simt_body(i % PB.nkc, i / PB.nkc, PB);
-        else encode_b_tc_body<MODE>(i % PB.nkc, i / PB.nkc, PB);
+        const EncBP pb = at_batch(PB, blockIdx.y);
+        if constexpr (MODE == 2) encode_b_simt_body(i % pb.nkc, i / pb.nkc, pb);
+        else encode_b_tc_body<MODE>(i % pb.nkc, i / pb.nkc, pb);
     } else {
         const int j = i - nblk_b;
-        encode_a_body<MODE>(j % PA.nkc, j / PA.nkc, PA);
+        const EncAP pa = at_batch(PA, blockIdx.y);
+        encode_a_body<MODE>(j % pa.nkc, j / pa.nkc, pa);
     }
 }
 
@@ -669,7 +697,7 @@ __global__ void __launch_bounds__(256, 4) encode_ab_kernel(const EncAP PA, const
 
 cudaError_t launch_encode(const Geometry& g, const EncLayout& L, int64_t M, int64_t N, int64_t K,
                           const void* A, int64_t lda, const void* B, int64_t ldb, void* enc, int which,
-                          cudaStream_t st) {
+                          cudaStream_t st, int batch, int64_t sA, int64_t sB, int64_t sE) {
     char* base = reinterpret_cast<char*>(enc);
     const int mode = g.dtype == FTGEMM_BF16 ? 0 : (g.dtype == FTGEMM_TF32 ? 1 : 2);
     auto F = [&](size_t off) { return reinterpret_cast<float*>(base + off); };
@@ -679,32 +707,35 @@ cudaError_t launch_encode(const Geometry& g, const EncLayout& L, int64_t M, int6
     if (which & 2) {
         // tickets of the last-block norm reduction (self-resetting; zeroed here
         // because enc_ws is caller memory of unknown content)
-        if ((e = cudaMemsetAsync(base + L.cnt_b, 0, sizeof(int) * (size_t)g.tiles_n, st)) != cudaSuccess) return e;
+        if ((e = cudaMemset2DAsync(base + L.cnt_b, (size_t)(batch > 1 ? sE : (int64_t)sizeof(int) * g.tiles_n), 0, sizeof(int) * (size_t)g.tiles_n,
+                                   (size_t)batch, st)) != cudaSuccess) return e;
         uint8_t* Bt = (mode == 2 || (which & 4)) ? nullptr : reinterpret_cast<uint8_t*>(base + L.bt);   // 4: no encoded operand
         pb = EncBP{B, ldb, (int)N, (int)K, g.bnd, g.bn, g.kp, g.tiles_n * g.bn, g.nkc_b, g.enc_b_rows,
-                   F(L.br), Bt, F(L.cn2), F(L.brn2), reinterpret_cast<int*>(base + L.cnt_b), F(L.colnorm), F(L.brnorm)};
+                   F(L.br), Bt, F(L.cn2), F(L.brn2), reinterpret_cast<int*>(base + L.cnt_b), F(L.colnorm), F(L.brnorm),
+                   sB, sE};
     }
     if (which & 1) {
-        if ((e = cudaMemsetAsync(base + L.cnt_a, 0, sizeof(int) * (size_t)g.tiles_m, st)) != cudaSuccess) return e;
+        if ((e = cudaMemset2DAsync(base + L.cnt_a, (size_t)(batch > 1 ? sE : (int64_t)sizeof(int) * g.tiles_m), 0, sizeof(int) * (size_t)g.tiles_m,
+                                   (size_t)batch, st)) != cudaSuccess) return e;
         pa = EncAP{A, lda, (int)M, (int)K, g.bmd, g.kp, g.bk, g.nkc_a, F(L.ac), reinterpret_cast<uint8_t*>(base + L.y),
-                   F(L.rn2), F(L.acn2), reinterpret_cast<int*>(base + L.cnt_a), F(L.rownorm), F(L.acnorm)};
+                   F(L.rn2), F(L.acn2), reinterpret_cast<int*>(base + L.cnt_a), F(L.rownorm), F(L.acnorm), sA, sE};
     }
     if ((which & 3) == 3) {                      // both operands: one launch
         const int nb = g.nkc_b * g.tiles_n, na = g.nkc_a * g.tiles_m;
-#define ENC_AB(MD) encode_ab_kernel<MD><<<nb + na, 256, 0, st>>>(pa, pb, nb)
+#define ENC_AB(MD) encode_ab_kernel<MD><<<dim3(nb + na, batch), 256, 0, st>>>(pa, pb, nb)
         if (mode == 0) ENC_AB(0); else if (mode == 1) ENC_AB(1); else ENC_AB(2);
 #undef ENC_AB
         return cudaGetLastError();
     }
     if (which & 2) {
-        dim3 grid(g.nkc_b, g.tiles_n);
+        dim3 grid(g.nkc_b, g.tiles_n, batch);
         if (mode == 2) encode_b_simt_kernel<<<grid, 256, 0, st>>>(pb);
         else if (mode == 0) encode_b_tc_kernel<0><<<grid, 256, 0, st>>>(pb);
         else encode_b_tc_kernel<1><<<grid, 256, 0, st>>>(pb);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (which & 1) {
-        dim3 grid(g.nkc_a, g.tiles_m);
+        dim3 grid(g.nkc_a, g.tiles_m, batch);
         if (mode == 0) encode_a_kernel<0><<<grid, 256, 0, st>>>(pa);
         else if (mode == 1) encode_a_kernel<1><<<grid, 256, 0, st>>>(pa);
         else encode_a_kernel<2><<<grid, 256, 0, st>>>(pa);

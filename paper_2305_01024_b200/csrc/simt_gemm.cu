@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(256, FTGEMM_SIMT_MINB) simt_ftgemm_kernel(cons
     float (*brs)[SK] = reinterpret_cast<float (*)[SK]>(simt_dsmem + NST * SB * SKP + NST * SK * SB + NST * SK);
     __shared__ float red_col[8][SB];                   // column partial sums per warp
     __shared__ float srow_s[SB], rref_s[SB], cref_s[SB], rres[SB], rtau[SB], cres[SB], ctau[SB];
-    __shared__ int sflag[5];
+    __shared__ int sflag[6];
     __shared__ DevInject sinj[8];
     __shared__ int s_ninj;
 
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(256, FTGEMM_SIMT_MINB) simt_ftgemm_kernel(cons
     int kind = 0, pstar = -1, qstar = -1;
     if (FT) {
         // ---- verification ----
-        if (tid == 0) { sflag[0] = 0; sflag[1] = 0; sflag[2] = 1 << 30; sflag[3] = 1 << 30; }
+        if (tid == 0) { sflag[0] = 0; sflag[1] = 0; sflag[2] = 1 << 30; sflag[3] = 1 << 30; sflag[5] = 0; }
         float rs[8], cs[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -313,6 +313,7 @@ __global__ void __launch_bounds__(256, FTGEMM_SIMT_MINB) simt_ftgemm_kernel(cons
         }
         if (tid < SB) rref_s[tid] = ref; else cref_s[tid - SB] = ref;
         __syncthreads();
+        unsigned margin = 0u;        // largest |r| / tau among unflagged residuals (telemetry)
         if (tid < SB) {
             const int p = tid;
             if (p < bm) {
@@ -322,6 +323,7 @@ __global__ void __launch_bounds__(256, FTGEMM_SIMT_MINB) simt_ftgemm_kernel(cons
                                             a.tau_l2 * __ldg(a.rownorm + r0 + p) * __ldg(a.brnorm + tj));
                 rres[p] = r; rtau[p] = tr;
                 if (!(fabsf(r) <= tr)) { atomicAdd(&sflag[0], 1); atomicMin(&sflag[2], p); }
+                else if (tr > 0.0f) margin = __float_as_uint(fabsf(r) / tr);
             }
         } else {
             const int q = tid - SB;
@@ -335,9 +337,13 @@ __global__ void __launch_bounds__(256, FTGEMM_SIMT_MINB) simt_ftgemm_kernel(cons
                                             a.tau_l2 * __ldg(a.acnorm + ti) * __ldg(a.colnorm + c0 + q));
                 cres[q] = c; ctau[q] = tc;
                 if (!(fabsf(c) <= tc)) { atomicAdd(&sflag[1], 1); atomicMin(&sflag[3], q); }
+                else if (tc > 0.0f) margin = __float_as_uint(fabsf(c) / tc);
             }
         }
+        margin = __reduce_max_sync(0xffffffffu, margin);
+        if ((tid & 31) == 0 && margin) atomicMax(reinterpret_cast<unsigned*>(&sflag[5]), margin);
         __syncthreads();
+        if (tid == 0 && sflag[5]) atomicMax(&a.rep->max_ratio_bits, (unsigned)sflag[5]);
         const int nr = sflag[0], nc = sflag[1];
         pstar = nr ? sflag[2] : -1;
         qstar = nc ? sflag[3] : -1;

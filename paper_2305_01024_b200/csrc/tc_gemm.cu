@@ -203,8 +203,8 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             mbar_init(&yrdy[s], 2 * CG);         // both encoder warps of both CTAs
         }
         for (int b = 0; b < 2; ++b) {
-            mbar_init(&nrdy[b], 2);
-            mbar_init(&nfree[b], 4);
+            mbar_init(&nrdy[b], 64);             // every lane of the two encoder warps
+            mbar_init(&nfree[b], 128);           // every lane of the tile's epilogue warpgroup
         }
         fence_barrier_init();
     }
@@ -237,8 +237,10 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                                      : fa ? Cfg::B_BYTES : (Cfg::BMD * 128 + Cfg::Y_BYTES + Cfg::B_BYTES);
 #endif
             for (int u = cluster_id; u < a.num_units; u += num_clusters) {
+                // batched launches: unit u = problem bb's unit ul (problems back to back)
+                const int bb = u / a.units_pb, ul = u - bb * a.units_pb;
                 int tmu, tj;
-                tile_coords(u, a.units_m, a.tiles_n, a.group, tmu, tj);
+                tile_coords(ul, a.units_m, a.tiles_n, a.group, tmu, tj);
                 const int ti = tmu * CG + (int)rank;
                 const int row0 = ti * Cfg::BMD;
                 const int colb = tj * BN + (int)rank * (BN / CG);
@@ -249,32 +251,32 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     uint8_t* sb = sa + Cfg::A_BYTES;
                     if (fa) {
                         mbar_arrive_expect_tx(&afull[s], Cfg::BMD * 128);
-                        tma_load_2d(sa, &tmA, &afull[s], kb * Cfg::BK, row0);
+                        tma_load_3d(sa, &tmA, &afull[s], kb * Cfg::BK, row0, bb);
                     }
                     if constexpr (CG == 1) {
-                        if (!fa) tma_load_2d(sa, &tmA, &full[s], kb * Cfg::BK, row0);
+                        if (!fa) tma_load_3d(sa, &tmA, &full[s], kb * Cfg::BK, row0, bb);
 #if !defined(FTGEMM_EXP_A128)
-                        if (FT && !fa) tma_load_2d(sa + Cfg::BMD * 128, &tmY, &full[s], 0, ti * a.num_kb + kb);
+                        if (FT && !fa) tma_load_3d(sa + Cfg::BMD * 128, &tmY, &full[s], 0, ti * a.num_kb + kb, bb);
 #endif
                         if (b3d) {
-                            tma_load_3d(sb, &tmB, &full[s], 0, kb * Cfg::BK, colb / Cfg::BOXN);
+                            tma_load_4d(sb, &tmB, &full[s], 0, kb * Cfg::BK, colb / Cfg::BOXN, bb);
                         } else {
 #pragma unroll
                             for (int b = 0; b < Cfg::NBOX; ++b)
-                                tma_load_2d(sb + b * Cfg::B_BOX_BYTES, &tmB, &full[s], colb + b * Cfg::BOXN, kb * Cfg::BK);
+                                tma_load_3d(sb + b * Cfg::B_BOX_BYTES, &tmB, &full[s], colb + b * Cfg::BOXN, kb * Cfg::BK, bb);
                         }
                     } else {
                         const uint32_t mb = smem_u32(&full[s]) & kPeerBitMask;
-                        if (!fa) tma_load_2d_pair(sa, &tmA, mb, kb * Cfg::BK, row0);
+                        if (!fa) tma_load_3d_pair(sa, &tmA, mb, kb * Cfg::BK, row0, bb);
 #if !defined(FTGEMM_EXP_A128)
-                        if (FT && !fa) tma_load_2d_pair(sa + Cfg::BMD * 128, &tmY, mb, 0, ti * a.num_kb + kb);
+                        if (FT && !fa) tma_load_3d_pair(sa + Cfg::BMD * 128, &tmY, mb, 0, ti * a.num_kb + kb, bb);
 #endif
                         if (b3d) {
-                            tma_load_3d_pair(sb, &tmB, mb, 0, kb * Cfg::BK, colb / Cfg::BOXN);
+                            tma_load_4d_pair(sb, &tmB, mb, 0, kb * Cfg::BK, colb / Cfg::BOXN, bb);
                         } else {
 #pragma unroll
                             for (int b = 0; b < Cfg::NBOX / CG; ++b)
-                                tma_load_2d_pair(sb + b * Cfg::B_BOX_BYTES, &tmB, mb, colb + b * Cfg::BOXN, kb * Cfg::BK);
+                                tma_load_3d_pair(sb + b * Cfg::B_BOX_BYTES, &tmB, mb, colb + b * Cfg::BOXN, kb * Cfg::BK, bb);
                         }
                     }
                     if (++s == S) { s = 0; ph ^= 1; }
@@ -469,7 +471,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 }
                 if (lane == 0) acsq[acc * 2 + half] = asq;
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&nrdy[acc]);     // release: the epilogue of this tile may read them
+                mbar_arrive(&nrdy[acc]);                    // release (each lane its own writes): the epilogue may read
             }
         }
     } else if (warp >= W_EPI0 && warp < W_EPI0 + kEpiWarps) {
@@ -499,8 +501,9 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             else mbar_arrive_cluster(mapa_shared(smem_u32(bar), 0));
         };
         for (int t = cluster_id; t < a.num_units; t += num_clusters, ++lt) {
+            const int bb = t / a.units_pb;                     // problem of a batched launch
             int tmu, tj;
-            tile_coords(t, a.units_m, a.tiles_n, a.group, tmu, tj);
+            tile_coords(t - bb * a.units_pb, a.units_m, a.tiles_n, a.group, tmu, tj);
             const int ti = tmu * CG + (int)rank;
             const int r0 = ti * Cfg::BMD, c0 = tj * Cfg::BND;
             const bool has_rows = r0 < a.M;                    // the pair's second tile may lie beyond M
@@ -514,14 +517,15 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             // norms for this tile's thresholds, fetched before the accumulator is ready
             float nrow = 0.f, nbr = 0.f, nac = 0.f, ncol[2] = {0.f, 0.f};
             if (FT && has_rows) {
+                const int64_t eo = (int64_t)bb * a.enc_bs;     // this problem's encode (floats)
                 if (!a.fuse_a) {
-                    if (rloc < bm) nrow = __ldg(a.rownorm + r0 + rloc);
-                    nac = __ldg(a.acnorm + ti);
+                    if (rloc < bm) nrow = __ldg(a.rownorm + eo + r0 + rloc);
+                    nac = __ldg(a.acnorm + eo + ti);
                 }
-                nbr = __ldg(a.brnorm + tj);
+                nbr = __ldg(a.brnorm + eo + tj);
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
-                    if (et + 128 * h < bn) ncol[h] = __ldg(a.colnorm + c0 + et + 128 * h);
+                    if (et + 128 * h < bn) ncol[h] = __ldg(a.colnorm + eo + c0 + et + 128 * h);
             }
 
             // Verification of the accumulator in TMEM:
@@ -536,7 +540,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 // every reader of sflag / residual arrays is done
                 if (lane == 0) bulk_wait_read0();
                 named_bar_sync(ebar, 128);
-                if (et == 0) { sflag[0] = 0; sflag[1] = 0; sflag[2] = 1 << 30; sflag[3] = 1 << 30; }
+                if (et == 0) { sflag[0] = 0; sflag[1] = 0; sflag[2] = 1 << 30; sflag[3] = 1 << 30; sflag[5] = 0; }
                 const bool rvalid = rloc < bm;
                 const bool isref = rloc >= Cfg::BMD;      // lanes 29..31 of warp 3: split rows of e^T A B
                 const bool all_rows = ew < 3 && bm >= (ew + 1) * 32;   // warp-uniform: no row of this warp masked
@@ -663,11 +667,15 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 }
                 named_bar_sync(ebar, 128);
                 // ---- row residuals ----
+                // (threshold margin telemetry: the largest |r| / tau among the
+                // unflagged residuals, one shared atomic per warp)
+                unsigned margin = 0u;
                 if (rvalid) {
                     const float r = srow - rref;
                     const float tr = a.tau_u * (a.tau_l1 * sqrtk * fabsf(rref) + a.tau_l2 * nrow * nbr);
                     rres[rloc] = r; rtau[rloc] = tr;
                     if (!(fabsf(r) <= tr)) { atomicAdd(&sflag[0], 1); atomicMin(&sflag[2], rloc); }
+                    else if (tr > 0.0f) margin = __float_as_uint(fabsf(r) / tr);
                 }
                 // ---- column residuals ----
 #pragma unroll
@@ -680,8 +688,11 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         const float tc = a.tau_u * (a.tau_l1 * sqrtk * fabsf(rc) + a.tau_l2 * nac * ncol[h]);
                         cres[col] = c; ctau[col] = tc;
                         if (!(fabsf(c) <= tc)) { atomicAdd(&sflag[1], 1); atomicMin(&sflag[3], col); }
+                        else if (tc > 0.0f) margin = max(margin, __float_as_uint(fabsf(c) / tc));
                     }
                 }
+                margin = __reduce_max_sync(0xffffffffu, margin);
+                if (lane == 0 && margin) atomicMax(reinterpret_cast<unsigned*>(&sflag[5]), margin);
                 named_bar_sync(ebar, 128);
                 // ---- decide (R3-R5) ----
                 const int nr = sflag[0], nc = sflag[1];
@@ -723,6 +734,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 }
                 if (et == 0) {
                     ++n_checked;
+                    if (sflag[5]) atomicMax(&a.rep->max_ratio_bits, (unsigned)sflag[5]);
                     if (kind) {
                         unsigned long long* cnt = a.rep->counts;
                         atomicAdd(&cnt[CNT_DETECTED], 1ull);
@@ -734,9 +746,10 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         const unsigned long long slot = atomicAdd(&cnt[CNT_EVENTS], 1ull);
                         if (slot < (unsigned long long)kMaxEvents) {
                             ftgemm_event_t& e = a.rep->events[slot];
-                            e.row = pstar >= 0 ? (int64_t)(r0 + pstar) : -1;
+                            // batched: rows / tile rows of the stacked (batch x M) x N view
+                            e.row = pstar >= 0 ? (int64_t)bb * a.M + r0 + pstar : -1;
                             e.col = qstar >= 0 ? (int64_t)(c0 + qstar) : -1;
-                            e.tile_m = ti; e.tile_n = tj; e.kind = kind;
+                            e.tile_m = bb * a.tiles_m + ti; e.tile_n = tj; e.kind = kind;
                             e.n_rows = nr; e.n_cols = kind == FTGEMM_EV_DETECTED ? 0 : nc; e.k_checked = kchk;
                             e.resid_row = pstar >= 0 ? rres[pstar] : 0.0f;
                             e.resid_col = qstar >= 0 ? cres[qstar] : 0.0f;
@@ -812,8 +825,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 mbar_wait(&nrdy[acc], accph);
                 nrow = sqrtf(nsq[acc * 256 + rloc] + nsq[acc * 256 + 128 + rloc]);
                 nac = sqrtf(acsq[acc * 2] + acsq[acc * 2 + 1]);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&nfree[acc]);
+                mbar_arrive(&nfree[acc]);                   // each lane releases its own reads
             }
             if (!has_rows) {                                   // padding half of the last pair row
                 __syncwarp();
@@ -869,7 +881,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     for (int i = 0; i < 4; ++i) x[i] = (qs == lo + i) ? corr : x[i];
                 }
                 if (row_ok && lo < bn) {
-                    uint16_t* Cp = reinterpret_cast<uint16_t*>(a.C) + (int64_t)(r0 + trow) * a.ldc + c0 + lo;
+                    uint16_t* Cp = reinterpret_cast<uint16_t*>(a.C) + (int64_t)bb * a.c_bs + (int64_t)(r0 + trow) * a.ldc + c0 + lo;
                     float o4[4];
 #pragma unroll
                     for (int i = 0; i < 4; ++i)
@@ -937,7 +949,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 if (a.beta != 0.0f) {
                     if (lane == 0) {
                         mbar_arrive_expect_tx(cbw, (FT && ew == 3 ? 29 : 32) * 128);
-                        tma_load_2d(sbuf, cmap, cbw, gcol, grow);
+                        tma_load_3d(sbuf, cmap, cbw, gcol, grow, bb);
                     }
                     mbar_wait(cbw, cph);
                     cph ^= 1;
@@ -985,7 +997,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 __syncwarp();
                 if (lane == 0) {
 #if !defined(FTGEMM_EXP_NO_STORE)
-                    tma_store_2d(cmap, sbuf, gcol, grow);
+                    tma_store_3d(cmap, sbuf, gcol, grow, bb);
 #endif
                     bulk_commit();
                 }

@@ -41,7 +41,8 @@ class Event(C.Structure):
 
 class Counts(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("tiles_checked", "tiles_detected", "corrected", "checksum_only",
-                                         "uncorrectable", "located", "events", "dropped")]
+                                         "uncorrectable", "located", "events", "dropped")] + \
+               [("max_resid_ratio", C.c_float), ("pad", C.c_int32)]
 
 
 class PlanStruct(C.Structure):
@@ -65,7 +66,8 @@ class Cost(C.Structure):
 
 SYMBOLS = ("ftgemm_plan", "ftgemm_encode", "ftgemm_encode_layout", "ftgemm_run", "ftgemm_run_fused", "ftgemm_run_online", "ftgemm_run_offline", "ftgemm_cost_model",
            "ftgemm_nonfused_workspace", "ftgemm_run_nonfused",
-           "ftgemm_report", "ftgemm_report_reset", "ftgemm_last_error", "ftgemm_version", "ftgemm_device_arch")
+           "ftgemm_report", "ftgemm_report_reset", "ftgemm_last_error", "ftgemm_version", "ftgemm_device_arch",
+           "ftgemm_plan_batched", "ftgemm_encode_batched", "ftgemm_run_batched")
 DTYPE_MASK = 0xFF
 
 
@@ -101,6 +103,10 @@ def lib():
         L.ftgemm_run_nonfused.argtypes = [C.c_int, i64, i64, i64, C.c_float, vp, i64, vp, i64, C.c_float, vp, i64,
                                           vp, vp, C.c_int, vp, i32, vp, vp]
         L.ftgemm_report.argtypes = [vp, C.POINTER(Counts), vp, i32, vp]
+        L.ftgemm_plan_batched.argtypes = [C.c_int, i64, i64, i64, i64, C.POINTER(PlanStruct)]
+        L.ftgemm_encode_batched.argtypes = [C.c_int, i64, i64, i64, i64, vp, i64, i64, vp, i64, i64, vp, i64, C.c_int, vp]
+        L.ftgemm_run_batched.argtypes = [C.c_int, i64, i64, i64, i64, C.c_float, vp, i64, i64, vp, i64, i64, C.c_float,
+                                         vp, i64, i64, vp, i64, C.c_int, vp, i32, vp, vp]
         L.ftgemm_report_reset.argtypes = [vp, i64, vp]
         L.ftgemm_last_error.restype = C.c_char_p
         for n in SYMBOLS:
@@ -321,7 +327,7 @@ def report(report_ws: torch.Tensor, max_events: int = 4096, stream=None):
     evs = (Event * max(1, max_events))()
     _check(lib().ftgemm_report(report_ws.data_ptr(), C.byref(cnt), C.cast(evs, C.c_void_p), max_events,
                                _stream(stream)), "ftgemm_report")
-    counts = {f: getattr(cnt, f) for f, _ in Counts._fields_}
+    counts = {f: getattr(cnt, f) for f, _ in Counts._fields_ if f != "pad"}
     out = []
     for i in range(min(counts["events"], max_events)):
         e = evs[i]
@@ -411,3 +417,68 @@ class FTGemm:
     @property
     def enc_a(self) -> torch.Tensor:
         return self.enc_ws[:self.plan.enc_b_offset]
+
+
+# ------------------------------------------------------------------ batched ---
+def plan_batched(dtype, batch: int, M: int, N: int, K: int, tile: tuple[int, int] | None = None) -> Plan:
+    if tile is not None:
+        dtype = tile_code(dtype, *tile)
+    p = PlanStruct()
+    _check(lib().ftgemm_plan_batched(_dt(dtype), batch, M, N, K, C.byref(p)), "ftgemm_plan_batched")
+    return Plan(**{f: getattr(p, f) for f in Plan.__dataclass_fields__})
+
+
+def _batch_operand(name, t, dtype, batch, rows, cols):
+    """A 3-D CUDA tensor [batch, rows, cols] with contiguous rows (stride(2) == 1)."""
+    want = _TORCH_DT[_dt(dtype) & DTYPE_MASK]
+    if not isinstance(t, torch.Tensor) or t.dim() != 3 or not t.is_cuda or t.dtype != want:
+        raise ValueError(f"{name}: expected a 3-D CUDA tensor of {want}")
+    if tuple(t.shape) != (batch, rows, cols):
+        raise ValueError(f"{name}: shape {tuple(t.shape)}, expected {(batch, rows, cols)}")
+    if t.stride(2) != 1 or t.stride(1) < cols:
+        raise ValueError(f"{name}: rows must be contiguous")
+
+
+class FTGemmBatched:
+    """`batch` independent (M, N, K) problems in one persistent launch
+    (ftgemm_run_batched).  A: [batch, M, K], B: [batch, K, N] (a stride-0
+    expand of one B is allowed), C: [batch, M, N]; one encode workspace per
+    problem in a single buffer."""
+
+    def __init__(self, dtype, batch: int, M: int, N: int, K: int, device="cuda", tile: tuple[int, int] | None = None):
+        self.batch, self.M, self.N, self.K = batch, M, N, K
+        self.plan = plan_batched(dtype, batch, M, N, K, tile=tile)
+        self.dtype = self.plan.dtype
+        self.enc_stride = (self.plan.enc_bytes + 255) // 256 * 256
+        self.enc_ws = torch.empty(self.enc_stride * batch, dtype=torch.uint8, device=device)
+        self.report_ws = torch.zeros(self.plan.report_bytes, dtype=torch.uint8, device=device)
+
+    def encode(self, A=None, B=None, which: int = 3, stream=None):
+        if which & 1:
+            _batch_operand("A", A, self.dtype, self.batch, self.M, self.K)
+        if which & 2:
+            _batch_operand("B", B, self.dtype, self.batch, self.K, self.N)
+        _check(lib().ftgemm_encode_batched(
+            self.dtype, self.batch, self.M, self.N, self.K,
+            A.data_ptr() if A is not None else None, A.stride(1) if A is not None else self.K,
+            A.stride(0) if A is not None else 0,
+            B.data_ptr() if B is not None else None, B.stride(1) if B is not None else self.N,
+            B.stride(0) if B is not None else 0,
+            self.enc_ws.data_ptr(), self.enc_stride, which, _stream(stream)), "ftgemm_encode_batched")
+
+    def run(self, A, B, C_, *, alpha=1.0, beta=0.0, ft_level=FT_CORRECT, injections=(), stream=None):
+        _batch_operand("A", A, self.dtype, self.batch, self.M, self.K)
+        _batch_operand("B", B, self.dtype, self.batch, self.K, self.N)
+        _batch_operand("C", C_, self.dtype, self.batch, self.M, self.N)
+        arr, n = _inj_array(injections)
+        _check(lib().ftgemm_run_batched(
+            self.dtype, self.batch, self.M, self.N, self.K, alpha, A.data_ptr(), A.stride(1), A.stride(0),
+            B.data_ptr(), B.stride(1), B.stride(0), beta, C_.data_ptr(), C_.stride(1), C_.stride(0),
+            self.enc_ws.data_ptr(), self.enc_stride, ft_level, C.cast(arr, C.c_void_p) if arr is not None else None,
+            n, self.report_ws.data_ptr(), _stream(stream)), "ftgemm_run_batched")
+
+    def report(self, max_events: int = 4096, stream=None):
+        return report(self.report_ws, max_events, stream)
+
+    def reset(self, stream=None):
+        report_reset(self.report_ws, stream)

@@ -38,7 +38,7 @@ def test_library_exports_every_declared_symbol(F):
     lib = F.lib()
     for s in declared_symbols():
         assert hasattr(lib, s), s
-    assert lib.ftgemm_version() == 1
+    assert lib.ftgemm_version() == 2
     assert lib.ftgemm_device_arch() == 1000
 
 
@@ -65,7 +65,7 @@ def test_struct_layouts(F, tmp_path):
     got = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()))
     assert got == [C.sizeof(F.Inject), C.sizeof(F.Event), C.sizeof(F.Counts), C.sizeof(F.PlanStruct),
                    F.PlanStruct.tiles_m.offset, F.PlanStruct.u_acc.offset]
-    assert got[:3] == [40, 56, 64]
+    assert got[:3] == [40, 56, 72]
 
 
 @pytest.mark.parametrize("dtype", ["f32_simt", "tf32", "bf16"])
