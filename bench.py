@@ -46,7 +46,7 @@ ERRORS_PER_MIN = 500.0                    # "hundreds of errors per minute" (nor
 SWEEP_RATES = (0.0, 1.0, 10.0, 100.0, 500.0)
 FAULTS_PER_CALL = (0, 1, 10, 100, -1)     # -1: one fault in every check tile
 OFFLINE_GAMMA0 = (1e-5, 1e-4, 2e-4)       # per-tile error probability per execution (online vs offline)
-BURST_WINDOW_S = 0.25                     # timed regions shorter than this run at burst clocks
+BURST_WINDOW_S = 0.25                     # without clock samples: regions shorter than this run at burst clocks
 SIMT_FFMA_PEAK = 148 * 128 * 2 * 1.965e9 / 1e12   # FP32 FFMA: SMs x FMA lanes x 2 x max clock
 
 
@@ -294,7 +294,13 @@ def roofline(peaks, kind, achieved_tflops, window_s, clk, traffic, kernel, flops
     scale = 0.5 if tf32 else 1.0                        # TF32 dense = BF16 x 1/2 (guide's nominal ratio)
     burst = peaks["bf16_tflops"] * scale
     sus = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) * scale
-    regime = "burst" if window_s < BURST_WINDOW_S else "sustained"
+    # the clock regime the region actually ran in: power-capped (sustained) when
+    # the sampled median SM clock sits below 90 % of its max, else burst; with
+    # too few samples (a short region), by the region's length
+    if clk.get("samples", 0) >= 3 and clk.get("sm_mhz") and clk.get("sm_max_mhz"):
+        regime = "sustained" if clk["sm_mhz"] < 0.9 * clk["sm_max_mhz"] else "burst"
+    else:
+        regime = "burst" if window_s < BURST_WINDOW_S else "sustained"
     peak = burst if regime == "burst" else sus
     return {"bound": "tensor", "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved_tflops / peak, "traffic": traffic, "kernel": kernel,

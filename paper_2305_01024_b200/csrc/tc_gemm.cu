@@ -69,6 +69,7 @@ struct TcCfg {
     static constexpr int STG_BYTES = 4 * 2 * 4096;     // per epilogue warpgroup (see below)
     static constexpr int EPI_BYTES = EPI_WG * STG_BYTES;
     static constexpr int MISC_BYTES = 2048;            // barriers, TMEM address, in-kernel-encode norms
+    static_assert((4 * 8 + 8 + 4 * EPI_WG) * 8 + 16 + (2 * 128 + 2) * 4 <= MISC_BYTES, "misc shared memory");
     static constexpr int STAGE_FIT = (227 * 1024 - 1024 - MISC_BYTES - EPI_BYTES) / (A_BYTES + B_BYTES);
     static constexpr int STAGES = STAGE_FIT < 8 ? STAGE_FIT : 8;
     static constexpr int BMD = FT ? BM - 3 : BM;   // data rows of a check tile
@@ -154,11 +155,11 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     uint64_t* cbar = inj_done + 2;      // [4 kEpiWG]  C_in tile loads (beta != 0), one per epilogue warp
     uint64_t* afull = cbar + 4 * kEpiWG;  // [S]  in-kernel encode: this CTA's A tile landed
     uint64_t* yrdy = afull + S;           // [S]  in-kernel encode: split rows of e^T A written (leader's)
-    uint64_t* nrdy = yrdy + S;            // [2]  in-kernel encode: row / tile norms of the tile written
-    uint64_t* nfree = nrdy + 2;           // [2]  ... and read by the epilogue (slot reusable)
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(nfree + 2);
-    float* nsq = reinterpret_cast<float*>(tmem_holder + 4);   // [2 acc][2 half][128] row sums of squares
-    float* acsq = nsq + 2 * 2 * 128;                          // [2 acc][2 half] sum of (e^T A)^2
+    uint64_t* nrdy = yrdy + S;            // [1]  in-kernel encode: row / tile norms of the tile written
+    uint64_t* nfree = nrdy + 1;           // [1]  ... and read by the epilogue (slot reusable)
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(nfree + 1);
+    float* nsq = reinterpret_cast<float*>(tmem_holder + 4);   // [2 half][128] row sums of squares (one tile)
+    float* acsq = nsq + 2 * 128;                              // [2 half] sum of (e^T A)^2
 
     const int warp = threadIdx.x >> 5;
     // Warp roles.  The SM sub-partition scheduler favours the highest warp id
@@ -202,10 +203,8 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             mbar_init(&afull[s], 1);
             mbar_init(&yrdy[s], 2 * CG);         // both encoder warps of both CTAs
         }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(&nrdy[b], 64);             // every lane of the two encoder warps
-            mbar_init(&nfree[b], 128);           // every lane of the tile's epilogue warpgroup
-        }
+        mbar_init(&nrdy[0], 64);                 // every lane of the two encoder warps
+        mbar_init(&nfree[0], 128);               // every lane of the tile's epilogue warpgroup
         fence_barrier_init();
     }
     if (warp == W_ALLOC) tmem_alloc<Cfg::TMEM_COLS, CG>(tmem_holder);
@@ -322,42 +321,55 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 int evt = FT ? next_event(-1) : 0x7fffffff;
                 // two instantiations of the k-loop: the lean one (no hand-off, no
                 // in-kernel encode -- the common case) carries no per-k-block tests
-                auto kloop = [&](auto general_c) {
+                // one k-block: wait for the stage, issue its MMAs, release the stage
+                auto kblock = [&](int kb, auto general_c) {
                     constexpr bool kGeneral = decltype(general_c)::value;
-                    for (int kb = 0; kb < nkb; ++kb) {
-                        mbar_wait(&full[s], ph);
-                        if constexpr (kGeneral) {
-                            if (fuse) mbar_wait(&yrdy[s], ph);     // both CTAs' A tiles + split rows ready
-                        }
-                        tc_fence_after();
-                        const uint32_t sa = smem_u32(stage_base + s * Cfg::STAGE_BYTES);
-                        const uint32_t sb = sa + Cfg::A_BYTES;
-#pragma unroll
-                        for (int kk = 0; kk < Cfg::BK / Cfg::UK; ++kk) {
-                            const uint64_t ad = smem_desc_sw128(sa + kk * 32, 16, 1024);
-                            // B is N-major: bf16 -> SW128 (8-row atoms), tf32 -> SW128_BASE32B (4-row atoms)
-                            const uint64_t bd = kTF32 ? smem_desc_sw128<1>(sb + kk * Cfg::UK * 128, Cfg::B_BOX_BYTES, 512)
-                                                      : smem_desc_sw128<2>(sb + kk * Cfg::UK * 128, Cfg::B_BOX_BYTES, 1024);
-                            umma<kTF32, CG>(d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
-                        }
-                        commit(&empty[s]);
-                        if constexpr (kGeneral) {
-                            if (FT && kb == evt) {
-                                // hand the accumulator to the epilogue warps (of both CTAs) for the
-                                // fault(s) of this k-block and / or the check closing a K_s step
-                                commit(&inj_req[acc]);
-                                mbar_wait(&inj_done[acc], acc ? injph1 : injph0);
-                                if (acc) injph1 ^= 1; else injph0 ^= 1;
-                                tc_fence_after();
-                                while (ii < ie && a.inj[ii].kb == kb) ++ii;
-                                evt = next_event(kb);
-                            }
-                        }
-                        if (++s == S) { s = 0; ph ^= 1; }
+                    mbar_wait(&full[s], ph);
+                    if constexpr (kGeneral) {
+                        if (fuse) mbar_wait(&yrdy[s], ph);     // both CTAs' A tiles + split rows ready
                     }
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(stage_base + s * Cfg::STAGE_BYTES);
+                    const uint32_t sb = sa + Cfg::A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < Cfg::BK / Cfg::UK; ++kk) {
+                        const uint64_t ad = smem_desc_sw128(sa + kk * 32, 16, 1024);
+                        // B is N-major: bf16 -> SW128 (8-row atoms), tf32 -> SW128_BASE32B (4-row atoms)
+                        const uint64_t bd = kTF32 ? smem_desc_sw128<1>(sb + kk * Cfg::UK * 128, Cfg::B_BOX_BYTES, 512)
+                                                  : smem_desc_sw128<2>(sb + kk * Cfg::UK * 128, Cfg::B_BOX_BYTES, 1024);
+                        umma<kTF32, CG>(d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                    }
+                    commit(&empty[s]);
+                    if (++s == S) { s = 0; ph ^= 1; }
                 };
-                if (FT && (fuse || evt != 0x7fffffff)) kloop(std::true_type{});
-                else kloop(std::false_type{});
+                // hand the accumulator to the epilogue warps (of both CTAs) for the
+                // fault(s) of k-block kb and / or the check closing a K_s step
+                auto handoff = [&](int kb) {
+                    commit(&inj_req[acc]);
+                    mbar_wait(&inj_done[acc], acc ? injph1 : injph0);
+                    if (acc) injph1 ^= 1; else injph0 ^= 1;
+                    tc_fence_after();
+                    while (ii < ie && a.inj[ii].kb == kb) ++ii;
+                    evt = next_event(kb);
+                };
+                if (FT && fuse) {
+                    // in-kernel encode: per-k-block split-row barrier and hand-off tests
+                    for (int kb = 0; kb < nkb; ++kb) {
+                        kblock(kb, std::true_type{});
+                        if (kb == evt) handoff(kb);
+                    }
+                } else {
+                    // lean runs of k-blocks between hand-offs: no per-k-block tests in
+                    // the issue loop (a tile with a fault pays only its hand-offs)
+                    int kb = 0;
+                    for (;;) {
+                        const int end = evt < nkb ? evt + 1 : nkb;
+                        for (; kb < end; ++kb) kblock(kb, std::false_type{});
+                        if (kb >= nkb && !(evt < nkb)) break;
+                        handoff(kb - 1);
+                        if (kb >= nkb) break;
+                    }
+                }
                 commit(&tm_full[acc]);
             }
         }
@@ -455,8 +467,9 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
                 // tile end: row sums of squares (4 lanes per row group) and sum of (e^T A)^2
-                const int acc = lt & 1;
-                if (lt >= 2) mbar_wait(&nfree[acc], ((lt >> 1) & 1) ^ 1);   // tile lt-2 read its norms
+                // (one slot: tile lt-1's epilogue read its norms right after its
+                // accumulator completed, long before this tile's mainloop ended)
+                if (lt >= 1) mbar_wait(&nfree[0], (lt - 1) & 1);
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     rsq[i] += __shfl_xor_sync(0xffffffffu, rsq[i], 1);
@@ -467,11 +480,11 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 if (cq == 0) {
 #pragma unroll
                     for (int i = 0; i < 16; ++i)
-                        if (rg + 8 * i < 128) nsq[(acc * 2 + half) * 128 + rg + 8 * i] = rsq[i];
+                        if (rg + 8 * i < 128) nsq[half * 128 + rg + 8 * i] = rsq[i];
                 }
-                if (lane == 0) acsq[acc * 2 + half] = asq;
+                if (lane == 0) acsq[half] = asq;
                 __syncwarp();
-                mbar_arrive(&nrdy[acc]);                    // release (each lane its own writes): the epilogue may read
+                mbar_arrive(&nrdy[0]);                      // release (each lane its own writes): the epilogue may read
             }
         }
     } else if (warp >= W_EPI0 && warp < W_EPI0 + kEpiWarps) {
@@ -822,10 +835,10 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             tc_fence_after();
             if (FT && a.fuse_a) {
                 // norms of the in-kernel encode (the tile's own rows)
-                mbar_wait(&nrdy[acc], accph);
-                nrow = sqrtf(nsq[acc * 256 + rloc] + nsq[acc * 256 + 128 + rloc]);
-                nac = sqrtf(acsq[acc * 2] + acsq[acc * 2 + 1]);
-                mbar_arrive(&nfree[acc]);                   // each lane releases its own reads
+                mbar_wait(&nrdy[0], lt & 1);
+                nrow = sqrtf(nsq[rloc] + nsq[128 + rloc]);
+                nac = sqrtf(acsq[0] + acsq[1]);
+                mbar_arrive(&nfree[0]);                     // each lane releases its own reads
             }
             if (!has_rows) {                                   // padding half of the last pair row
                 __syncwarp();
