@@ -72,9 +72,17 @@ def main():
         lines.append(f"| {i} | `{short}` | {t:.1f} | {rd / 1e6 if m.get('dram__bytes_read.sum', (0, 'byte'))[1] == 'byte' else rd:.1f} | "
                      f"{wr / 1e6 if m.get('dram__bytes_write.sum', (0, 'byte'))[1] == 'byte' else wr:.1f} |")
     s = sum(tot.values()) or 1.0
-    lines += ["", "| kernel | total (us) | share |", "|---|---|---|"]
+    lines += ["", "All launches of the command (incl. the harness's device-side input generation):", "",
+              "| kernel | total (us) | share |", "|---|---|---|"]
     for k, v in sorted(tot.items(), key=lambda x: -x[1]):
         lines.append(f"| `{k}` | {v:.1f} | {100 * v / s:.1f}% |")
+    # the step's kernels: libftgemm's own (namespace ftg)
+    mine = {k: v for k, v in tot.items() if "ftg::" in k}
+    sm = sum(mine.values()) or 1.0
+    lines += ["", "Shares of the step (libftgemm kernels only):", "", "| kernel | total (us) | share of step |",
+              "|---|---|---|"]
+    for k, v in sorted(mine.items(), key=lambda x: -x[1]):
+        lines.append(f"| `{k}` | {v:.1f} | {100 * v / sm:.1f}% |")
     open(os.path.join(PROF, f"{tag}_launches.md"), "w").write("\n".join(lines) + "\n")
     traffic = {}
     for rep in reps:

@@ -38,7 +38,49 @@ def timeit(fn, reps):
     return e0.elapsed_time(e1) / reps
 
 
+def measure_batched(dt, M, N, K, batch):
+    """One persistent launch over the batch (ftgemm_run_batched) vs torch.bmm."""
+    odt = "bf16" if dt == "bf16" else "f32"
+    A = torch.stack([synth.matrix_torch(synth.BASE_SEED + b, M, K, dtype=odt) for b in range(batch)])
+    B = torch.stack([synth.matrix_torch(synth.BASE_SEED + 100 + b, K, N, dtype=odt) for b in range(batch)])
+    C = torch.empty(batch, M, N, dtype=A.dtype, device="cuda")
+    g = F.FTGemmBatched(dt, batch, M, N, K)
+    flops = 2.0 * M * N * K * batch
+    reps = max(3, min(200, int(2e10 / flops) + 1))
+    torch.backends.cuda.matmul.allow_tf32 = dt == "tf32"
+    cfg = {"ft_step": lambda: (g.encode(A, B), g.run(A, B, C)), "ft_run": lambda: g.run(A, B, C),
+           "ft_off": lambda: g.run(A, B, C, ft_level=F.FT_OFF), "encode": lambda: g.encode(A, B),
+           "cublas": lambda: torch.bmm(A, B, out=C),
+           "detect_rows_run": lambda: g.run(A, B, C, ft_level=F.FT_DETECT_ROWS)}
+    g.encode(A, B)
+    samp = {k: [] for k in cfg}
+    for _ in range(3):
+        for k, fn in cfg.items():
+            samp[k].append(timeit(fn, reps))
+    med = {k: statistics.median(v) for k, v in samp.items()}
+    counts, _ = g.report(0)
+    assert counts["tiles_detected"] == 0, counts
+    peak = {"bf16": PEAK_BF16, "tf32": PEAK_BF16 / 2, "f32_simt": 74.4}[dt]
+    out = {"dtype": dt, "M": M, "N": N, "K": K, "batch": batch, "reps": reps, "launch": "one batched launch",
+           "check_tile": [g.plan.check_tile_m, g.plan.check_tile_n], "mma_tile": [g.plan.bm, g.plan.bn, g.plan.bk]}
+    for k, v in med.items():
+        out[f"{k}_ms"] = v
+        if k != "encode":
+            out[f"{k}_tflops"] = flops / (v * 1e-3) / 1e12
+    out["ft_step_frac_of_peak"] = out["ft_step_tflops"] / peak
+    out["ft_run_frac_of_peak"] = out["ft_run_tflops"] / peak
+    out["ft_off_frac_of_peak"] = out["ft_off_tflops"] / peak
+    out["overhead_step_vs_ft_off_pct"] = 100 * (med["ft_step"] - med["ft_off"]) / med["ft_off"]
+    out["overhead_run_vs_ft_off_pct"] = 100 * (med["ft_run"] - med["ft_off"]) / med["ft_off"]
+    out["overhead_step_vs_cublas_pct"] = 100 * (med["ft_step"] - med["cublas"]) / med["cublas"]
+    out["ft_run_io_gbs"] = batch * (M * K + K * N + M * N) * A.element_size() / (med["ft_run"] * 1e-3) / 1e9
+    out["peak_tflops"] = peak
+    return out
+
+
 def measure(dt, M, N, K, batch=1):
+    if batch > 1 and dt != "f32_simt":
+        return measure_batched(dt, M, N, K, batch)
     odt = "bf16" if dt == "bf16" else "f32"
     A = synth.to_torch(synth.matrix(synth.BASE_SEED, M, K, dtype=odt), odt).cuda()
     B = synth.to_torch(synth.matrix(synth.BASE_SEED + 1, K, N, dtype=odt), odt).cuda()
