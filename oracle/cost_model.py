@@ -5,13 +5,13 @@ bench.py's model columns, never by the product path.
 
 The paper's model: C += AB of size M x N is computed by M/m_tb x N/n_tb
 threadblock tiles; each tile's accumulation errs with probability gamma0, so
-the whole call errs with probability (PAPER.md:579)
+the whole call errs with probability (PAPER.md:583)
 
     gamma = 1 - (1 - gamma0)^(M/m_tb * N/n_tb).
 
 Online ABFT corrects on the fly: expected executions 1.  Offline (detect-only)
 ABFT restarts on a detected error, and the paper sums the restart series
-(PAPER.md:579)
+(PAPER.md:583)
 
     E = (1 - gamma) + 2 gamma ((1 - gamma) + 2 gamma (...)) = (1 - gamma) / (1 - 2 gamma),
 
@@ -28,21 +28,21 @@ import random
 
 
 def gamma(gamma0: float, tiles: int) -> float:
-    """Overall error rate of one call, PAPER.md:579 ("gamma = 1-(1-gamma_0)^{M/m x N/n}")."""
+    """Overall error rate of one call, PAPER.md:583 ("gamma = 1-(1-gamma_0)^{M/m x N/n}")."""
     if not (0.0 <= gamma0 < 1.0) or tiles < 1:
         raise ValueError("need 0 <= gamma0 < 1 and tiles >= 1")
     return 1.0 - (1.0 - gamma0) ** tiles
 
 
 def offline_expected_runs(g: float) -> float:
-    """PAPER.md:579: (1 - gamma)(1 + 2 gamma + (2 gamma)^2 + ...) = (1-gamma)/(1-2gamma)."""
+    """PAPER.md:583: (1 - gamma)(1 + 2 gamma + (2 gamma)^2 + ...) = (1-gamma)/(1-2gamma)."""
     if not (0.0 <= g < 0.5):
         raise ValueError("the offline restart series diverges for gamma >= 1/2")
     return (1.0 - g) / (1.0 - 2.0 * g)
 
 
 def online_expected_runs(g: float) -> float:
-    """PAPER.md:579: "the expected computation times ... is just 1"."""
+    """PAPER.md:583: "the expected computation times ... is just 1"."""
     return 1.0
 
 
