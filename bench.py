@@ -359,6 +359,7 @@ def run_single(args, H):
     clocks = ClockSampler(dev.index)
     H.barrier(); torch.cuda.synchronize()
     e0, e1 = H.ev(), H.ev()
+    torch.cuda.nvtx.range_push("timed_steps")
     e0.record(stream)
     for i in range(args.steps):
         g.encode(A, B)
@@ -366,6 +367,7 @@ def run_single(args, H):
         g.run(A, B, C, ft_level=F.FT_CORRECT, injections=sched[i])
         kev[i][1].record(stream)
     e1.record(stream)
+    torch.cuda.nvtx.range_pop()
     e1.synchronize()
     H.barrier(); torch.cuda.synchronize()
     clk = clocks.stop()

@@ -6,7 +6,9 @@ peak = d.get("peak_bf16_tflops")
 L = [f"# Shape sweep ({d.get('gpu')}) — medians of 3 interleaved rounds, CUDA events", "",
      "step = encode + FT run; run = FT run alone (CORRECT, no faults); off = same kernel family FT compiled out;",
      "rows = offline detect-only (row checks); nf = non-fused baseline step (encode + cuBLAS GEMMs + verify kernel).",
-     f"TFLOPS = 2MNK / t.  Peaks: BF16 {peak} (measured burst), TF32 = BF16/2, FP32 SIMT 74.4.", "",
+     f"TFLOPS = 2MNK / t.  Peaks: BF16 {peak} (measured burst), TF32 = BF16/2, FP32 SIMT 74.4.",
+     "Rows whose operands total < 256 MB (2x L2) are timed call by call with an L2 flush before every call;",
+     "larger ones back to back (their operands exceed L2).", "",
      "| cfg | dtype | M | N | K | step ms | run ms | off ms | cuBLAS ms | rows ms | nf step ms | run TFLOPS | run / off | step vs nf |",
      "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
 for r in d["rows"]:
