@@ -1,4 +1,4 @@
-"""Tile-class variants (FTGEMM_BN x FTGEMM_CG) of the FT run at one shape,
+"""Tile-class variants (explicit FTGEMM_TILE(bn, cta_group) codes) of the FT run at one shape,
 interleaved call by call (development timing; never a bench number):
 python tools/bn_sweep.py dtype M N K  "BN:CG" ["BN:CG" ...]"""
 import json
@@ -21,8 +21,7 @@ C = torch.empty(M, N, dtype=A.dtype, device="cuda")
 gs = {}
 for v in variants:
     bn, cg = v.split(":")
-    os.environ["FTGEMM_BN"], os.environ["FTGEMM_CG"] = bn, cg
-    g = F.FTGemm(dt, M, N, K)
+    g = F.FTGemm(dt, M, N, K, tile=(int(bn), int(cg)))
     g.encode(A, B)
     gs[v] = g
 n = int(os.environ.get("NREP", "30"))
@@ -30,8 +29,6 @@ s = torch.cuda.current_stream()
 ev = {v: [] for v in variants}
 for j in range(n + 2):
     for v, g in gs.items():
-        bn, cg = v.split(":")
-        os.environ["FTGEMM_BN"], os.environ["FTGEMM_CG"] = bn, cg
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
         g.run(A, B, C, ft_level=F.FT_CORRECT)

@@ -1,6 +1,7 @@
 """Time the encode kernels (A, B, both) at one shape, GPU-side (20 back-to-back
 calls between two events, so host launch overhead is hidden), for each encode
-variant: python tools/enc_time.py dtype M N K"""
+variant: python tools/enc_time.py dtype M N K  (variants: builds with -DFTGEMM_*
+selected through FTGEMM_LIB; the rows-per-block knob is compile-time since round 2)"""
 import json
 import os
 import sys
@@ -16,7 +17,7 @@ A = (torch.rand(M, K, device="cuda") * 2 - 1).to(tdt)
 B = (torch.rand(K, N, device="cuda") * 2 - 1).to(tdt)
 s = torch.cuda.current_stream()
 elt = A.element_size()
-VARIANTS = {"default": {}, "b_rows128": {"FTGEMM_ENC_B_ROWS": "128"}, "b_rows512": {"FTGEMM_ENC_B_ROWS": "512"}, "b_rows1024": {"FTGEMM_ENC_B_ROWS": "1024"}}
+VARIANTS = {"default": {}}
 for vname, env in VARIANTS.items():
     for k in ("FTGEMM_ENC_B_ROWS",):
         os.environ.pop(k, None)
