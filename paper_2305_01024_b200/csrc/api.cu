@@ -517,6 +517,10 @@ static int run_impl(int code, int64_t M, int64_t N, int64_t K, float alpha, cons
         a.enc_bs = enc_stride / 4;
         a.c_bs = bt.sC;
         a.group = tc_group(a.units_m, p.cta_group);
+        a.fd_upb = FastDiv::make((uint32_t)a.units_pb);
+        a.fd_pg = FastDiv::make((uint32_t)(a.group * a.tiles_n));
+        a.fd_g = FastDiv::make((uint32_t)a.group);
+        a.fd_gt = FastDiv::make((uint32_t)(a.units_m % a.group ? a.units_m % a.group : a.group));
         a.ft_level = ft_level; a.alpha = alpha; a.beta = beta; a.C = C; a.ldc = ldc;
         a.ks_kb = ks > 0 ? (int)std::min<int64_t>(ks / p.bk, num_kb) : 0;
         a.fuse_a = fuse_a;

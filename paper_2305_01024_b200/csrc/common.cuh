@@ -47,6 +47,27 @@ enum { CNT_CHECKED = 0, CNT_DETECTED, CNT_CORRECTED, CNT_CHECKSUM_ONLY, CNT_UNCO
 inline size_t report_bytes() { return sizeof(ReportDev) + (size_t)kMaxInject * sizeof(DevInject); }
 inline size_t report_inject_offset() { return sizeof(ReportDev); }
 
+// ---- division by a launch constant (host-computed multiplier) ---------------
+// q = floor(n / d) = umul64hi(n, ceil(2^64 / d)) for 0 <= n < 2^32, d >= 2 (the
+// error n (m - 2^64/d) / 2^64 < 2^-32 cannot carry past an integer); d == 1 is
+// passed through.  Replaces the per-tile 32-bit divisions of the persistent
+// tile scheduler (a few IMADs instead of ~25 instructions each).
+struct FastDiv {
+    uint64_t m;
+    uint32_t d;
+    static FastDiv make(uint32_t d_) {
+        FastDiv f;
+        f.d = d_ ? d_ : 1u;
+        f.m = f.d > 1 ? (~0ull / f.d) + 1ull : 0ull;
+        return f;
+    }
+#ifdef __CUDACC__
+    __device__ __forceinline__ uint32_t div(uint32_t n) const {
+        return d == 1u ? n : (uint32_t)__umul64hi((uint64_t)n, m);
+    }
+#endif
+};
+
 // ---- kernel arguments (plain data, passed by value) ------------------------
 struct TcArgs {
     int M, N, K, num_kb;
@@ -56,6 +77,7 @@ struct TcArgs {
     int64_t enc_bs;           // encode-workspace stride between problems, in floats
     int64_t c_bs;             // C stride between problems, in elements
     int group;            // M-units per schedule group (tile_coords)
+    FastDiv fd_upb, fd_pg, fd_g, fd_gt;   // units_pb, group x tiles_n, group, last (ragged) group size
     int ft_level;
     int ks_kb;            // > 0: verify after every ks_kb k-blocks too (online-interval mode)
     int fuse_a;           // 1: the A-side encode (split e^T A rows, row / tile norms) runs in the kernel

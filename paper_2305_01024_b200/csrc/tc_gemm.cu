@@ -92,14 +92,16 @@ struct TcCfg {
 // Tile schedule: groups of G consecutive M-tiles are swept across all N-tiles
 // (M-tile fastest), so concurrently running tiles share A rows and B^r slots in
 // L2.  G comes from the host (tc_group(), also used to key fault lists).
-__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int G, int& ti, int& tj) {
-    const int per_group = G * tiles_n;
-    const int grp = t / per_group;
-    const int first = grp * G;
-    const int gsz = min(G, tiles_m - first);
+__device__ __forceinline__ void tile_coords(int t, const TcArgs& a, int& ti, int& tj) {
+    const int per_group = a.group * a.tiles_n;
+    const int grp = (int)a.fd_pg.div((uint32_t)t);
+    const int first = grp * a.group;
+    const bool full = a.units_m - first >= a.group;          // every group but a ragged last one
+    const int gsz = full ? a.group : a.units_m - first;
     const int loc = t - grp * per_group;
-    ti = first + loc % gsz;
-    tj = loc / gsz;
+    const int q = (int)(full ? a.fd_g.div((uint32_t)loc) : a.fd_gt.div((uint32_t)loc));
+    ti = first + (loc - q * gsz);
+    tj = q;
 }
 
 // first index of inj[] with tile >= t (inj sorted by tile, then kb)
@@ -237,9 +239,9 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #endif
             for (int u = cluster_id; u < a.num_units; u += num_clusters) {
                 // batched launches: unit u = problem bb's unit ul (problems back to back)
-                const int bb = u / a.units_pb, ul = u - bb * a.units_pb;
+                const int bb = (int)a.fd_upb.div((uint32_t)u), ul = u - bb * a.units_pb;
                 int tmu, tj;
-                tile_coords(ul, a.units_m, a.tiles_n, a.group, tmu, tj);
+                tile_coords(ul, a, tmu, tj);
                 const int ti = tmu * CG + (int)rank;
                 const int row0 = ti * Cfg::BMD;
                 const int colb = tj * BN + (int)rank * (BN / CG);
@@ -514,9 +516,9 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             else mbar_arrive_cluster(mapa_shared(smem_u32(bar), 0));
         };
         for (int t = cluster_id; t < a.num_units; t += num_clusters, ++lt) {
-            const int bb = t / a.units_pb;                     // problem of a batched launch
+            const int bb = (int)a.fd_upb.div((uint32_t)t);     // problem of a batched launch
             int tmu, tj;
-            tile_coords(t - bb * a.units_pb, a.units_m, a.tiles_n, a.group, tmu, tj);
+            tile_coords(t - bb * a.units_pb, a, tmu, tj);
             const int ti = tmu * CG + (int)rank;
             const int r0 = ti * Cfg::BMD, c0 = tj * Cfg::BND;
             const bool has_rows = r0 < a.M;                    // the pair's second tile may lie beyond M
