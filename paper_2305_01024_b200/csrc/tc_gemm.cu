@@ -49,7 +49,10 @@ namespace ftg {
 #define FTGEMM_EPI_WG 2
 #endif
 
-template <bool kTF32, int BN_, bool FT, int CG_ = 1>
+// EPI_: epilogue warpgroups with FT on, one TMEM accumulator buffer each (2 by
+// default; 3 for the small-K BN = 128 instantiation, where the verification
+// pass bounds the kernel and a third tile in flight hides its latency)
+template <bool kTF32, int BN_, bool FT, int CG_ = 1, int EPI_ = FTGEMM_EPI_WG>
 struct TcCfg {
     static constexpr int CG = CG_;                 // 1: one CTA per MMA; 2: CTA pair (M = 256)
     static constexpr int BM = 128;
@@ -64,17 +67,19 @@ struct TcCfg {
     static constexpr int B_BYTES = (NBOX / CG) * B_BOX_BYTES;   // this CTA's share of the B tile
     static constexpr int Y_BYTES = 384;            // 3 split rows x 128 bytes
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int EPI_WG = FT ? FTGEMM_EPI_WG : 1;
+    static constexpr int EPI_WG = FT ? EPI_ : 1;
+    static constexpr int NACC = EPI_WG > 2 ? EPI_WG : 2;   // TMEM accumulator buffers
+    static_assert(NACC * BN_ <= 512, "accumulator buffers must fit the 512 TMEM columns");
     static constexpr int THREADS = 128 + 128 * EPI_WG;
     static constexpr int STG_BYTES = 4 * 2 * 4096;     // per epilogue warpgroup (see below)
     static constexpr int EPI_BYTES = EPI_WG * STG_BYTES;
     static constexpr int MISC_BYTES = 2048;            // barriers, TMEM address, in-kernel-encode norms
-    static_assert((4 * 8 + 8 + 4 * EPI_WG) * 8 + 16 + (2 * 128 + 2) * 4 <= MISC_BYTES, "misc shared memory");
+    static_assert((4 * 8 + 4 * NACC + 4 * EPI_WG) * 8 + 16 + (2 * 128 + 2) * 4 <= MISC_BYTES, "misc shared memory");
     static constexpr int STAGE_FIT = (227 * 1024 - 1024 - MISC_BYTES - EPI_BYTES) / (A_BYTES + B_BYTES);
     static constexpr int STAGES = STAGE_FIT < 8 ? STAGE_FIT : 8;
     static constexpr int BMD = FT ? BM - 3 : BM;   // data rows of a check tile
     static constexpr int BND = FT ? BN - 4 : BN;   // data cols of a check tile
-    static constexpr int TMEM_COLS = 2 * BN;
+    static constexpr int TMEM_COLS = NACC * BN <= 256 ? 256 : 512;   // tcgen05.alloc: a power of two
     static constexpr int NCHUNK = BN / 32;
     // epilogue shared memory: per-warp double-buffered 32 x 128-byte SWIZZLE_128B
     // staging for the TMA stores; the verification arrays (column partial sums,
@@ -133,13 +138,14 @@ __device__ __forceinline__ uint32_t apply_fault(uint32_t bits, const DevInject& 
     return bits ^ (1u << (f.bit & 31));
 }
 
-template <bool kTF32, int BN, bool FT, int CG>
-__global__ void __launch_bounds__(TcCfg<kTF32, BN, FT, CG>::THREADS, 1)
+template <bool kTF32, int BN, bool FT, int CG, int EPI>
+__global__ void __launch_bounds__(TcCfg<kTF32, BN, FT, CG, EPI>::THREADS, 1)
 tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC29,
                  const __grid_constant__ CUtensorMap tmY, const TcArgs a) {
-    using Cfg = TcCfg<kTF32, BN, FT, CG>;
+    using Cfg = TcCfg<kTF32, BN, FT, CG, EPI>;
     constexpr int S = Cfg::STAGES;
+    constexpr int NACC = Cfg::NACC;
     constexpr int kEpiWG = Cfg::EPI_WG;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte aligned base (SWIZZLE_128B atoms); pointer arithmetic on the
@@ -150,11 +156,11 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * Cfg::STAGE_BYTES + Cfg::EPI_BYTES);
     uint64_t* full = bars;              // [S]  stage landed (TMA + bulk bytes)
     uint64_t* empty = bars + S;         // [S]  producer may refill
-    uint64_t* tm_full = bars + 2 * S;   // [2]  accumulator complete
-    uint64_t* tm_empty = tm_full + 2;   // [2]
-    uint64_t* inj_req = tm_empty + 2;   // [2]  mid-mainloop hand-off, per accumulator buffer
-    uint64_t* inj_done = inj_req + 2;   // [2]
-    uint64_t* cbar = inj_done + 2;      // [4 kEpiWG]  C_in tile loads (beta != 0), one per epilogue warp
+    uint64_t* tm_full = bars + 2 * S;   // [NACC]  accumulator complete
+    uint64_t* tm_empty = tm_full + NACC;   // [NACC]
+    uint64_t* inj_req = tm_empty + NACC;   // [NACC]  mid-mainloop hand-off, per accumulator buffer
+    uint64_t* inj_done = inj_req + NACC;   // [NACC]
+    uint64_t* cbar = inj_done + NACC;   // [4 kEpiWG]  C_in tile loads (beta != 0), one per epilogue warp
     uint64_t* afull = cbar + 4 * kEpiWG;  // [S]  in-kernel encode: this CTA's A tile landed
     uint64_t* yrdy = afull + S;           // [S]  in-kernel encode: split rows of e^T A written (leader's)
     uint64_t* nrdy = yrdy + S;            // [1]  in-kernel encode: row / tile norms of the tile written
@@ -192,11 +198,9 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < NACC; ++b) {
             mbar_init(&tm_full[b], 1);
             mbar_init(&tm_empty[b], 4 * CG);     // every epilogue warp of the pair
-        }
-        for (int b = 0; b < 2; ++b) {
             mbar_init(&inj_req[b], 1);
             mbar_init(&inj_done[b], CG);
         }
@@ -293,13 +297,13 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 if constexpr (CG == 2) umma_commit_pair(bar, pair); else umma_commit(bar);
             };
             int s = 0; uint32_t ph = 0;
-            uint32_t injph0 = 0, injph1 = 0;            // hand-off phases per accumulator buffer
+            uint32_t injph = 0;                         // hand-off phase bit per accumulator buffer
             const bool fuse = FT && a.fuse_a;
             const int ks_kb = a.ks_kb, nkb = a.num_kb;
             int lt = 0;
             for (int t = cluster_id; t < a.num_units; t += num_clusters, ++lt) {
-                const int acc = lt & 1;
-                const uint32_t accph = (lt >> 1) & 1;
+                const int acc = lt % NACC;
+                const uint32_t accph = (uint32_t)(lt / NACC) & 1u;
                 mbar_wait(&tm_empty[acc], accph ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + acc * BN;
@@ -348,8 +352,8 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 // fault(s) of k-block kb and / or the check closing a K_s step
                 auto handoff = [&](int kb) {
                     commit(&inj_req[acc]);
-                    mbar_wait(&inj_done[acc], acc ? injph1 : injph0);
-                    if (acc) injph1 ^= 1; else injph0 ^= 1;
+                    mbar_wait(&inj_done[acc], (injph >> acc) & 1u);
+                    injph ^= 1u << acc;
                     tc_fence_after();
                     while (ii < ie && a.inj[ii].kb == kb) ++ii;
                     evt = next_event(kb);
@@ -491,13 +495,13 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         }
     } else if (warp >= W_EPI0 && warp < W_EPI0 + kEpiWarps) {
         // ----------------------------------------------------- epilogue -----
-        const int wg = (warp - W_EPI0) >> 2;          // epilogue warpgroup (owns accumulator buffer wg when kEpiWG == 2)
+        const int wg = (warp - W_EPI0) >> 2;          // epilogue warpgroup (owns accumulator buffer wg when kEpiWG > 1)
         const int ew = (warp - W_EPI0) & 3;           // TMEM lane quadrant
         const int rloc = ew * 32 + (int)lane;    // row of the 128-row tile
         const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
         const int et = threadIdx.x - 32 * W_EPI0 - 128 * wg;   // 0..127
         const uint32_t ebar = 1 + wg;            // named barrier of this warpgroup
-        uint32_t injph0 = 0, injph1 = 0, cph = 0, gcount = 0;   // gcount: store groups issued by this warp
+        uint32_t injph = 0, cph = 0, gcount = 0;   // injph: hand-off phase bit per buffer; gcount: store groups of this warp
         uint64_t* cbw = &cbar[4 * wg + ew];
         uint8_t* stg = stg0 + wg * Cfg::STG_BYTES;
         float* colsum = reinterpret_cast<float*>(stg);                            // [4][BN] (aliases staging)
@@ -525,9 +529,9 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             const int bm = min(Cfg::BMD, a.M - r0), bn = min(Cfg::BND, a.N - c0);
             constexpr int doff = 0;                            // data col q <-> MMA col q
             constexpr int xoff = BN - 4;                       // row-reference split columns
-            const int acc = lt & 1;
-            if (kEpiWG == 2 && acc != wg) continue;            // the other warpgroup's tile
-            const uint32_t accph = (lt >> 1) & 1;
+            const int acc = lt % NACC;
+            if (kEpiWG > 1 && acc != wg) continue;             // another warpgroup's tile
+            const uint32_t accph = (uint32_t)(lt / NACC) & 1u;
             const uint32_t tb = tmem_base + acc * BN;
             // norms for this tile's thresholds, fetched before the accumulator is ready
             float nrow = 0.f, nbr = 0.f, nac = 0.f, ncol[2] = {0.f, 0.f};
@@ -568,7 +572,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     float2 rs2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
                     const bool w3 = ew == 3;
                     const bool rows_only = a.ft_level == FTGEMM_FT_DETECT_ROWS;   // offline ABFT: no column sums
-                    if constexpr (CG == 1) {
+                    if constexpr (CG == 1 && kEpiWG <= 2) {
                     // (one CTA per MMA: the small-K classes, where the epilogue bounds the
                     // kernel; measured -3 % at 16384^2 x 128.  The CTA-pair instantiation
                     // keeps the single-buffer form below: the extra live registers spill
@@ -791,8 +795,8 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     const int kb_c = next_chk < a.num_kb - 1 ? next_chk : 0x7fffffff;
                     const int kb = min(kb_f, kb_c);
                     if (kb == 0x7fffffff) break;
-                    mbar_wait(&inj_req[acc], acc ? injph1 : injph0);
-                    if (acc) injph1 ^= 1; else injph0 ^= 1;
+                    mbar_wait(&inj_req[acc], (injph >> acc) & 1u);
+                    injph ^= 1u << acc;
                     tc_fence_after();
                     for (; ii < ie && a.inj[ii].kb == kb; ++ii) {
                         const DevInject f = a.inj[ii];
@@ -1032,11 +1036,11 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 }
 
 // ---------------------------------------------------------------- launch ---
-template <bool kTF32, int BN, bool FT, int CG>
+template <bool kTF32, int BN, bool FT, int CG, int EPI = FTGEMM_EPI_WG>
 cudaError_t launch_tc_t(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mC, const CUtensorMap& mC29,
                         const CUtensorMap& mY, const TcArgs& a, cudaStream_t st) {
-    using Cfg = TcCfg<kTF32, BN, FT, CG>;
-    auto kern = tc_ftgemm_kernel<kTF32, BN, FT, CG>;
+    using Cfg = TcCfg<kTF32, BN, FT, CG, EPI>;
+    auto kern = tc_ftgemm_kernel<kTF32, BN, FT, CG, EPI>;
     static PerDeviceOnce smem_attr;
     cudaError_t e = smem_attr.run([&] {
         return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
@@ -1065,11 +1069,14 @@ cudaError_t launch_tc_t(const CUtensorMap& mA, const CUtensorMap& mB, const CUte
     return cudaLaunchKernelEx(&cfg, kern, mA, mB, mC, mC29, mY, a);
 }
 
-cudaError_t launch_tc(bool tf32, int bn, bool ft, int cg, const CUtensorMap& mA, const CUtensorMap& mB,
+cudaError_t launch_tc(bool tf32, int bn, bool ft, int cg, int epi, const CUtensorMap& mA, const CUtensorMap& mB,
                       const CUtensorMap& mC, const CUtensorMap& mC29, const CUtensorMap& mY, const TcArgs& a,
                       cudaStream_t st) {
 #define L_(T, B, F) (cg == 2 ? launch_tc_t<T, B, F, 2>(mA, mB, mC, mC29, mY, a, st) \
                              : launch_tc_t<T, B, F, 1>(mA, mB, mC, mC29, mY, a, st))
+    // small-K narrow tiles with FT: three epilogue warpgroups (one CTA per MMA)
+    if (ft && tf32 && bn == 128 && epi == 3 && cg == 1)
+        return launch_tc_t<true, 128, true, 1, 3>(mA, mB, mC, mC29, mY, a, st);
     if (tf32) {
         if (bn == 256) return ft ? L_(true, 256, true) : L_(true, 256, false);
         return ft ? L_(true, 128, true) : L_(true, 128, false);

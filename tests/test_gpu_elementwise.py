@@ -183,3 +183,24 @@ def test_uncorrectable_and_detect_elementwise(dtype):
     skip[tm + 3, tn + 4] = True
     assert d.elementwise(skip=skip) <= 1.0
     assert abs(d.C[tm + 3, tn + 4] - d.ref.C[tm + 3, tn + 4]) <= 2 ** -7 * 250.0 + 0.5
+
+
+@pytest.mark.parametrize("K", [128, 96])
+def test_small_k_three_epilogue_warpgroups(K):
+    """TF32 with K <= 4 k-blocks on the narrow one-CTA tile runs three epilogue
+    warpgroups (three TMEM accumulator buffers in flight): integer faults
+    bit-exact (corrected, uncorrectable and reference faults), real data
+    element-wise, FT on == FT off bitwise."""
+    F = _F()
+    M, N = 1013, 2000
+    plan = F.plan("tf32", M, N, K, tile=(128, 1))
+    inj = _int_faults(plan, M, N, K)
+    c = Case("tf32", M, N, K, dist="int", alpha=2.0, beta=-1.0, injections=inj, tile=(128, 1))
+    _check_bit_exact(c, F.FT_CORRECT)
+    r = Case("tf32", M, N, K, alpha=1.5, beta=-0.5, tile=(128, 1),
+             injections=detectable_sites("tf32", 8, M, N, K, plan, *[oracle_operand(x, "tf32") for x in
+                                                                    synth.problem(M, N, K, dtype="f32")[:2]], seed=3))
+    assert r.counts_match() and r.events_match() and r.elementwise() <= 1.0
+    on = Case("tf32", M, N, K, run_oracle=False, tile=(128, 1))
+    off = Case("tf32", M, N, K, ft=F.FT_OFF, run_oracle=False, tile=(128, 1))
+    assert np.array_equal(on.C.view(np.uint32), off.C.view(np.uint32))
