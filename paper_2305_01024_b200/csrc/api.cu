@@ -466,12 +466,8 @@ static int run_impl(int code, int64_t M, int64_t N, int64_t K, float alpha, cons
         const int bnd = ft ? p.check_tile_n : p.off_tile_n;
         const uint32_t boxn = 128 / elt;
         CUtensorMap mA, mB;
-#if defined(FTGEMM_EXP_A128)
-        if ((e = make_map(&mA, dt, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * elt, (uint32_t)p.bk, 128u))) return e;
-#else
         if ((e = make_map(&mA, dt, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * elt, (uint32_t)p.bk, (uint32_t)bmd,
                           CU_TENSOR_MAP_SWIZZLE_128B, Batch{(uint64_t)bt.n, (uint64_t)(bt.sA * elt)}))) return e;
-#endif
         const Batch benc{(uint64_t)bt.n, (uint64_t)enc_stride};
         // B (N-major, 128-byte column slices): one 3-D request per stage when the
         // column count is a whole number of slices (B^r always is), else one
@@ -524,6 +520,7 @@ static int run_impl(int code, int64_t M, int64_t N, int64_t K, float alpha, cons
         a.ft_level = ft_level; a.alpha = alpha; a.beta = beta; a.C = C; a.ldc = ldc;
         a.ks_kb = ks > 0 ? (int)std::min<int64_t>(ks / p.bk, num_kb) : 0;
         a.fuse_a = fuse_a;
+        a.y_warp = num_kb > 4 ? 1 : 0;
         a.b3d = b3d ? 1 : 0;
         if (ft) {
             a.Y = enc + L.y; a.kp = g.kp;

@@ -82,6 +82,7 @@ struct TcArgs {
     int ks_kb;            // > 0: verify after every ks_kb k-blocks too (online-interval mode)
     int fuse_a;           // 1: the A-side encode (split e^T A rows, row / tile norms) runs in the kernel
     int b3d;              // 1: tmB is the 3-D (column slice, k, column block) view of B / B^r
+    int y_warp;           // FT: 1 = the split rows of e^T A are loaded by their own warp
     float alpha, beta;
     void* C; int64_t ldc;
     const void* Y; int kp;

@@ -48,6 +48,9 @@ namespace ftg {
 #ifndef FTGEMM_EPI_WG
 #define FTGEMM_EPI_WG 2
 #endif
+#ifndef FTGEMM_MAX_STAGES
+#define FTGEMM_MAX_STAGES 8    // (development: cap the smem ring depth)
+#endif
 
 // EPI_: epilogue warpgroups with FT on, one TMEM accumulator buffer each (2 by
 // default; 3 for the small-K BN = 128 instantiation, where the verification
@@ -76,7 +79,7 @@ struct TcCfg {
     static constexpr int MISC_BYTES = 2048;            // barriers, TMEM address, in-kernel-encode norms
     static_assert((4 * 8 + 4 * NACC + 4 * EPI_WG) * 8 + 16 + (2 * 128 + 2) * 4 <= MISC_BYTES, "misc shared memory");
     static constexpr int STAGE_FIT = (227 * 1024 - 1024 - MISC_BYTES - EPI_BYTES) / (A_BYTES + B_BYTES);
-    static constexpr int STAGES = STAGE_FIT < 8 ? STAGE_FIT : 8;
+    static constexpr int STAGES = STAGE_FIT < FTGEMM_MAX_STAGES ? STAGE_FIT : FTGEMM_MAX_STAGES;
     static constexpr int BMD = FT ? BM - 3 : BM;   // data rows of a check tile
     static constexpr int BND = FT ? BN - 4 : BN;   // data cols of a check tile
     static constexpr int TMEM_COLS = NACC * BN <= 256 ? 256 : 512;   // tcgen05.alloc: a power of two
@@ -194,8 +197,9 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         tma_prefetch_desc(&tmC);
         tma_prefetch_desc(&tmC29);
         if constexpr (FT) tma_prefetch_desc(&tmY);
+        // FT (separately encoded A): the TMA producer and the Y producer arrive
         for (int s = 0; s < S; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], (FT && !a.fuse_a && a.y_warp) ? 2 : 1);
             mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < NACC; ++b) {
@@ -234,13 +238,12 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             // the encoder warps instead of loaded
             const bool fa = FT && a.fuse_a;
             const bool b3d = a.b3d != 0;                 // B tile in one 3-D TMA request
-#if defined(FTGEMM_EXP_A128)
-            // timing experiment: FT kernel fed like FT off (one 128-row A box, no split rows)
-            const uint32_t bytes_cta = Cfg::A_BYTES + Cfg::B_BYTES;
-#else
+            // (FT: the split rows of e^T A come from the Y-producer warp, which
+            // arrives on the same full barrier with their bytes)
+            const bool yself = FT && !fa && !a.y_warp;   // short K: this thread loads them too
             const uint32_t bytes_cta = !FT ? (Cfg::A_BYTES + Cfg::B_BYTES)
-                                     : fa ? Cfg::B_BYTES : (Cfg::BMD * 128 + Cfg::Y_BYTES + Cfg::B_BYTES);
-#endif
+                                     : fa ? Cfg::B_BYTES
+                                     : (Cfg::BMD * 128 + Cfg::B_BYTES + (yself ? Cfg::Y_BYTES : 0));
             for (int u = cluster_id; u < a.num_units; u += num_clusters) {
                 // batched launches: unit u = problem bb's unit ul (problems back to back)
                 const int bb = (int)a.fd_upb.div((uint32_t)u), ul = u - bb * a.units_pb;
@@ -260,9 +263,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     }
                     if constexpr (CG == 1) {
                         if (!fa) tma_load_3d(sa, &tmA, &full[s], kb * Cfg::BK, row0, bb);
-#if !defined(FTGEMM_EXP_A128)
-                        if (FT && !fa) tma_load_3d(sa + Cfg::BMD * 128, &tmY, &full[s], 0, ti * a.num_kb + kb, bb);
-#endif
+                        if (yself) tma_load_3d(sa + Cfg::BMD * 128, &tmY, &full[s], 0, ti * a.num_kb + kb, bb);
                         if (b3d) {
                             tma_load_4d(sb, &tmB, &full[s], 0, kb * Cfg::BK, colb / Cfg::BOXN, bb);
                         } else {
@@ -273,9 +274,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     } else {
                         const uint32_t mb = smem_u32(&full[s]) & kPeerBitMask;
                         if (!fa) tma_load_3d_pair(sa, &tmA, mb, kb * Cfg::BK, row0, bb);
-#if !defined(FTGEMM_EXP_A128)
-                        if (FT && !fa) tma_load_3d_pair(sa + Cfg::BMD * 128, &tmY, mb, 0, ti * a.num_kb + kb, bb);
-#endif
+                        if (yself) tma_load_3d_pair(sa + Cfg::BMD * 128, &tmY, mb, 0, ti * a.num_kb + kb, bb);
                         if (b3d) {
                             tma_load_4d_pair(sb, &tmB, mb, 0, kb * Cfg::BK, colb / Cfg::BOXN, bb);
                         } else {
@@ -389,7 +388,34 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         // running row sums of squares / sum of (e^T A)^2 of the threshold
         // (R1).  Warp 2 covers 16-byte chunks 0..3 of each 128-byte
         // row, warp 3 chunks 4..7; lane = (row group rg, chunk cq).
-        if (FT && a.fuse_a) {
+        if (FT && !a.fuse_a && a.y_warp && warp == W_ENC0 + 1) {
+            // ---------------------------------------------- Y producer -------
+            // The 384-byte split rows of e^T A (rows 125..127 of every stage's A
+            // tile) from their own warp: a third TMA per stage on the main
+            // producer thread made its issue rate the limiter (BF16 8192^3 FT run
+            // -2.8 %).  Short K (<= 4 k-blocks): the producer loads them itself.
+            if (lane == 0) {
+                int s = 0; uint32_t ph = 0;
+                for (int u = cluster_id; u < a.num_units; u += num_clusters) {
+                    const int bb = (int)a.fd_upb.div((uint32_t)u), ul = u - bb * a.units_pb;
+                    int tmu, tj;
+                    tile_coords(ul, a, tmu, tj);
+                    const int ti = tmu * CG + (int)rank;
+                    for (int kb = 0; kb < a.num_kb; ++kb) {
+                        mbar_wait(&empty[s], ph ^ 1);
+                        if (leader) mbar_arrive_expect_tx(&full[s], CG * Cfg::Y_BYTES);
+                        uint8_t* sy = stage_base + s * Cfg::STAGE_BYTES + Cfg::BMD * 128;
+                        if constexpr (CG == 1) {
+                            tma_load_3d(sy, &tmY, &full[s], 0, ti * a.num_kb + kb, bb);
+                        } else {
+                            tma_load_3d_pair(sy, &tmY, smem_u32(&full[s]) & kPeerBitMask, 0, ti * a.num_kb + kb, bb);
+                        }
+                        if (++s == S) { s = 0; ph ^= 1; }
+                    }
+                }
+            }
+            __syncwarp();
+        } else if (FT && a.fuse_a) {
             constexpr int EPC = kTF32 ? 4 : 8;            // elements per 16-byte chunk
             const int half = warp - W_ENC0;
             const int cq = lane & 3, rg = lane >> 2;
