@@ -645,7 +645,7 @@ def cfg5_one_gpu(args, H):
     g.encode(None, B, which=2)
     med = H.interleave({"step": lambda i: (g.encode(A, None, which=1), g.run(A, B, C)),
                         "ft_off": lambda i: g.run(A, B, C, ft_level=F.FT_OFF),
-                        "cublas": lambda i: torch.matmul(A, B, out=C)}, 5)
+                        "cublas": lambda i: torch.matmul(A, B, out=C)}, 12)
     cnt, _ = g.report(0)
     out = {**{k + "_ms": v for k, v in med.items()}, "step_tflops": tflops(flops, med["step"]),
            "overhead_vs_ft_off_pct": 100.0 * (med["step"] - med["ft_off"]) / med["ft_off"],

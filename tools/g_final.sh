@@ -1,6 +1,6 @@
 #!/bin/bash
 # round-2 final evidence: full GPU suite (+ threshold sweep log, smoke), sanitizers, bench, sweep, ncu
-T=${1:-r2b}
+T=${1:-r2c}
 D=gpurun_out/prof_$T; mkdir -p $D
 export PYTHONUNBUFFERED=1 FTGEMM_FP_SWEEP_OUT=$D
 timeout 1800 python -m pytest tests -m gpu -q -rf 2>&1 | tail -15 > $D/pytest.txt; tail -3 $D/pytest.txt
