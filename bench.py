@@ -426,6 +426,9 @@ def cfg3_comparators(args, H, g, A, B, C, fl, est, step):
     rate_sched = {str(int(r)): fl.schedule(r, n_calls, est)[0] for r in SWEEP_RATES}
     fpc_lists = {str(n) if n >= 0 else "all_tiles": [fl.per_call(n) for _ in range(4 if n >= 0 else 1)]
                  for n in FAULTS_PER_CALL}
+    # in-kernel encode of A (ftgemm_run_fused): B encoded separately
+    g_fa = F.FTGemm("bf16", M, N, K)
+    g_fa.encode(None, B, which=2)
     configs = {
         "ft_off": lambda i: g.run(A, B, C, ft_level=F.FT_OFF),
         "cublas": lambda i: torch.matmul(A, B, out=C),
@@ -435,6 +438,8 @@ def cfg3_comparators(args, H, g, A, B, C, fl, est, step):
         "encode": lambda i: g.encode(A, B),
         "encode_a": lambda i: g.encode(A, None, which=1),
         "step_b_resident": lambda i: (g.encode(A, None, which=1), g.run(A, B, C, ft_level=F.FT_CORRECT)),
+        "fused_a_step": lambda i: (g_fa.encode(None, B, which=2), g_fa.run(A, B, C, fuse_a=True)),
+        "fused_a_step_b_resident": lambda i: g_fa.run(A, B, C, fuse_a=True),
         "detect_rows_run": lambda i: g.run(A, B, C, ft_level=F.FT_DETECT_ROWS),
         # the paper's comparison scheme (Ding 2011): cuBLAS GEMMs + separate verification
         "nonfused_step": lambda i: (g.encode(A, B, which=3 | 4), g.run_nonfused(A, B, C, ft_level=F.FT_CORRECT)),
@@ -449,6 +454,7 @@ def cfg3_comparators(args, H, g, A, B, C, fl, est, step):
         configs["fpc_" + key] = (lambda ls: (lambda i: step(ls[i % len(ls)])))(lists)
     med = H.interleave(configs, n_calls, after_warmup=g.reset)
     cs_sweep, _ = g.report(0)
+    cs_fa, _ = g_fa.report(0)                    # fault-free fused-A calls: nothing may be flagged
     g.reset()
     g.encode(A, B)                               # restore the fused path's encoded operand (nonfused re-encodes)
     n_expect = sum(sum(len(x) for x in sc) for sc in rate_sched.values())
@@ -520,6 +526,9 @@ def cfg3_comparators(args, H, g, A, B, C, fl, est, step):
         "overhead_vs_ft_off_pct": ov(med["ft_step"], t_off),
         "overhead_vs_cublas_pct": ov(med["ft_step"], t_cub),
         "overhead_b_resident_vs_ft_off_pct": ov(med["step_b_resident"], t_off),
+        "overhead_fused_a_step_vs_ft_off_pct": ov(med["fused_a_step"], t_off),
+        "overhead_fused_a_b_resident_vs_ft_off_pct": ov(med["fused_a_step_b_resident"], t_off),
+        "fused_a_tiles_checked": int(cs_fa["tiles_checked"]), "fused_a_tiles_detected": int(cs_fa["tiles_detected"]),
         "overhead_run_only_vs_ft_off_pct": ov(med["ft_run"], t_off),
         "encode_gbs": enc_bytes / (med["encode"] * 1e-3) / 1e9,
         "encode_hbm_frac": enc_bytes / (med["encode"] * 1e-3) / 1e9 / peaks["hbm_gbs"],

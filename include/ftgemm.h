@@ -104,14 +104,18 @@ typedef struct ftgemm_inject {
  * SURVEY 8(f) row 1, the paper's threadblock-level fusion of the checksum
  * encoding into the prefetch stage.  As ftgemm_run, but the
  * column checksum of A (Eq. 1: e^T A per check tile, its exact split into the
- * operand format) and the threshold's row / tile norms are computed by the
- * kernel from the A tiles it stages anyway, so enc_ws needs only the B part
- * (ftgemm_encode which = 2).  Runs one CTA per MMA (no CTA pairs).  Measured
- * on B200 it is SLOWER than the separate encode pass for BF16 (the column sums
- * on two spare warps cannot keep pace with the tensor core: 2x at 8192^2 x
- * 1024), within 1.2x for TF32; kept as the paper's fusion for comparison.
+ * operand format) and the threshold's row / tile norms are computed inside
+ * the GEMM kernel, so enc_ws needs only the B part (ftgemm_encode which = 2).
+ * One encoder warp per CTA (and, during the first wave, the epilogue warps)
+ * claims (check tile, k-block) items in the order the tile schedule first
+ * needs them, reads A from global memory, and publishes each item with a
+ * release flag; the split-row loads of every k-block wait for its flag.  Every
+ * item is computed once per call (not once per tile column).  The call first
+ * clears the item flags in enc_ws (cudaMemsetAsync on `stream`).  C is
+ * bit-identical to ftgemm_run's (same operands, same k order); the carried
+ * references and norms may differ in the last bits (summation order).
  * Tensor-core dtypes, ft_level DETECT, CORRECT or DETECT_ROWS; UNSUPPORTED for
- * F32_SIMT, FT_OFF and the online-interval mode.                             */
+ * F32_SIMT, FT_OFF, batched runs and the online-interval mode.               */
 FTGEMM_API int ftgemm_run_fused(int dtype, int64_t M, int64_t N, int64_t K, float alpha,
                const void* A, int64_t lda, const void* B, int64_t ldb,
                float beta, void* C, int64_t ldc, const void* enc_ws, int ft_level,

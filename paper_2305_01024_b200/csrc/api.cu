@@ -388,9 +388,6 @@ static int run_impl(int code, int64_t M, int64_t N, int64_t K, float alpha, cons
     ftgemm_plan_t p;
     fill_plan(code, M, N, K, &p, bt.n);
     if (ks > 0 && ks % p.bk) return fail(FTGEMM_ERR_INVALID_VALUE, "ks must be a multiple of plan.bk (%d)", p.bk);
-    // in-kernel encode: one CTA per MMA (a CTA pair would put a cluster-scope
-    // release of the peer's split rows on every k-block's critical path)
-    if (fuse_a) p.cta_group = 1;
     const bool ft = ft_level != FTGEMM_FT_OFF;
     const Geometry g = geometry(p, K);
     const EncLayout L = enc_layout(g, M, N);
@@ -520,12 +517,23 @@ static int run_impl(int code, int64_t M, int64_t N, int64_t K, float alpha, cons
         a.ft_level = ft_level; a.alpha = alpha; a.beta = beta; a.C = C; a.ldc = ldc;
         a.ks_kb = ks > 0 ? (int)std::min<int64_t>(ks / p.bk, num_kb) : 0;
         a.fuse_a = fuse_a;
-        a.y_warp = num_kb > 4 ? 1 : 0;
+        a.y_warp = (num_kb > 4 || fuse_a) ? 1 : 0;     // the in-kernel encode's flag waits live in the Y warp
         a.b3d = b3d ? 1 : 0;
         if (ft) {
             a.Y = enc + L.y; a.kp = g.kp;
             a.rownorm = (const float*)(enc + L.rownorm); a.colnorm = (const float*)(enc + L.colnorm);
             a.acnorm = (const float*)(enc + L.acnorm); a.brnorm = (const float*)(enc + L.brnorm);
+        }
+        if (fuse_a) {
+            // the encoder warps' item flags start cleared on every launch (so a
+            // replayed or aborted launch never sees stale items)
+            a.A = A; a.lda = lda;
+            a.fflag = (uint32_t*)(enc + L.fflag);
+            a.frn2 = (float*)(enc + L.frn2);
+            a.facn2 = (float*)(enc + L.facn2);
+            a.nkb4 = (g.nkb + 3) & ~3;
+            if ((ce = cudaMemsetAsync(a.fflag, 0, sizeof(uint32_t) * ((size_t)g.tiles_m * g.nkb + 2), st)) != cudaSuccess)
+                return fail_cuda(ce, "in-kernel encode flags");
         }
         a.tau_u = tau_u; a.tau_l1 = l1; a.tau_l2 = l2; a.sqrtK = sqk;
         a.rep = (ReportDev*)report_ws; a.inj = dinj; a.n_inj = n_inj;

@@ -81,6 +81,14 @@ struct TcArgs {
     int ft_level;
     int ks_kb;            // > 0: verify after every ks_kb k-blocks too (online-interval mode)
     int fuse_a;           // 1: the A-side encode (split e^T A rows, row / tile norms) runs in the kernel
+    // in-kernel encode of A (fuse_a): encoder warps stream A from global
+    // memory, one claimed (check tile, k-block) item at a time, in the order
+    // the tile schedule first needs them, and publish each item with a flag
+    const void* A; int64_t lda;
+    uint32_t* fflag;      // [tiles_m][num_kb]: 1 = item written; then the item claim counter (zeroed before every launch)
+    float* frn2;          // [tiles_m][128][nkb4]: per-k-block partial row sums of squares
+    float* facn2;         // [tiles_m][nkb4]: per-k-block partial sums of (e^T A)^2
+    int nkb4;             // num_kb rounded up to 4
     int b3d;              // 1: tmB is the 3-D (column slice, k, column block) view of B / B^r
     int y_warp;           // FT: 1 = the split rows of e^T A are loaded by their own warp
     float alpha, beta;
@@ -137,8 +145,11 @@ struct Geometry {
 //           B^r = [B_j, B_j e] of PAPER.md Eq. (2), N-major, kp rows of
 //           tiles_n * bn: tile j's slot holds columns 0..bnd-1 of B_j, then
 //           split(B_j e) (3 columns) and a zero column), column norms, tile norms.
+//   In-kernel A encode (ftgemm_run_fused, tensor-core paths): item flags and
+//           the per-k-block partial norms the encoder warps publish.
 struct EncLayout {
     size_t ac, y, rownorm, acnorm, rn2, acn2, cnt_a;     // A part
+    size_t fflag, frn2, facn2;                           // A part, in-kernel encode
     size_t b_off;                                        // start of the B part
     size_t br, bt, colnorm, brnorm, cn2, brn2, cnt_b;    // absolute offsets
     size_t a_bytes, b_bytes, total;
@@ -156,6 +167,10 @@ inline EncLayout enc_layout(const Geometry& g, int64_t M, int64_t N) {
     L.rn2 = o;     o = align256(o + sizeof(float) * (size_t)g.nkc_a * M);
     L.acn2 = o;    o = align256(o + sizeof(float) * (size_t)g.nkc_a * g.tiles_m);
     L.cnt_a = o;   o = align256(o + sizeof(int) * (size_t)g.tiles_m);
+    const size_t nkb4 = g.tc ? (size_t)((g.nkb + 3) & ~3) : 0;
+    L.fflag = o;   o = align256(o + (g.tc ? sizeof(uint32_t) * ((size_t)g.tiles_m * g.nkb + 2) : 0));   // + claim, publish counters
+    L.frn2 = o;    o = align256(o + sizeof(float) * (size_t)g.tiles_m * 128 * nkb4);
+    L.facn2 = o;   o = align256(o + sizeof(float) * (size_t)g.tiles_m * nkb4);
     L.a_bytes = o;
     L.b_off = o;
     L.br = o;      o = align256(o + sizeof(float) * (size_t)g.tiles_n * g.kp);

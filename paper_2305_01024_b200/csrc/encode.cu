@@ -669,13 +669,16 @@ __device__ __forceinline__ void encode_b_tc_body(const int kc, const int tj, con
 // as every block has started.
 template <int MODE>
 __global__ void __launch_bounds__(256, ENC_A_MINB) encode_a_kernel(const EncAP P) {
+    griddep_launch_dependents();
     encode_a_body<MODE>(blockIdx.x, blockIdx.y, at_batch(P, blockIdx.z));
 }
 template <int MODE>
 __global__ void __launch_bounds__(256) encode_b_tc_kernel(const EncBP P) {
+    griddep_launch_dependents();
     encode_b_tc_body<MODE>(blockIdx.x, blockIdx.y, at_batch(P, blockIdx.z));
 }
 __global__ void __launch_bounds__(256) encode_b_simt_kernel(const EncBP P) {
+    griddep_launch_dependents();
     encode_b_simt_body(blockIdx.x, blockIdx.y, at_batch(P, blockIdx.z));
 }
 template <int MODE>

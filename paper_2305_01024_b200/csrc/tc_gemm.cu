@@ -25,7 +25,9 @@
 //                 sums (warp transpose-reduce + smem), residuals vs thresholds,
 //                 locate, correct, alpha/beta, store; they
 //                 also service mid-mainloop fault injections
-//   warp E        TMEM allocator (+ in-kernel A encode with warp E+1)
+//   warp E        TMEM allocator; in-kernel A encode (ftgemm_run_fused)
+//   warp E+1      Y producer (split rows of e^T A; waits for the in-kernel
+//                 encode's item flags)
 //   warp E+2      TMA producer
 //   warp E+3      MMA issuer (one thread: tcgen05.mma, tcgen05.commit)
 // (FTGEMM_ROLES_HI=0 restores the earlier layout: producer 0, MMA 1, epilogue 4..)
@@ -141,6 +143,199 @@ __device__ __forceinline__ uint32_t apply_fault(uint32_t bits, const DevInject& 
     return bits ^ (1u << (f.bit & 31));
 }
 
+#if defined(FTGEMM_EXP_FA_TRACE)
+// timing experiment: globaltimer stamps into a debug buffer (ftgemm_debug_trace)
+__device__ unsigned long long g_fa_trace[1 << 17];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
+// One item of the in-kernel A encode (one warp): check tile ti (125 rows of A),
+// k-block kb (128 bytes of every row).  Lane = (row group rg = lane / 8, 16-byte
+// chunk c = lane % 8); the lane loads rows rg, rg + 4, ..., rg + 124 -- all 32
+// loads in flight at once (one memory round trip per item).
+//   split rows 125..127 of the MMA A tile: the exact 3-term split of
+//       e^T A_i [kb * BK .. +BK) (Eq. 1), pre-swizzled, into Y
+//   frn2[ti][row][kb]: this k-block's sum of squares of every row (R1)
+//   facn2[ti][kb]:     this k-block's sum of (e^T A_i)^2
+// then a release flag.  Rows >= M and columns >= K are zeros, as the TMA loads.
+// item index (claim order) -> (check tile, k-block): the order in which the
+// persistent schedule first needs them -- schedule group by schedule group,
+// k-block by k-block, the group's check tiles fastest
+__device__ __forceinline__ void enc_item_coords(int it, const TcArgs& a, int cg, int& ti, int& kb) {
+    const int tpg = a.group * cg;
+    const int per_group = tpg * a.num_kb;
+    const int grp = it / per_group;
+    const int first = grp * tpg;
+    const int tg = min(tpg, a.tiles_m - first);
+    const int rem = it - grp * per_group;
+    kb = rem / tg;
+    ti = first + (rem - kb * tg);
+}
+
+template <bool kTF32>
+__device__ __forceinline__ void encode_a_item(const TcArgs& a, const int ti, const int kb, const uint32_t lane) {
+    constexpr int ELT = kTF32 ? 4 : 2, EPC = 16 / ELT, BK = 128 / ELT, BMD = 125;
+    const int rg = (int)(lane >> 3), c = (int)(lane & 7);
+    const int r0 = ti * BMD, bm = min(BMD, a.M - r0);
+    const int k0 = kb * BK + c * EPC;
+    const int64_t pitch = a.lda * ELT;
+    const uint8_t* base = reinterpret_cast<const uint8_t*>(a.A) + ((int64_t)r0 * a.lda + k0) * ELT;
+    const bool kfull = k0 + EPC <= a.K;
+#if defined(FTGEMM_EXP_FA_TRACE)
+    if (lane == 0) g_fa_trace[20480 + ti * a.num_kb + kb] = gtimer();
+#endif
+    uint4 v[32];
+    if (kfull && rg + 4 * 31 < bm) {                     // every row present, whole chunk below K
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = ldg_stream_v4(base + (int64_t)(rg + 4 * i) * pitch);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const int r = rg + 4 * i;
+            v[i] = make_uint4(0u, 0u, 0u, 0u);
+            if (r < bm && k0 < a.K) {
+                const uint8_t* p = base + (int64_t)r * pitch;
+                if (kfull) {
+                    v[i] = ldg_stream_v4(p);
+                } else {
+                    uint32_t wd[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+                    for (int e = 0; e < EPC; ++e) {
+                        if (k0 + e < a.K) {
+                            if constexpr (ELT == 2) wd[e >> 1] |= (uint32_t)reinterpret_cast<const uint16_t*>(p)[e] << (16 * (e & 1));
+                            else wd[e] = reinterpret_cast<const uint32_t*>(p)[e];
+                        }
+                    }
+                    v[i] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+                }
+            }
+        }
+    }
+#if defined(FTGEMM_EXP_FA_TRACE)
+    {
+        uint32_t x = 0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x ^= v[i].x ^ v[i].w;
+        x = __reduce_xor_sync(0xffffffffu, x);
+        if (lane == 0) g_fa_trace[60000 + ti * a.num_kb + kb] = gtimer() + (x == 0x12345678u);
+    }
+#endif
+    float2 cs2[EPC / 2];
+#pragma unroll
+    for (int j = 0; j < EPC / 2; ++j) cs2[j] = make_float2(0.0f, 0.0f);
+    float* rn2 = a.frn2 + (int64_t)ti * 128 * a.nkb4 + kb;
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+        float q[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const uint4 u = v[16 * b + i];
+            const uint32_t wd[4] = {u.x, u.y, u.z, u.w};
+            float2 q2 = make_float2(0.0f, 0.0f);
+#pragma unroll
+            for (int j = 0; j < EPC / 2; ++j) {
+                float2 x;
+                if constexpr (kTF32) x = make_float2(tf32_trunc(__uint_as_float(wd[2 * j])), tf32_trunc(__uint_as_float(wd[2 * j + 1])));
+                else x = make_float2(__uint_as_float(wd[j] << 16), __uint_as_float(wd[j] & 0xFFFF0000u));
+                cs2[j] = __fadd2_rn(cs2[j], x);
+                q2 = __ffma2_rn(x, x, q2);
+            }
+            q[i] = q2.x + q2.y;
+        }
+        // row sums of squares across the 8 chunk lanes, transposed: the lane with
+        // chunk c ends up holding rows i = 2c, 2c + 1 of this half (14 shuffles)
+        float h8[8], h4[4], h2[2];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const bool up = c & 4;
+            const float send = up ? q[i] : q[i + 8], keep = up ? q[i + 8] : q[i];
+            h8[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const bool up = c & 2;
+            const float send = up ? h8[i] : h8[i + 4], keep = up ? h8[i + 4] : h8[i];
+            h4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const bool up = c & 1;
+            const float send = up ? h4[i] : h4[i + 2], keep = up ? h4[i + 2] : h4[i];
+            h2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) rn2[(int64_t)(rg + 4 * (16 * b + 2 * c + j)) * a.nkb4] = h2[j];
+    }
+    // column sums across the 4 row groups
+    float cs[EPC];
+#pragma unroll
+    for (int j = 0; j < EPC / 2; ++j) { cs[2 * j] = cs2[j].x; cs[2 * j + 1] = cs2[j].y; }
+#pragma unroll
+    for (int j = 0; j < EPC; ++j) {
+        cs[j] += __shfl_xor_sync(0xffffffffu, cs[j], 8);
+        cs[j] += __shfl_xor_sync(0xffffffffu, cs[j], 16);
+    }
+    float asq = 0.0f;
+    if (rg == 0) {
+        uint32_t pk[3][4];
+#pragma unroll
+        for (int j = 0; j < EPC; ++j) {
+            const float sv = cs[j];
+            asq = fmaf(sv, sv, asq);
+            float hi, mid, lo;
+            split3<kTF32 ? 1 : 0>(sv, hi, mid, lo);
+            const float parts[3] = {hi, mid, lo};
+#pragma unroll
+            for (int r3 = 0; r3 < 3; ++r3) {
+                if constexpr (kTF32) pk[r3][j] = __float_as_uint(parts[r3]);
+                else if (j & 1) pk[r3][j >> 1] |= (uint32_t)f32_to_bf16_rn(parts[r3]) << 16;
+                else pk[r3][j >> 1] = (uint32_t)f32_to_bf16_rn(parts[r3]);
+            }
+        }
+        uint8_t* yb = reinterpret_cast<uint8_t*>(const_cast<void*>(a.Y)) + ((int64_t)ti * a.num_kb + kb) * 384;
+#pragma unroll
+        for (int r3 = 0; r3 < 3; ++r3) {
+            const int row = BMD + r3;
+            *reinterpret_cast<uint4*>(yb + r3 * 128 + ((c ^ (row & 7)) << 4)) = make_uint4(pk[r3][0], pk[r3][1], pk[r3][2], pk[r3][3]);
+        }
+    }
+    asq += __shfl_xor_sync(0xffffffffu, asq, 1);
+    asq += __shfl_xor_sync(0xffffffffu, asq, 2);
+    asq += __shfl_xor_sync(0xffffffffu, asq, 4);
+    if (lane == 0) a.facn2[(int64_t)ti * a.nkb4 + kb] = asq;
+    // publish: every lane's writes (the Y rows are read by TMA -- the async
+    // proxy -- on other SMs), then one release flag (cumulative over the
+    // warp's writes ordered before it by the warp barrier)
+#if defined(FTGEMM_EXP_FA_TRACE)
+    __syncwarp();
+    if (lane == 0) g_fa_trace[80000 + ti * a.num_kb + kb] = gtimer();
+#endif
+    fence_proxy_async_global();
+    __syncwarp();
+#if defined(FTGEMM_EXP_FA_TRACE)
+    if (lane == 0) g_fa_trace[100000 + ti * a.num_kb + kb] = gtimer();
+#endif
+    if (lane == 0) st_release_u32(a.fflag + (int64_t)ti * a.num_kb + kb, 1u);
+#if defined(FTGEMM_EXP_FA_TRACE)
+    if (lane == 0) {
+        g_fa_trace[4096 + ti * a.num_kb + kb] = gtimer();
+    }
+#endif
+    __syncwarp();
+}
+
+// Claim the next item of the in-kernel A encode (warp-uniform result; an
+// index >= the item count means every item is claimed).
+__device__ __forceinline__ uint32_t enc_claim(const TcArgs& a, uint32_t lane) {
+    uint32_t it = 0;
+    if (lane == 0) it = atomicAdd(a.fflag + (int64_t)a.tiles_m * a.num_kb, 1u);
+    return __shfl_sync(0xffffffffu, it, 0);
+}
+
 template <bool kTF32, int BN, bool FT, int CG, int EPI>
 __global__ void __launch_bounds__(TcCfg<kTF32, BN, FT, CG, EPI>::THREADS, 1)
 tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -164,13 +359,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     uint64_t* inj_req = tm_empty + NACC;   // [NACC]  mid-mainloop hand-off, per accumulator buffer
     uint64_t* inj_done = inj_req + NACC;   // [NACC]
     uint64_t* cbar = inj_done + NACC;   // [4 kEpiWG]  C_in tile loads (beta != 0), one per epilogue warp
-    uint64_t* afull = cbar + 4 * kEpiWG;  // [S]  in-kernel encode: this CTA's A tile landed
-    uint64_t* yrdy = afull + S;           // [S]  in-kernel encode: split rows of e^T A written (leader's)
-    uint64_t* nrdy = yrdy + S;            // [1]  in-kernel encode: row / tile norms of the tile written
-    uint64_t* nfree = nrdy + 1;           // [1]  ... and read by the epilogue (slot reusable)
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(nfree + 1);
-    float* nsq = reinterpret_cast<float*>(tmem_holder + 4);   // [2 half][128] row sums of squares (one tile)
-    float* acsq = nsq + 2 * 128;                              // [2 half] sum of (e^T A)^2
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(cbar + 4 * kEpiWG);
 
     const int warp = threadIdx.x >> 5;
     // Warp roles.  The SM sub-partition scheduler favours the highest warp id
@@ -191,15 +380,18 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const bool leader = rank == 0;
     const int cluster_id = blockIdx.x / CG, num_clusters = gridDim.x / CG;
 
+#if defined(FTGEMM_EXP_FA_TRACE)
+    if (threadIdx.x == 0) g_fa_trace[40000 + blockIdx.x] = gtimer();
+#endif
     if (warp == W_PROD && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
         tma_prefetch_desc(&tmC);
         tma_prefetch_desc(&tmC29);
         if constexpr (FT) tma_prefetch_desc(&tmY);
-        // FT (separately encoded A): the TMA producer and the Y producer arrive
+        // FT with the Y-producer warp: the TMA producer and the Y producer arrive
         for (int s = 0; s < S; ++s) {
-            mbar_init(&full[s], (FT && !a.fuse_a && a.y_warp) ? 2 : 1);
+            mbar_init(&full[s], (FT && a.y_warp) ? 2 : 1);
             mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < NACC; ++b) {
@@ -209,12 +401,6 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             mbar_init(&inj_done[b], CG);
         }
         for (int w = 0; w < 4 * kEpiWG; ++w) mbar_init(&cbar[w], 1);
-        for (int s = 0; s < S; ++s) {
-            mbar_init(&afull[s], 1);
-            mbar_init(&yrdy[s], 2 * CG);         // both encoder warps of both CTAs
-        }
-        mbar_init(&nrdy[0], 64);                 // every lane of the two encoder warps
-        mbar_init(&nfree[0], 128);               // every lane of the tile's epilogue warpgroup
         fence_barrier_init();
     }
     if (warp == W_ALLOC) tmem_alloc<Cfg::TMEM_COLS, CG>(tmem_holder);
@@ -233,16 +419,11 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             // row-major B.  B is N-major in BOXN-column boxes; with a CTA pair each
             // CTA loads half of the tile's columns.  All bytes of a stage (both CTAs)
             // are counted on the leader's full barrier.
-            // in-kernel encode (a.fuse_a): the A box lands on this CTA's own afull
-            // barrier (the encoder warps read it); rows 125..127 are written by
-            // the encoder warps instead of loaded
-            const bool fa = FT && a.fuse_a;
             const bool b3d = a.b3d != 0;                 // B tile in one 3-D TMA request
             // (FT: the split rows of e^T A come from the Y-producer warp, which
             // arrives on the same full barrier with their bytes)
-            const bool yself = FT && !fa && !a.y_warp;   // short K: this thread loads them too
+            const bool yself = FT && !a.y_warp;          // short K: this thread loads them too
             const uint32_t bytes_cta = !FT ? (Cfg::A_BYTES + Cfg::B_BYTES)
-                                     : fa ? Cfg::B_BYTES
                                      : (Cfg::BMD * 128 + Cfg::B_BYTES + (yself ? Cfg::Y_BYTES : 0));
             for (int u = cluster_id; u < a.num_units; u += num_clusters) {
                 // batched launches: unit u = problem bb's unit ul (problems back to back)
@@ -257,12 +438,8 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     if (leader) mbar_arrive_expect_tx(&full[s], CG * bytes_cta);
                     uint8_t* sa = stage_base + s * Cfg::STAGE_BYTES;
                     uint8_t* sb = sa + Cfg::A_BYTES;
-                    if (fa) {
-                        mbar_arrive_expect_tx(&afull[s], Cfg::BMD * 128);
-                        tma_load_3d(sa, &tmA, &afull[s], kb * Cfg::BK, row0, bb);
-                    }
                     if constexpr (CG == 1) {
-                        if (!fa) tma_load_3d(sa, &tmA, &full[s], kb * Cfg::BK, row0, bb);
+                        tma_load_3d(sa, &tmA, &full[s], kb * Cfg::BK, row0, bb);
                         if (yself) tma_load_3d(sa + Cfg::BMD * 128, &tmY, &full[s], 0, ti * a.num_kb + kb, bb);
                         if (b3d) {
                             tma_load_4d(sb, &tmB, &full[s], 0, kb * Cfg::BK, colb / Cfg::BOXN, bb);
@@ -273,7 +450,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         }
                     } else {
                         const uint32_t mb = smem_u32(&full[s]) & kPeerBitMask;
-                        if (!fa) tma_load_3d_pair(sa, &tmA, mb, kb * Cfg::BK, row0, bb);
+                        tma_load_3d_pair(sa, &tmA, mb, kb * Cfg::BK, row0, bb);
                         if (yself) tma_load_3d_pair(sa + Cfg::BMD * 128, &tmY, mb, 0, ti * a.num_kb + kb, bb);
                         if (b3d) {
                             tma_load_4d_pair(sb, &tmB, mb, 0, kb * Cfg::BK, colb / Cfg::BOXN, bb);
@@ -297,7 +474,6 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             };
             int s = 0; uint32_t ph = 0;
             uint32_t injph = 0;                         // hand-off phase bit per accumulator buffer
-            const bool fuse = FT && a.fuse_a;
             const int ks_kb = a.ks_kb, nkb = a.num_kb;
             int lt = 0;
             for (int t = cluster_id; t < a.num_units; t += num_clusters, ++lt) {
@@ -324,15 +500,12 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     return e;
                 };
                 int evt = FT ? next_event(-1) : 0x7fffffff;
-                // two instantiations of the k-loop: the lean one (no hand-off, no
-                // in-kernel encode -- the common case) carries no per-k-block tests
+#if defined(FTGEMM_EXP_FA_TRACE)
+                if (t < 2048) g_fa_trace[2 * t] = gtimer();
+#endif
                 // one k-block: wait for the stage, issue its MMAs, release the stage
-                auto kblock = [&](int kb, auto general_c) {
-                    constexpr bool kGeneral = decltype(general_c)::value;
+                auto kblock = [&](int kb) {
                     mbar_wait(&full[s], ph);
-                    if constexpr (kGeneral) {
-                        if (fuse) mbar_wait(&yrdy[s], ph);     // both CTAs' A tiles + split rows ready
-                    }
                     tc_fence_after();
                     const uint32_t sa = smem_u32(stage_base + s * Cfg::STAGE_BYTES);
                     const uint32_t sb = sa + Cfg::A_BYTES;
@@ -357,51 +530,61 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     while (ii < ie && a.inj[ii].kb == kb) ++ii;
                     evt = next_event(kb);
                 };
-                if (FT && fuse) {
-                    // in-kernel encode: per-k-block split-row barrier and hand-off tests
-                    for (int kb = 0; kb < nkb; ++kb) {
-                        kblock(kb, std::true_type{});
-                        if (kb == evt) handoff(kb);
-                    }
-                } else {
+                {
                     // lean runs of k-blocks between hand-offs: no per-k-block tests in
                     // the issue loop (a tile with a fault pays only its hand-offs)
                     int kb = 0;
                     for (;;) {
                         const int end = evt < nkb ? evt + 1 : nkb;
-                        for (; kb < end; ++kb) kblock(kb, std::false_type{});
+                        for (; kb < end; ++kb) kblock(kb);
                         if (kb >= nkb && !(evt < nkb)) break;
                         handoff(kb - 1);
                         if (kb >= nkb) break;
                     }
                 }
                 commit(&tm_full[acc]);
+#if defined(FTGEMM_EXP_FA_TRACE)
+                if (t < 2048) g_fa_trace[2 * t + 1] = gtimer();
+#endif
             }
         }
         __syncwarp();
     } else if (warp == W_ENC0 || warp == W_ENC0 + 1) {
-        // ------------------------------------- in-kernel encode of A -------
-        // (the paper's threadblock-level fusion of the
-        // checksum encoding into the prefetch stage.)  Per k-block,
-        // from the A tile in shared memory: e^T A_i over the 125 data rows, its
-        // exact 3-term split written as MMA rows 125..127 (SWIZZLE_128B), and the
-        // running row sums of squares / sum of (e^T A)^2 of the threshold
-        // (R1).  Warp 2 covers 16-byte chunks 0..3 of each 128-byte
-        // row, warp 3 chunks 4..7; lane = (row group rg, chunk cq).
-        if (FT && !a.fuse_a && a.y_warp && warp == W_ENC0 + 1) {
+        if (FT && a.y_warp && warp == W_ENC0 + 1) {
             // ---------------------------------------------- Y producer -------
             // The 384-byte split rows of e^T A (rows 125..127 of every stage's A
             // tile) from their own warp: a third TMA per stage on the main
             // producer thread made its issue rate the limiter (BF16 8192^3 FT run
-            // -2.8 %).  Short K (<= 4 k-blocks): the producer loads them itself.
-            if (lane == 0) {
-                int s = 0; uint32_t ph = 0;
-                for (int u = cluster_id; u < a.num_units; u += num_clusters) {
-                    const int bb = (int)a.fd_upb.div((uint32_t)u), ul = u - bb * a.units_pb;
-                    int tmu, tj;
-                    tile_coords(ul, a, tmu, tj);
-                    const int ti = tmu * CG + (int)rank;
-                    for (int kb = 0; kb < a.num_kb; ++kb) {
+            // -2.8 %).  Short K (<= 4 k-blocks, separate encode): the producer
+            // loads them itself.  With the in-kernel encode (a.fuse_a) the warp
+            // first waits for the item flags of the k-blocks it loads (32 flags
+            // per poll, one L2 round trip per 32 k-blocks).
+            int s = 0; uint32_t ph = 0;
+            for (int u = cluster_id; u < a.num_units; u += num_clusters) {
+                const int bb = (int)a.fd_upb.div((uint32_t)u), ul = u - bb * a.units_pb;
+                int tmu, tj;
+                tile_coords(ul, a, tmu, tj);
+                const int ti = tmu * CG + (int)rank;
+#if defined(FTGEMM_EXP_FA_NOWAIT) || defined(FTGEMM_EXP_FA_NOENC)
+                int ready = a.num_kb;                                      // timing experiment: no waits
+#else
+                int ready = (a.fuse_a && ti < a.tiles_m) ? 0 : a.num_kb;   // k-blocks known published
+#endif
+                for (int kb = 0; kb < a.num_kb; ++kb) {
+                    if (kb >= ready) {
+                        const uint32_t* fl = a.fflag + (int64_t)ti * a.num_kb;
+                        for (;;) {
+                            const int k = kb + (int)lane;
+                            const bool ok = k >= a.num_kb || ld_acquire_u32(fl + k) != 0u;
+                            const uint32_t bad = __ballot_sync(0xffffffffu, !ok);
+                            const int n = bad ? __ffs(bad) - 1 : 32;
+                            if (n > 0) { ready = kb + n; break; }
+                            __nanosleep(400);
+                        }
+                        __syncwarp();
+                        fence_proxy_async_global();      // the TMA below reads what the flags published
+                    }
+                    if (lane == 0) {
                         mbar_wait(&empty[s], ph ^ 1);
                         if (leader) mbar_arrive_expect_tx(&full[s], CG * Cfg::Y_BYTES);
                         uint8_t* sy = stage_base + s * Cfg::STAGE_BYTES + Cfg::BMD * 128;
@@ -410,113 +593,30 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         } else {
                             tma_load_3d_pair(sy, &tmY, smem_u32(&full[s]) & kPeerBitMask, 0, ti * a.num_kb + kb, bb);
                         }
-                        if (++s == S) { s = 0; ph ^= 1; }
                     }
-                }
-            }
-            __syncwarp();
-        } else if (FT && a.fuse_a) {
-            constexpr int EPC = kTF32 ? 4 : 8;            // elements per 16-byte chunk
-            const int half = warp - W_ENC0;
-            const int cq = lane & 3, rg = lane >> 2;
-            const int c = 4 * half + cq;                  // 16-byte chunk of the row
-            auto arrive_yrdy = [&](uint64_t* bar) {
-                if (CG == 1 || leader) mbar_arrive(bar);
-                else mbar_arrive_cluster(mapa_shared(smem_u32(bar), 0));
-            };
-            int s = 0; uint32_t ph = 0; int lt = 0;
-            for (int u = cluster_id; u < a.num_units; u += num_clusters, ++lt) {
-                float rsq[16];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) rsq[i] = 0.0f;
-                float asq = 0.0f;
-                for (int kb = 0; kb < a.num_kb; ++kb) {
-                    mbar_wait(&afull[s], ph);
-                    uint8_t* sa = stage_base + s * Cfg::STAGE_BYTES;
-                    // column sums and squares with paired FP32 ops (FADD2 / FFMA2)
-                    float2 cs2[EPC / 2];
-#pragma unroll
-                    for (int j = 0; j < EPC / 2; ++j) cs2[j] = make_float2(0.0f, 0.0f);
-                    uint4 v[16];
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const int r = rg + 8 * i;
-                        v[i] = r < Cfg::BMD ? ld_shared_v4(sa + r * 128 + ((c ^ (r & 7)) << 4)) : make_uint4(0u, 0u, 0u, 0u);
-                    }
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const uint32_t wd[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-                        float2 q2 = make_float2(0.0f, 0.0f);
-#pragma unroll
-                        for (int j = 0; j < EPC / 2; ++j) {
-                            float2 x;
-                            if constexpr (kTF32) {
-                                x = make_float2(tf32_trunc(__uint_as_float(wd[2 * j])), tf32_trunc(__uint_as_float(wd[2 * j + 1])));
-                            } else {
-                                x = make_float2(__uint_as_float(wd[j] << 16), __uint_as_float(wd[j] & 0xFFFF0000u));
-                            }
-                            cs2[j] = __fadd2_rn(cs2[j], x);
-                            q2 = __ffma2_rn(x, x, q2);
-                        }
-                        rsq[i] += q2.x + q2.y;
-                    }
-                    float cs[EPC];
-#pragma unroll
-                    for (int j = 0; j < EPC / 2; ++j) { cs[2 * j] = cs2[j].x; cs[2 * j + 1] = cs2[j].y; }
-#pragma unroll
-                    for (int j = 0; j < EPC; ++j) {
-                        cs[j] += __shfl_xor_sync(0xffffffffu, cs[j], 4);
-                        cs[j] += __shfl_xor_sync(0xffffffffu, cs[j], 8);
-                        cs[j] += __shfl_xor_sync(0xffffffffu, cs[j], 16);
-                    }
-                    if (rg == 0) {
-                        // columns of this chunk: split rows 125..127 (operand format)
-                        uint32_t pk[3][4];
-#pragma unroll
-                        for (int j = 0; j < EPC; ++j) {
-                            const int k = kb * Cfg::BK + c * EPC + j;
-                            const float sv = k < a.K ? cs[j] : 0.0f;
-                            asq = fmaf(sv, sv, asq);
-                            float hi, mid, lo;
-                            split3<kTF32 ? 1 : 0>(sv, hi, mid, lo);
-                            const float parts[3] = {hi, mid, lo};
-#pragma unroll
-                            for (int r3 = 0; r3 < 3; ++r3) {
-                                if constexpr (kTF32) pk[r3][j] = __float_as_uint(parts[r3]);
-                                else if (j & 1) pk[r3][j >> 1] |= (uint32_t)f32_to_bf16_rn(parts[r3]) << 16;
-                                else pk[r3][j >> 1] = (uint32_t)f32_to_bf16_rn(parts[r3]);
-                            }
-                        }
-#pragma unroll
-                        for (int r3 = 0; r3 < 3; ++r3) {
-                            const int row = Cfg::BMD + r3;
-                            st_shared_v4(sa + row * 128 + ((c ^ (row & 7)) << 4), pk[r3][0], pk[r3][1], pk[r3][2], pk[r3][3]);
-                        }
-                    }
-                    fence_proxy_async_smem();               // generic writes -> tensor-core reads
                     __syncwarp();
-                    if (lane == 0) arrive_yrdy(&yrdy[s]);
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
-                // tile end: row sums of squares (4 lanes per row group) and sum of (e^T A)^2
-                // (one slot: tile lt-1's epilogue read its norms right after its
-                // accumulator completed, long before this tile's mainloop ended)
-                if (lt >= 1) mbar_wait(&nfree[0], (lt - 1) & 1);
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    rsq[i] += __shfl_xor_sync(0xffffffffu, rsq[i], 1);
-                    rsq[i] += __shfl_xor_sync(0xffffffffu, rsq[i], 2);
-                }
-                asq += __shfl_xor_sync(0xffffffffu, asq, 1);
-                asq += __shfl_xor_sync(0xffffffffu, asq, 2);
-                if (cq == 0) {
-#pragma unroll
-                    for (int i = 0; i < 16; ++i)
-                        if (rg + 8 * i < 128) nsq[half * 128 + rg + 8 * i] = rsq[i];
-                }
-                if (lane == 0) acsq[half] = asq;
-                __syncwarp();
-                mbar_arrive(&nrdy[0]);                      // release (each lane its own writes): the epilogue may read
+            }
+        } else if (FT && a.fuse_a && warp == W_ENC0) {
+            // ------------------------------------- in-kernel encode of A -------
+            // (the paper fuses the checksum encoding into the
+            // prefetch stage.)  Items (check tile, k-block) are
+            // claimed from one counter, in the order the persistent schedule
+            // first needs them, by this warp of every CTA (and by the epilogue
+            // warps while their first accumulator is not ready); each is
+            // computed once (not once per tile column) from global memory, off
+            // the tensor core's shared-memory path, and published with a
+            // release flag.
+#if defined(FTGEMM_EXP_FA_NOENC)
+            const uint32_t total = 0;
+#else
+            const uint32_t total = (uint32_t)(a.tiles_m * a.num_kb);
+#endif
+            for (uint32_t it = enc_claim(a, lane); it < total; it = enc_claim(a, lane)) {
+                int ti, kb;
+                enc_item_coords((int)it, a, CG, ti, kb);
+                encode_a_item<kTF32>(a, ti, kb, lane);
             }
         }
     } else if (warp >= W_EPI0 && warp < W_EPI0 + kEpiWarps) {
@@ -540,6 +640,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 
         unsigned long long n_checked = 0;
         int lt = 0;
+        bool enc_help = true;                    // in-kernel encode: epilogue warps help on their first tile
         // arrival on a barrier of the MMA leader (remote for the peer CTA)
         auto arrive_leader = [&](uint64_t* bar) {
             if (CG == 1 || leader) mbar_arrive(bar);
@@ -809,6 +910,34 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 named_bar_sync(ebar, 128);
             };
 
+            // ---- in-kernel encode of A: while this warpgroup's first
+            // accumulator is not ready (the first wave, whose tiles need the
+            // items first), its warps claim items too -- unless the tile has a
+            // mid-mainloop hand-off to service.  (Helping on every tile was
+            // measured 7 % slower: an item in flight delays the epilogue.) ----
+            if constexpr (FT) {
+                if (a.fuse_a && enc_help) {
+                    enc_help = false;
+                    const bool handoffs = a.n_inj > 0 && inj_lower(a.inj, a.n_inj, t) != inj_lower(a.inj, a.n_inj, t + 1);
+#if defined(FTGEMM_EXP_FA_NOHELP) || defined(FTGEMM_EXP_FA_NOENC)
+                    if (false) {
+#else
+                    if (!handoffs) {
+#endif
+                        const uint32_t total = (uint32_t)(a.tiles_m * a.num_kb);
+                        for (;;) {
+                            uint32_t ready = lane == 0 ? (uint32_t)mbar_test_wait(&tm_full[acc], accph) : 0u;
+                            if (__shfl_sync(0xffffffffu, ready, 0)) break;
+                            const uint32_t it = enc_claim(a, lane);
+                            if (it >= total) break;
+                            int eti, ekb;
+                            enc_item_coords((int)it, a, CG, eti, ekb);
+                            encode_a_item<kTF32>(a, eti, ekb, lane);
+                        }
+                    }
+                }
+            }
+
             // ---- mid-mainloop hand-offs: fault injection and, in
             // online-interval mode, verification after every K_s step
             // with the correction written back to TMEM ----
@@ -865,19 +994,48 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 
             mbar_wait(&tm_full[acc], accph);
             tc_fence_after();
-            if (FT && a.fuse_a) {
-                // norms of the in-kernel encode (the tile's own rows)
-                mbar_wait(&nrdy[0], lt & 1);
-                nrow = sqrtf(nsq[rloc] + nsq[128 + rloc]);
-                nac = sqrtf(acsq[0] + acsq[1]);
-                mbar_arrive(&nfree[0]);                     // each lane releases its own reads
-            }
             if (!has_rows) {                                   // padding half of the last pair row
                 __syncwarp();
                 if (lane == 0) arrive_leader(&tm_empty[acc]);
                 continue;
             }
 
+            if (FT && a.fuse_a && has_rows) {
+                // norms of the in-kernel encode.  The accumulator is complete, so
+                // every k-block item of this check tile was published (the Y
+                // warps waited for each flag before loading its split rows): one
+                // acquiring pass over the flags (no polling while the items are
+                // being written -- polls of every epilogue warp slowed the flag
+                // stores), then the per-k-block partials summed in k order
+                // (thread = row; 16-byte loads)
+                const uint32_t* fl = a.fflag + (int64_t)ti * a.num_kb;
+#if defined(FTGEMM_EXP_FA_NOWAIT) || defined(FTGEMM_EXP_FA_NOENC)
+                for (int k0 = a.num_kb; k0 < a.num_kb; k0 += 32) {
+#else
+                for (int k0 = 0; k0 < a.num_kb; k0 += 32) {
+#endif
+                    for (;;) {
+                        const int k = k0 + (int)lane;
+                        const bool ok = k >= a.num_kb || ld_acquire_u32(fl + k) != 0u;
+                        if (__all_sync(0xffffffffu, ok)) break;
+                        __nanosleep(500);
+                    }
+                }
+                __syncwarp();
+                const float* pr = a.frn2 + ((int64_t)ti * 128 + rloc) * a.nkb4;
+                const float* pa = a.facn2 + (int64_t)ti * a.nkb4;
+                float sr = 0.0f, sa = 0.0f;
+#pragma unroll 8
+                for (int k = 0; k < a.num_kb; k += 4) {
+                    const float4 x = ld_cg_f4(pr + k), y = ld_cg_f4(pa + k);   // padding k-blocks: never read past num_kb
+                    sr += x.x; sa += y.x;
+                    if (k + 1 < a.num_kb) { sr += x.y; sa += y.y; }
+                    if (k + 2 < a.num_kb) { sr += x.z; sa += y.z; }
+                    if (k + 3 < a.num_kb) { sr += x.w; sa += y.w; }
+                }
+                nrow = sqrtf(sr);
+                nac = sqrtf(sa);
+            }
             int kind = 0, pstar = -1, qstar = -1;
             float corr = 0.0f;
 #ifndef FTGEMM_EXP_NO_VERIFY
@@ -1052,6 +1210,9 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         if (FT && et == 0 && n_checked) atomicAdd(&a.rep->counts[CNT_CHECKED], n_checked);
     }
 
+#if defined(FTGEMM_EXP_FA_TRACE)
+    if (threadIdx.x == 0) g_fa_trace[41000 + blockIdx.x] = gtimer();
+#endif
     tc_fence_before();
     // a CTA pair stays resident until both are done (remote arrivals, pair MMA into the peer's TMEM)
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
@@ -1113,3 +1274,9 @@ cudaError_t launch_tc(bool tf32, int bn, bool ft, int cg, int epi, const CUtenso
 }
 
 }  // namespace ftg
+
+#if defined(FTGEMM_EXP_FA_TRACE)
+extern "C" __attribute__((visibility("default"))) int ftgemm_debug_trace(void* host, size_t bytes) {
+    return (int)cudaMemcpyFromSymbol(host, ftg::g_fa_trace, bytes < sizeof(ftg::g_fa_trace) ? bytes : sizeof(ftg::g_fa_trace));
+}
+#endif
