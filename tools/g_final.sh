@@ -1,6 +1,6 @@
 #!/bin/bash
 # round-2 final evidence: full GPU suite (+ threshold sweep log, smoke), sanitizers, bench, sweep, ncu
-T=${1:-r2c}
+T=${1:-r2d}
 D=gpurun_out/prof_$T; mkdir -p $D
 export PYTHONUNBUFFERED=1 FTGEMM_FP_SWEEP_OUT=$D
 timeout 1800 python -m pytest tests -m gpu -q -rf 2>&1 | tail -15 > $D/pytest.txt; tail -3 $D/pytest.txt
@@ -16,4 +16,7 @@ timeout 300 ncu --set full --clock-control none --import-source on -k regex:tc_f
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:encode_ab -s 1 -c 1 -o $D/encode_ab python tools/prof_run.py bf16 8192 2 > $D/p3.log 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:tc_ftgemm -s 1 -c 1 -o $D/fused_k128 python tools/prof_shape.py bf16 16384 16384 128 2 > $D/p4.log 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:simt_ftgemm -s 1 -c 1 -o $D/simt_ft python tools/prof_run.py f32_simt 4096 2 > $D/p5.log 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:tc_ftgemm -s 1 -c 1 -o $D/fused_a python tools/prof_fused.py 8192 8192 8192 > $D/p6.log 2>&1
+# in-kernel A encode timeline (needs the -DFTGEMM_EXP_FA_TRACE build: libftgemm_fa_trace.so)
+for f in 0 1; do FUSE=$f FTGEMM_LIB=paper_2305_01024_b200/libftgemm_fa_trace.so timeout 200 python tools/fa_trace.py bf16 8192 8192 8192 >> $D/fa_trace.txt 2>&1; done
 echo done
