@@ -279,6 +279,59 @@ def test_fused_encode_parity(dtype, cg, shape):
     assert c0["tiles_detected"] == 0 and c0["tiles_checked"] == plan.tiles_m * plan.tiles_n
 
 
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+def test_fused_encode_repeat_and_cuda_graph(dtype):
+    """The in-kernel encode's item flags are cleared on every call (a memset
+    captured with the kernel), so back-to-back calls with new A values, and a
+    CUDA-graph replay after A changed in place, see only this call's items: C
+    bit-identical to a separately encoded run of the same operands, no tile
+    flagged, every tile checked."""
+    import torch
+    F = ftmod()
+    M, N, K = 1000, 2016, 1536
+    A1, B, _ = synth.problem(M, N, K, dtype=odt(dtype))
+    A2 = synth.matrix(77, M, K, dtype=odt(dtype))
+    Ad1, Ad2 = synth.to_torch(A1, odt(dtype)).cuda(), synth.to_torch(A2, odt(dtype)).cuda()
+    Bd = synth.to_torch(B, odt(dtype)).cuda()
+    g = F.FTGemm(dtype, M, N, K)
+    g.encode(None, Bd, which=2)
+    ref = F.FTGemm(dtype, M, N, K)
+
+    def reference(Ad):
+        Cr = torch.empty(M, N, dtype=Ad.dtype, device="cuda")
+        ref.encode(Ad, Bd)
+        ref.run(Ad, Bd, Cr)
+        return Cr
+
+    R1, R2 = reference(Ad1), reference(Ad2)
+    C = torch.empty(M, N, dtype=Ad1.dtype, device="cuda")
+    for Ad, R in ((Ad1, R1), (Ad2, R2), (Ad1, R1)):          # back to back, A changes every call
+        g.run(Ad, Bd, C, fuse_a=True)
+        torch.cuda.synchronize()
+        assert bool(torch.equal(C, R))
+    # CUDA graph: capture one fused call on A_buf, replay after refilling A_buf
+    A_buf = Ad1.clone()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        g.run(A_buf, Bd, C, fuse_a=True)                     # warm-up outside the capture
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        g.run(A_buf, Bd, C, fuse_a=True)
+    for Ad, R in ((Ad2, R2), (Ad1, R1), (Ad2, R2)):
+        A_buf.copy_(Ad)
+        C.zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        assert bool(torch.equal(C, R))
+    counts, _ = g.report()
+    tiles = g.plan.tiles_m * g.plan.tiles_n
+    assert counts["tiles_detected"] == 0
+    assert counts["tiles_checked"] == 7 * tiles       # 3 direct + warm-up + 3 replays
+
+
 # ------------------------------------------- multi-GPU partition invariant --
 
 @pytest.mark.parametrize("dtype,shape", [("bf16", (4000, 8192, 2048)), ("tf32", (2000, 3000, 1024)),
