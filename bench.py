@@ -653,12 +653,16 @@ def cfg5_one_gpu(args, H):
     g = F.FTGemm("bf16", M5, N5, K5, device=H.dev)
     g.encode(None, B, which=2)
     med = H.interleave({"step": lambda i: (g.encode(A, None, which=1), g.run(A, B, C)),
+                        # the A encode inside the GEMM kernel (ftgemm_run_fused): B resident
+                        "step_fused_a": lambda i: g.run(A, B, C, fuse_a=True),
                         "ft_off": lambda i: g.run(A, B, C, ft_level=F.FT_OFF),
                         "cublas": lambda i: torch.matmul(A, B, out=C)}, 12)
     cnt, _ = g.report(0)
     out = {**{k + "_ms": v for k, v in med.items()}, "step_tflops": tflops(flops, med["step"]),
            "overhead_vs_ft_off_pct": 100.0 * (med["step"] - med["ft_off"]) / med["ft_off"],
            "overhead_vs_cublas_pct": 100.0 * (med["step"] - med["cublas"]) / med["cublas"],
+           "step_fused_a_tflops": tflops(flops, med["step_fused_a"]),
+           "overhead_fused_a_vs_ft_off_pct": 100.0 * (med["step_fused_a"] - med["ft_off"]) / med["ft_off"],
            "tiles_detected_fault_free": cnt["tiles_detected"], "M": M5, "N": N5, "K": K5}
     del A, B, C, g
     torch.cuda.empty_cache()
@@ -789,11 +793,14 @@ def run_multi(args, H):
     extra = {}
     if not args.no_sweep:
         med = H.interleave({"step": lambda i: step(),
+                            # the rank's A block encoded inside the GEMM kernel (ftgemm_run_fused)
+                            "step_fused_a": lambda i: P.run(A, B, C, ft_level=F.FT_CORRECT, fuse_a=True),
                             "ft_off": lambda i: g.run(A, B, C, ft_level=F.FT_OFF),
                             "cublas": lambda i: torch.matmul(A, B, out=C)}, 10)
         extra = {"comparators_ms": med,
                  "overhead_vs_ft_off_pct": 100.0 * (med["step"] - med["ft_off"]) / med["ft_off"],
-                 "overhead_vs_cublas_pct": 100.0 * (med["step"] - med["cublas"]) / med["cublas"]}
+                 "overhead_vs_cublas_pct": 100.0 * (med["step"] - med["cublas"]) / med["cublas"],
+                 "overhead_fused_a_vs_ft_off_pct": 100.0 * (med["step_fused_a"] - med["ft_off"]) / med["ft_off"]}
     e2e = e2e_pipeline(H, g, A, B, C, args.steps, flops_total, b_resident=True)
     if H.rank == 0:
         line = {"metric": METRIC, "value": tflops(flops_total, ms_step), "unit": "TFLOPS", "n_gpus": H.world,

@@ -328,6 +328,9 @@ __device__ __forceinline__ void encode_a_item(const TcArgs& a, const int ti, con
     __syncwarp();
 }
 
+#ifndef FTGEMM_FA_LEAD
+#define FTGEMM_FA_LEAD 4           // waves of units the in-kernel A encode may run ahead of the MMA warps
+#endif
 // Claim the next item of the in-kernel A encode (warp-uniform result; an
 // index >= the item count means every item is claimed).
 __device__ __forceinline__ uint32_t enc_claim(const TcArgs& a, uint32_t lane) {
@@ -500,6 +503,10 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     return e;
                 };
                 int evt = FT ? next_event(-1) : 0x7fffffff;
+                // in-kernel encode: publish the schedule's progress (the encoder
+                // warps stay a few waves ahead of it, not a whole operand: running
+                // ahead through A evicted the GEMM's L2 working set)
+                if (FT && a.fuse_a) atomicMax(a.fflag + (int64_t)a.tiles_m * nkb + 1, (uint32_t)t);
 #if defined(FTGEMM_EXP_FA_TRACE)
                 if (t < 2048) g_fa_trace[2 * t] = gtimer();
 #endif
@@ -616,6 +623,18 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             for (uint32_t it = enc_claim(a, lane); it < total; it = enc_claim(a, lane)) {
                 int ti, kb;
                 enc_item_coords((int)it, a, CG, ti, kb);
+                // the item's schedule group starts at unit first_unit: wait until the
+                // MMA warps are within FTGEMM_FA_LEAD waves of it
+                const uint32_t first_unit = (uint32_t)((ti / (a.group * CG)) * a.group * a.tiles_n);
+                const uint32_t lead = (uint32_t)(FTGEMM_FA_LEAD * num_clusters);
+                if (first_unit > lead) {
+                    const uint32_t* prog = a.fflag + (int64_t)a.tiles_m * a.num_kb + 1;
+                    for (;;) {
+                        uint32_t p = lane == 0 ? ld_relaxed_u32(prog) : 0u;
+                        if (__shfl_sync(0xffffffffu, p, 0) + lead >= first_unit) break;
+                        __nanosleep(2000);
+                    }
+                }
                 encode_a_item<kTF32>(a, ti, kb, lane);
             }
         }
@@ -928,6 +947,10 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                         for (;;) {
                             uint32_t ready = lane == 0 ? (uint32_t)mbar_test_wait(&tm_full[acc], accph) : 0u;
                             if (__shfl_sync(0xffffffffu, ready, 0)) break;
+                            // only items of the first schedule group (needed now)
+                            uint32_t nxt = lane == 0 ? ld_relaxed_u32(a.fflag + (int64_t)a.tiles_m * a.num_kb) : 0u;
+                            nxt = __shfl_sync(0xffffffffu, nxt, 0);
+                            if (nxt >= (uint32_t)(min(a.group * CG, a.tiles_m) * a.num_kb)) break;
                             const uint32_t it = enc_claim(a, lane);
                             if (it >= total) break;
                             int eti, ekb;

@@ -125,9 +125,11 @@ class PartitionedFTGemm:
         return 0.0
 
     def run(self, A_local, B, C_local, **kw):
+        """kw as FTGemm.run; fuse_a=True encodes the rank's A block inside the
+        GEMM kernel (ftgemm_run_fused) instead of a separate pass."""
         if self.rows == 0:
             return
-        if kw.get("ft_level", 2) != 0:
+        if kw.get("ft_level", 2) != 0 and not kw.get("fuse_a", False):
             self.g.encode(A_local, None, which=1)
         self.g.run(A_local, B, C_local, **kw)
 
