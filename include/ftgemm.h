@@ -130,7 +130,10 @@ FTGEMM_API int ftgemm_run_fused(int dtype, int64_t M, int64_t N, int64_t K, floa
  * accumulator against the partial carried references and corrects in place
  * (TMEM), so up to ceil(K / ks) faults per check tile are corrected.  Each
  * step's check counts in tiles_checked; events carry k_checked.  The step
- * threshold uses sqrt(k_checked) and the full-K norms (R17).
+ * threshold uses sqrt(k_checked) and the full-K norms (R17).  The
+ * checks before the end of K are row-first (R20): the column sums
+ * are formed only when a row residual is flagged (a fault in C always moves
+ * its row), so a column-reference fault is reported by the end-of-K check.
  * ft_level DETECT or CORRECT; tensor-core dtypes (F32_SIMT -> UNSUPPORTED).  */
 FTGEMM_API int ftgemm_run_online(int dtype, int64_t M, int64_t N, int64_t K, float alpha,
                const void* A, int64_t lda, const void* B, int64_t ldb,

@@ -468,7 +468,8 @@ static int run_tile(const oracle_problem_t *pr, int64_t ti, int64_t tj) {
  *     faults whose k-block ends in (k0, k1]: the FP32 view x of the running
  *       value at that k-block is flipped (or offset) and the difference kept
  *     verify with tau from DESIGN.md R1 / R17 (sqrt(k1) in place of sqrt(K),
- *       the full-K norms), decide and correct as at the end of K;
+ *       the full-K norms) -- before the end of K the columns only when a row
+ *       is flagged (R20) -- decide and correct as at the end of K;
  *       every step's check counts in tiles_checked; events carry k_checked = k1.
  * Mode FP64 only (the tensor-core paths). */
 static int run_tile_intervals(const oracle_problem_t *pr, int64_t ti, int64_t tj) {
@@ -551,7 +552,10 @@ static int run_tile_intervals(const oracle_problem_t *pr, int64_t ti, int64_t tj
         for (int64_t k = kdone; k < k1; ++k)
             for (int64_t q = 0; q < bn; ++q) Rc[q] += Ac[k] * (double)B[k * ldb + c0 + q];
 
-        /* verify this step */
+        /* verify this step: the rows first (R20) -- a
+         * corrupted element of C always moves its row sum, so a step before the
+         * end of K whose rows all match is clean for C and its columns are not
+         * examined; otherwise (and at the end of K) rows and columns as usual */
         const double sqk = sqrt((double)k1);
         int nr = 0, nc = 0; int64_t pstar = -1, qstar = -1; double rstar = 0.0, cstar = 0.0;
         for (int64_t q = 0; q < bn; ++q) Sc[q] = 0.0;
@@ -561,6 +565,12 @@ static int run_tile_intervals(const oracle_problem_t *pr, int64_t ti, int64_t tj
             tr[p] = u * (l1 * sqk * fabs(Rr[p]) + l2 * sqrt(na[p]) * nBr);
             double r = s - Rr[p];
             if (!(fabs(r) <= tr[p])) { if (nr == 0) { pstar = p; rstar = r; } ++nr; }
+        }
+        if (k1 < K && nr == 0) {
+#pragma omp atomic
+            pr->counts->tiles_checked++;
+            k0 = k1;
+            continue;
         }
         for (int64_t q = 0; q < bn; ++q) {
             tc[q] = u * (l1 * sqk * fabs(Rc[q]) + l2 * nAc * sqrt(nb[q]));

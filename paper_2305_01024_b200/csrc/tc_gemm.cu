@@ -698,8 +698,54 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             // threshold (sqrtk = sqrt of the K accumulated so far), decision and
             // the corrected value (applied by the caller).  Called once at the
             // end of K, and after every K_s step in online-interval mode.
-            auto verify = [&](float sqrtk, int kchk, int& kind, int& pstar, int& qstar, float& corr) {
+            auto verify = [&](float sqrtk, int kchk, int& kind, int& pstar, int& qstar, float& corr, bool rows_first) {
                 kind = 0; pstar = -1; qstar = -1; corr = 0.0f;
+#if !defined(FTGEMM_EXP_ONLINE_FULL)
+                if (rows_first) {
+                    // Row checks first (the K_s checks of the online mode, DESIGN.md
+                    // R20): any corrupted element of C moves its row sum, so when
+                    // every row matches its reference the tile is clean for C and
+                    // the column pass (the shared-memory transposes, most of the
+                    // verification time) is skipped; a flagged row runs the full
+                    // row + column verification below.
+                    if (lane == 0) bulk_wait_read0();
+                    named_bar_sync(ebar, 128);
+                    if (et == 0) { sflag[5] = 0; sflag[6] = 0; }
+                    named_bar_sync(ebar, 128);
+                    float2 rs2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+                    float rr = 0.0f;
+#pragma unroll
+                    for (int c2 = 0; c2 < Cfg::NCHUNK; c2 += 2) {
+                        float v[64];
+                        tmem_ld64(tb + lane_off + c2 * 32, v);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (c2 * 32 + 2 * i < Cfg::BND)
+                                rs2[i & 1] = __fadd2_rn(rs2[i & 1], make_float2(v[2 * i], v[2 * i + 1]));
+                        if (c2 + 2 == Cfg::NCHUNK) rr = (v[60] + v[61]) + v[62];
+                    }
+                    const float sr = (rs2[0].x + rs2[0].y) + (rs2[1].x + rs2[1].y);
+                    unsigned margin = 0u;
+                    if (rloc < bm) {
+                        const float r = sr - rr;
+                        const float tr = a.tau_u * (a.tau_l1 * sqrtk * fabsf(rr) + a.tau_l2 * nrow * nbr);
+                        if (!(fabsf(r) <= tr)) sflag[6] = 1;
+                        else if (tr > 0.0f) margin = __float_as_uint(fabsf(r) / tr);
+                    }
+                    margin = __reduce_max_sync(0xffffffffu, margin);
+                    if (lane == 0 && margin) atomicMax(reinterpret_cast<unsigned*>(&sflag[5]), margin);
+                    named_bar_sync(ebar, 128);
+                    const bool any = sflag[6] != 0;
+                    if (!any) {
+                        if (et == 0) {
+                            ++n_checked;
+                            if (sflag[5]) atomicMax(&a.rep->max_ratio_bits, (unsigned)sflag[5]);
+                        }
+                        named_bar_sync(ebar, 128);
+                        return;
+                    }
+                }
+#endif
                 // ---- pass 1: row sums, row refs, column partial sums ----
                 // previous tile's stores have read the staging area (aliased below) and
                 // every reader of sflag / residual arrays is done
@@ -1000,7 +1046,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                             const int kdone = min(a.K, (kb + 1) * Cfg::BK);
                             int k2 = 0, p2 = -1, q2 = -1;
                             float c2 = 0.0f;
-                            verify(sqrtf((float)kdone), kdone, k2, p2, q2, c2);
+                            verify(sqrtf((float)kdone), kdone, k2, p2, q2, c2, true);
                             if (k2 == FTGEMM_EV_CORRECTED && (p2 >> 5) == ew) {
                                 const uint32_t addr = tb + lane_off + (uint32_t)(q2 + doff);
                                 uint32_t v = tmem_ld1(addr);
@@ -1062,7 +1108,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             int kind = 0, pstar = -1, qstar = -1;
             float corr = 0.0f;
 #ifndef FTGEMM_EXP_NO_VERIFY
-            if (FT) verify(a.sqrtK, a.K, kind, pstar, qstar, corr);
+            if (FT) verify(a.sqrtK, a.K, kind, pstar, qstar, corr, false);
 #endif
 
             // ---- pass 2: alpha/beta, SWIZZLE_128B staging, TMA stores ----

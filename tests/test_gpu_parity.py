@@ -414,8 +414,10 @@ def test_online_interval_parity(dtype, cg):
     """ftgemm_run_online: the fused kernel verifies
     after every K_s step and corrects in TMEM.  Several faults per tile in
     different steps are all corrected; a double fault within one step is
-    uncorrectable at that step and after; a reference fault is reported at
-    every later check; events (with k_checked) and counts as in the oracle."""
+    uncorrectable at that step and after; a row-reference fault is reported at
+    every later check, a column-reference fault at the end of K only (the K_s
+    checks are row-first, R20); events (with k_checked) and counts as
+    in the oracle."""
     import torch
     F = ftmod()
     M, N, K = 845, 600, 1024
@@ -428,7 +430,10 @@ def test_online_interval_parity(dtype, cg):
            (tm + 3, tn + 4, 100, 30, oracle.INJ_FLIP, 0, 0.0), (tm + 3, tn + 40, 600, 0, oracle.INJ_ADD, 0, 500.0),
            (3 * tm + 1, 2, 520, 0, oracle.INJ_ADD, 0, 700.0), (3 * tm + 8, 9, 600, 0, oracle.INJ_ADD, 0, -700.0),  # same step
            (4 * tm + 2, tn + 1, 300, 0, oracle.INJ_ADD, oracle.TGT_ROW_REF, 600.0),
-           (6 * tm + 1, 3, 10, 0, oracle.INJ_ADD, 0, 900.0), (6 * tm + 2, 4, 900, 0, oracle.INJ_ADD, 0, 900.0)]
+           (6 * tm + 1, 3, 10, 0, oracle.INJ_ADD, 0, 900.0), (6 * tm + 2, 4, 900, 0, oracle.INJ_ADD, 0, 900.0),
+           # column-reference fault: the K_s checks look at the rows first (R20),
+           # so only the end-of-K check reports it
+           (2 * tm + 5, 2 * tn + 3, 300, 0, oracle.INJ_ADD, oracle.TGT_COL_REF, -700.0)]
     g = F.FTGemm(plan.dtype, M, N, K)
     assert g.plan.cta_group == cg
     Ad, Bd = synth.to_torch(A, odt(dtype)).cuda(), synth.to_torch(B, odt(dtype)).cuda()

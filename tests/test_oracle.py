@@ -305,6 +305,20 @@ def test_online_interval_mode(oracle_lib):
         a = oracle.ftgemm(A, B, ks=ks, injections=two[:1], **kw)
         b = oracle.ftgemm(A, B, injections=two[:1], **kw)
         assert a.counts == b.counts and np.array_equal(a.C, b.C)
+    # rows first before the end of K (R20): a column-reference fault
+    # leaves every row sum intact, so only the end-of-K check (rows and
+    # columns) reports it; C exact
+    cref = [(18, 20, 10, 0, oracle.INJ_ADD, oracle.TGT_COL_REF, 50.0)]
+    r = oracle.ftgemm(A, B, ks=32, injections=cref, **kw)
+    assert r.counts["checksum_only"] == 1 and [e["k_checked"] for e in r.events] == [96]
+    assert r.events[0]["n_rows"] == 0 and r.events[0]["n_cols"] == 1 and r.events[0]["col"] == 20
+    assert np.array_equal(r.C.astype(np.float64), exact)
+    # ... and with a C fault in a later step of the same tile the column fault is
+    # seen at that step's full check: two columns, one row -> uncorrectable
+    both = cref + [(19, 21, 70, 0, oracle.INJ_ADD, 0, 7.0)]
+    r = oracle.ftgemm(A, B, ks=32, injections=both, **kw)
+    assert [e["k_checked"] for e in r.events] == [96] and r.events[0]["kind"] == oracle.EV_UNCORRECTABLE
+    assert r.events[0]["n_rows"] == 1 and r.events[0]["n_cols"] == 2
     # ragged last step (K = 96 = 40 + 40 + 16) and a fault in it
     r = oracle.ftgemm(A, B, ks=40, injections=[(30, 31, 90, 0, oracle.INJ_ADD, 0, 3.0)], **kw)
     assert r.counts["tiles_checked"] == 12 and r.events[0]["k_checked"] == 96 and r.counts["corrected"] == 1
