@@ -363,6 +363,9 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     uint64_t* inj_done = inj_req + NACC;   // [NACC]
     uint64_t* cbar = inj_done + NACC;   // [4 kEpiWG]  C_in tile loads (beta != 0), one per epilogue warp
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(cbar + 4 * kEpiWG);
+    // row-first K_s checks (online mode): per epilogue warpgroup two slots of
+    // {row flagged, max |r|/tau}, alternating between consecutive checks
+    int* rf_slots = reinterpret_cast<int*>(tmem_holder + 4);                // [kEpiWG][2][2]
 
     const int warp = threadIdx.x >> 5;
     // Warp roles.  The SM sub-partition scheduler favours the highest warp id
@@ -404,6 +407,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             mbar_init(&inj_done[b], CG);
         }
         for (int w = 0; w < 4 * kEpiWG; ++w) mbar_init(&cbar[w], 1);
+        for (int i = 0; i < 4 * kEpiWG; ++i) rf_slots[i] = 0;
         fence_barrier_init();
     }
     if (warp == W_ALLOC) tmem_alloc<Cfg::TMEM_COLS, CG>(tmem_holder);
@@ -660,6 +664,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         unsigned long long n_checked = 0;
         int lt = 0;
         bool enc_help = true;                    // in-kernel encode: epilogue warps help on their first tile
+        uint32_t rf_parity = 0;                  // row-first check slots (online mode)
         // arrival on a barrier of the MMA leader (remote for the peer CTA)
         auto arrive_leader = [&](uint64_t* bar) {
             if (CG == 1 || leader) mbar_arrive(bar);
@@ -707,11 +712,14 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     // every row matches its reference the tile is clean for C and
                     // the column pass (the shared-memory transposes, most of the
                     // verification time) is skipped; a flagged row runs the full
-                    // row + column verification below.
-                    if (lane == 0) bulk_wait_read0();
-                    named_bar_sync(ebar, 128);
-                    if (et == 0) { sflag[5] = 0; sflag[6] = 0; }
-                    named_bar_sync(ebar, 128);
+                    // row + column verification below.  The flags live in their own
+                    // slots (not the staging area: no wait for earlier stores), two
+                    // per warpgroup used alternately, so one barrier per check
+                    // suffices: the slot of the next check is cleared here, before
+                    // the hand-off's barrier that precedes that check.
+                    int* rf = rf_slots + 4 * wg + 2 * (rf_parity & 1);
+                    int* rf_next = rf_slots + 4 * wg + 2 * ((rf_parity + 1) & 1);
+                    ++rf_parity;
                     float2 rs2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
                     float rr = 0.0f;
 #pragma unroll
@@ -729,21 +737,21 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     if (rloc < bm) {
                         const float r = sr - rr;
                         const float tr = a.tau_u * (a.tau_l1 * sqrtk * fabsf(rr) + a.tau_l2 * nrow * nbr);
-                        if (!(fabsf(r) <= tr)) sflag[6] = 1;
+                        if (!(fabsf(r) <= tr)) rf[0] = 1;
                         else if (tr > 0.0f) margin = __float_as_uint(fabsf(r) / tr);
                     }
                     margin = __reduce_max_sync(0xffffffffu, margin);
-                    if (lane == 0 && margin) atomicMax(reinterpret_cast<unsigned*>(&sflag[5]), margin);
+                    if (lane == 0 && margin) atomicMax(reinterpret_cast<unsigned*>(&rf[1]), margin);
                     named_bar_sync(ebar, 128);
-                    const bool any = sflag[6] != 0;
-                    if (!any) {
-                        if (et == 0) {
+                    const bool any = rf[0] != 0;
+                    if (et == 0) {
+                        rf_next[0] = 0; rf_next[1] = 0;
+                        if (!any) {
                             ++n_checked;
-                            if (sflag[5]) atomicMax(&a.rep->max_ratio_bits, (unsigned)sflag[5]);
+                            if (rf[1]) atomicMax(&a.rep->max_ratio_bits, (unsigned)rf[1]);
                         }
-                        named_bar_sync(ebar, 128);
-                        return;
                     }
+                    if (!any) return;
                 }
 #endif
                 // ---- pass 1: row sums, row refs, column partial sums ----
