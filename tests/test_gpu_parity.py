@@ -384,6 +384,34 @@ def test_partition_invariance(dtype, shape):
         assert sorted(map(key, evs)) == sorted(map(key, ev_full)), world
 
 
+# ------------------------------------------------------- degenerate shapes --
+
+DEGENERATE = [(1, 8, 8), (7, 16, 24), (130, 8, 16), (1, 4096, 8), (125, 248, 64), (2, 8, 4104), (251, 264, 72)]
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("shape", DEGENERATE, ids=lambda s: "x".join(map(str, s)))
+def test_degenerate_shapes(dtype, shape):
+    """The degenerate cases of the method: one row, one k-block or less (K = 8
+    < BK), a single column block, K just past a k-block multiple, exactly one
+    check tile, a tile row / column of one element past a check tile.  Clean
+    run within the bounds and bit-for-bit the oracle's events; one large offset
+    in the last element (last k) is corrected; FT off equals FT on."""
+    F = ftmod()
+    M, N, K = shape
+    clean = Case(dtype, M, N, K, alpha=1.5, beta=-0.5)
+    tol = TOL[dtype] if dtype != "f32_simt" else simt_tol(K)
+    assert clean.fro() < tol and clean.elementwise() <= 1.0
+    assert clean.counts["tiles_detected"] == 0 and clean.counts_match() and clean.events_match()
+    inj = [(M - 1, N - 1, K - 1, 0, oracle.INJ_ADD, 0, 1.0e4)]
+    c = Case(dtype, M, N, K, injections=inj)
+    assert c.counts["corrected"] == 1 and c.counts_match() and c.events_match(), (c.counts, c.ref.counts)
+    assert c.fro() < tol
+    off = Case(dtype, M, N, K, ft=F.FT_OFF, alpha=1.5, beta=-0.5, run_oracle=False)
+    import torch
+    assert bool(torch.equal(off.C_raw, clean.C_raw))
+
+
 # ------------------------------------------------------- skinny shapes -----
 
 @pytest.mark.parametrize("dtype", ["tf32", "bf16"])
