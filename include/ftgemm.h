@@ -308,7 +308,10 @@ FTGEMM_API int ftgemm_encode_layout(int dtype, int64_t M, int64_t N, int64_t K, 
  * C = alpha A B + beta C with online ABFT at ft_level.  A, B, C are device
  * row-major matrices of the dtype's operand type (float for F32_SIMT/TF32,
  * __nv_bfloat16 for BF16); C is read only when beta != 0.  enc_ws must hold
- * the encode of these A and B (ignored for FT_OFF).  inj is a HOST array of
+ * the encode of these A and B (ignored for FT_OFF).  With FT on, the
+ * tensor-core dtypes multiply by the copy of B inside enc_ws (the encoded
+ * operand B^r of Eq. 2) and do not read B itself: after changing B, encode it
+ * again (which = 2) before the next run.  inj is a HOST array of
  * n_inj faults (copied during the call; may be NULL when n_inj == 0;
  * n_inj <= plan.max_inject).  report_ws (plan.report_bytes, device) receives
  * counters and events; it accumulates across calls until ftgemm_report_reset.
