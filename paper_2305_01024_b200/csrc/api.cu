@@ -28,7 +28,7 @@ cudaError_t launch_encode(const Geometry& g, const EncLayout& L, int64_t M, int6
 }  // namespace ftg
 
 namespace ftg {
-cudaError_t launch_tc(bool tf32, int bn, bool ft, int cg, int epi, bool ext, const CUtensorMap& mA,
+cudaError_t launch_tc(bool tf32, int bn, bool ft, int cg, int epi, int ext, const CUtensorMap& mA,
                       const CUtensorMap& mB, const CUtensorMap& mC, const CUtensorMap& mC29, const CUtensorMap& mY,
                       const TcArgs& a, cudaStream_t st);
 cudaError_t launch_simt(bool ft, const SimtArgs& a, cudaStream_t st);
@@ -545,7 +545,7 @@ static int run_impl(int code, int64_t M, int64_t N, int64_t K, float alpha, cons
         // narrow one-CTA TF32 tile then runs three epilogue warpgroups (three tiles
         // in flight; 16384^2 x 128: 0.367 -> 0.334 ms).  The BF16 epilogue spills
         // at the 128 registers three warpgroups allow and measured slower.
-        const bool ext = fuse_a || ks > 0;              // the extended-mode instantiations
+        const int ext = fuse_a ? 1 : (ks > 0 ? 2 : 0);   // the extended-mode instantiations
         const int epi = (ft && tf32 && p.bn == 128 && p.cta_group == 1 && num_kb <= 4 && !ext) ? 3 : 2;
         ce = launch_tc(tf32, p.bn, ft, p.cta_group, epi, ext, mA, mB, mC, mC29, mY, a, st);
     }

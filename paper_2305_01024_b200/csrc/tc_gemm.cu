@@ -339,10 +339,11 @@ __device__ __forceinline__ uint32_t enc_claim(const TcArgs& a, uint32_t lane) {
     return __shfl_sync(0xffffffffu, it, 0);
 }
 
-// EXT: the extended modes -- the in-kernel A encode (ftgemm_run_fused) and
-// the row-first K_s checks of the online mode -- compiled in (their code
-// raised the register pressure of the plain path's epilogue into spills)
-template <bool kTF32, int BN, bool FT, int CG, int EPI, bool EXT>
+// EXT: the extended modes compiled in -- 1: the in-kernel A encode
+// (ftgemm_run_fused), 2: the row-first K_s checks of the online mode -- each
+// in its own instantiation (their code raised the register pressure of the
+// plain path's epilogue into spills)
+template <bool kTF32, int BN, bool FT, int CG, int EPI, int EXT>
 __global__ void __launch_bounds__(TcCfg<kTF32, BN, FT, CG, EPI>::THREADS, 1)
 tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC29,
@@ -513,7 +514,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 // in-kernel encode: publish the schedule's progress (the encoder
                 // warps stay a few waves ahead of it, not a whole operand: running
                 // ahead through A evicted the GEMM's L2 working set)
-                if constexpr (FT && EXT) {
+                if constexpr (FT && EXT == 1) {
                     if (a.fuse_a) atomicMax(a.fflag + (int64_t)a.tiles_m * nkb + 1, (uint32_t)t);
                 }
 #if defined(FTGEMM_EXP_FA_TRACE)
@@ -584,7 +585,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #if defined(FTGEMM_EXP_FA_NOWAIT) || defined(FTGEMM_EXP_FA_NOENC)
                 int ready = a.num_kb;                                      // timing experiment: no waits
 #else
-                int ready = (EXT && a.fuse_a && ti < a.tiles_m) ? 0 : a.num_kb;   // k-blocks known published
+                int ready = (EXT == 1 && a.fuse_a && ti < a.tiles_m) ? 0 : a.num_kb;   // k-blocks known published
 #endif
                 for (int kb = 0; kb < a.num_kb; ++kb) {
                     if (kb >= ready) {
@@ -614,7 +615,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
             }
-        } else if (FT && EXT && a.fuse_a && warp == W_ENC0) {
+        } else if (FT && EXT == 1 && a.fuse_a && warp == W_ENC0) {
             // ------------------------------------- in-kernel encode of A -------
             // (the paper fuses the checksum encoding into the
             // prefetch stage.)  Items (check tile, k-block) are
@@ -711,7 +712,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             auto verify = [&](float sqrtk, int kchk, int& kind, int& pstar, int& qstar, float& corr, bool rows_first) {
                 kind = 0; pstar = -1; qstar = -1; corr = 0.0f;
 #if !defined(FTGEMM_EXP_ONLINE_FULL)
-                if constexpr (EXT) if (rows_first) {
+                if constexpr (EXT == 2) if (rows_first) {
                     // Row checks first (the K_s checks of the online mode, DESIGN.md
                     // R20): any corrupted element of C moves its row sum, so when
                     // every row matches its reference the tile is clean for C and
@@ -728,14 +729,14 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                     float2 rs2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
                     float rr = 0.0f;
 #pragma unroll
-                    for (int c2 = 0; c2 < Cfg::NCHUNK; c2 += 2) {
-                        float v[64];
-                        tmem_ld64(tb + lane_off + c2 * 32, v);
+                    for (int c = 0; c < Cfg::NCHUNK; ++c) {
+                        float v[32];
+                        tmem_ld32(tb + lane_off + c * 32, v);
 #pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            if (c2 * 32 + 2 * i < Cfg::BND)
+                        for (int i = 0; i < 16; ++i)
+                            if (c * 32 + 2 * i < Cfg::BND)
                                 rs2[i & 1] = __fadd2_rn(rs2[i & 1], make_float2(v[2 * i], v[2 * i + 1]));
-                        if (c2 + 2 == Cfg::NCHUNK) rr = (v[60] + v[61]) + v[62];
+                        if (c + 1 == Cfg::NCHUNK) rr = (v[28] + v[29]) + v[30];
                     }
                     const float sr = (rs2[0].x + rs2[0].y) + (rs2[1].x + rs2[1].y);
                     unsigned margin = 0u;
@@ -993,7 +994,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             // items first), its warps claim items too -- unless the tile has a
             // mid-mainloop hand-off to service.  (Helping on every tile was
             // measured 7 % slower: an item in flight delays the epilogue.) ----
-            if constexpr (FT && EXT) {
+            if constexpr (FT && EXT == 1) {
                 if (a.fuse_a && enc_help) {
                     enc_help = false;
                     const bool handoffs = a.n_inj > 0 && inj_lower(a.inj, a.n_inj, t) != inj_lower(a.inj, a.n_inj, t + 1);
@@ -1082,7 +1083,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 continue;
             }
 
-            if (FT && EXT && a.fuse_a && has_rows) {
+            if (FT && EXT == 1 && a.fuse_a && has_rows) {
                 // norms of the in-kernel encode.  The accumulator is complete, so
                 // every k-block item of this check tile was published (the Y
                 // warps waited for each flag before loading its split rows): one
@@ -1305,7 +1306,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 }
 
 // ---------------------------------------------------------------- launch ---
-template <bool kTF32, int BN, bool FT, int CG, int EPI = FTGEMM_EPI_WG, bool EXT = false>
+template <bool kTF32, int BN, bool FT, int CG, int EPI = FTGEMM_EPI_WG, int EXT = 0>
 cudaError_t launch_tc_t(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mC, const CUtensorMap& mC29,
                         const CUtensorMap& mY, const TcArgs& a, cudaStream_t st) {
     using Cfg = TcCfg<kTF32, BN, FT, CG, EPI>;
@@ -1338,17 +1339,21 @@ cudaError_t launch_tc_t(const CUtensorMap& mA, const CUtensorMap& mB, const CUte
     return cudaLaunchKernelEx(&cfg, kern, mA, mB, mC, mC29, mY, a);
 }
 
-cudaError_t launch_tc(bool tf32, int bn, bool ft, int cg, int epi, bool ext, const CUtensorMap& mA,
+cudaError_t launch_tc(bool tf32, int bn, bool ft, int cg, int epi, int ext, const CUtensorMap& mA,
                       const CUtensorMap& mB, const CUtensorMap& mC, const CUtensorMap& mC29, const CUtensorMap& mY,
                       const TcArgs& a, cudaStream_t st) {
 #define L_(T, B, F) (cg == 2 ? launch_tc_t<T, B, F, 2>(mA, mB, mC, mC29, mY, a, st) \
                              : launch_tc_t<T, B, F, 1>(mA, mB, mC, mC29, mY, a, st))
-#define LX_(T, B) (cg == 2 ? launch_tc_t<T, B, true, 2, FTGEMM_EPI_WG, true>(mA, mB, mC, mC29, mY, a, st) \
-                          : launch_tc_t<T, B, true, 1, FTGEMM_EPI_WG, true>(mA, mB, mC, mC29, mY, a, st))
-    // the extended modes (in-kernel A encode, online K_s checks): FT on, their own instantiations
-    if (ext && ft) {
-        if (tf32) return bn == 256 ? LX_(true, 256) : LX_(true, 128);
-        return bn == 256 ? LX_(false, 256) : LX_(false, 128);
+#define LX_(T, B, X) (cg == 2 ? launch_tc_t<T, B, true, 2, FTGEMM_EPI_WG, X>(mA, mB, mC, mC29, mY, a, st) \
+                             : launch_tc_t<T, B, true, 1, FTGEMM_EPI_WG, X>(mA, mB, mC, mC29, mY, a, st))
+    // the extended modes (1: in-kernel A encode, 2: online K_s checks): FT on, their own instantiations
+    if (ext == 1 && ft) {
+        if (tf32) return bn == 256 ? LX_(true, 256, 1) : LX_(true, 128, 1);
+        return bn == 256 ? LX_(false, 256, 1) : LX_(false, 128, 1);
+    }
+    if (ext == 2 && ft) {
+        if (tf32) return bn == 256 ? LX_(true, 256, 2) : LX_(true, 128, 2);
+        return bn == 256 ? LX_(false, 256, 2) : LX_(false, 128, 2);
     }
     // small-K narrow tiles with FT: three epilogue warpgroups (one CTA per MMA)
     if (ft && tf32 && bn == 128 && epi == 3 && cg == 1)

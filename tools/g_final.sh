@@ -1,6 +1,6 @@
 #!/bin/bash
 # round-2 final evidence: full GPU suite (+ threshold sweep log, smoke), sanitizers, bench, sweep, ncu
-T=${1:-r2d}
+T=${1:-r2f}
 D=gpurun_out/prof_$T; mkdir -p $D
 export PYTHONUNBUFFERED=1 FTGEMM_FP_SWEEP_OUT=$D
 timeout 1800 python -m pytest tests -m gpu -q -rf 2>&1 | tail -15 > $D/pytest.txt; tail -3 $D/pytest.txt
@@ -19,4 +19,9 @@ timeout 300 ncu --set full --clock-control none --import-source on -k regex:simt
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:tc_ftgemm -s 1 -c 1 -o $D/fused_a python tools/prof_fused.py 8192 8192 8192 > $D/p6.log 2>&1
 # in-kernel A encode timeline (needs the -DFTGEMM_EXP_FA_TRACE build: libftgemm_fa_trace.so)
 for f in 0 1; do FUSE=$f FTGEMM_LIB=paper_2305_01024_b200/libftgemm_fa_trace.so timeout 200 python tools/fa_trace.py bf16 8192 8192 8192 >> $D/fa_trace.txt 2>&1; done
+# summaries on the box (the .ncu-rep files exceed gpurun's 64 MiB copy-back limit)
+python tools/profile_summary.py $T $D/launches.csv $D/fused_ft.ncu-rep $D/fused_off.ncu-rep $D/encode_ab.ncu-rep $D/fused_k128.ncu-rep $D/simt_ft.ncu-rep $D/fused_a.ncu-rep > $D/summary_profiles.log 2>&1
+python tools/sweep_md.py $D/sweep.json profiles/${T}_sweep.md >> $D/summary_profiles.log 2>&1
+mkdir -p $D/profiles; cp profiles/${T}_* profiles/ncu_traffic.json $D/profiles/ 2>/dev/null
+rm -f $D/*.ncu-rep
 echo done
