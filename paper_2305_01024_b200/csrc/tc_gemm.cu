@@ -153,15 +153,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #endif
 
-// One item of the in-kernel A encode (one warp): check tile ti (125 rows of A),
-// k-block kb (128 bytes of every row).  Lane = (row group rg = lane / 8, 16-byte
-// chunk c = lane % 8); the lane loads rows rg, rg + 4, ..., rg + 124 -- all 32
-// loads in flight at once (one memory round trip per item).
-//   split rows 125..127 of the MMA A tile: the exact 3-term split of
-//       e^T A_i [kb * BK .. +BK) (Eq. 1, PAPER.md:150), pre-swizzled, into Y
-//   frn2[ti][row][kb]: this k-block's sum of squares of every row (DESIGN.md R1)
-//   facn2[ti][kb]:     this k-block's sum of (e^T A_i)^2
-// then a release flag.  Rows >= M and columns >= K are zeros, as the TMA loads.
 // item index (claim order) -> (check tile, k-block): the order in which the
 // persistent schedule first needs them -- schedule group by schedule group,
 // k-block by k-block, the group's check tiles fastest
@@ -176,6 +167,15 @@ __device__ __forceinline__ void enc_item_coords(int it, const TcArgs& a, int cg,
     ti = first + (rem - kb * tg);
 }
 
+// One item of the in-kernel A encode (one warp): check tile ti (125 rows of A),
+// k-block kb (128 bytes of every row).  Lane = (row group rg = lane / 8, 16-byte
+// chunk c = lane % 8); the lane loads rows rg, rg + 4, ..., rg + 124 -- all 32
+// loads in flight at once (one memory round trip per item).
+//   split rows 125..127 of the MMA A tile: the exact 3-term split of
+//       e^T A_i [kb * BK .. +BK) (Eq. 1, PAPER.md:150), pre-swizzled, into Y
+//   frn2[ti][row][kb]: this k-block's sum of squares of every row (DESIGN.md R1)
+//   facn2[ti][kb]:     this k-block's sum of (e^T A_i)^2
+// then a release flag.  Rows >= M and columns >= K are zeros, as the TMA loads.
 template <bool kTF32>
 __device__ __forceinline__ void encode_a_item(const TcArgs& a, const int ti, const int kb, const uint32_t lane) {
     constexpr int ELT = kTF32 ? 4 : 2, EPC = 16 / ELT, BK = 128 / ELT, BMD = 125;
