@@ -410,6 +410,19 @@ def test_degenerate_shapes(dtype, shape):
     off = Case(dtype, M, N, K, ft=F.FT_OFF, alpha=1.5, beta=-0.5, run_oracle=False)
     import torch
     assert bool(torch.equal(off.C_raw, clean.C_raw))
+    if dtype != "f32_simt":
+        # the in-kernel A encode on the same degenerate shape: C bitwise as the
+        # separately encoded run, nothing flagged, every tile checked
+        g = F.FTGemm(dtype, M, N, K)
+        Ad = synth.to_torch(clean.A, odt(dtype)).cuda()
+        Bd = synth.to_torch(clean.B, odt(dtype)).cuda()
+        Cf = synth.to_torch(clean.Cin, odt(dtype)).cuda()
+        g.encode(None, Bd, which=2)
+        g.run(Ad, Bd, Cf, alpha=1.5, beta=-0.5, fuse_a=True)
+        torch.cuda.synchronize()
+        cnt, _ = g.report()
+        assert bool(torch.equal(Cf.cpu(), clean.C_raw))
+        assert cnt["tiles_detected"] == 0 and cnt["tiles_checked"] == g.plan.tiles_m * g.plan.tiles_n
 
 
 # ------------------------------------------------------- skinny shapes -----
