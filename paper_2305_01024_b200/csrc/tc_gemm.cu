@@ -34,6 +34,7 @@
 // The accumulator is double-buffered in TMEM (2 x BN columns), so the epilogue
 // of tile t (verification included) overlaps the mainloop of tile t+1.
 #include <cstdint>
+#include <cstdio>
 #include <type_traits>
 
 #include "common.cuh"
@@ -153,6 +154,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #endif
 
+// -DFTGEMM_DEBUG_CHECKS: device-side bounds assertions on the in-kernel encode's
+// item, flag and norm indices (a stand-in for compute-sanitizer memcheck, which
+// is closed on the GPU pool; tests/test_gpu_parity.py runs under such a build)
+#if defined(FTGEMM_DEBUG_CHECKS)
+#define FTG_CHECK(cond) do { if (!(cond)) { printf("FTG_CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond); __trap(); } } while (0)
+#else
+#define FTG_CHECK(cond) do { } while (0)
+#endif
+
 // item index (claim order) -> (check tile, k-block): the order in which the
 // persistent schedule first needs them -- schedule group by schedule group,
 // k-block by k-block, the group's check tiles fastest
@@ -165,6 +175,7 @@ __device__ __forceinline__ void enc_item_coords(int it, const TcArgs& a, int cg,
     const int rem = it - grp * per_group;
     kb = rem / tg;
     ti = first + (rem - kb * tg);
+    FTG_CHECK(it >= 0 && ti >= 0 && ti < a.tiles_m && kb >= 0 && kb < a.num_kb && tg > 0);
 }
 
 // One item of the in-kernel A encode (one warp): check tile ti (125 rows of A),
@@ -183,6 +194,7 @@ __device__ __forceinline__ void encode_a_item(const TcArgs& a, const int ti, con
     const int r0 = ti * BMD, bm = min(BMD, a.M - r0);
     const int k0 = kb * BK + c * EPC;
     const int64_t pitch = a.lda * ELT;
+    FTG_CHECK(bm > 0 && bm <= BMD && kb < a.num_kb && a.nkb4 >= a.num_kb && (a.nkb4 & 3) == 0);
     const uint8_t* base = reinterpret_cast<const uint8_t*>(a.A) + ((int64_t)r0 * a.lda + k0) * ELT;
     const bool kfull = k0 + EPC <= a.K;
 #if defined(FTGEMM_EXP_FA_TRACE)
@@ -590,6 +602,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 for (int kb = 0; kb < a.num_kb; ++kb) {
                     if (kb >= ready) {
                         const uint32_t* fl = a.fflag + (int64_t)ti * a.num_kb;
+                        FTG_CHECK(ti >= 0 && ti < a.tiles_m && kb < a.num_kb);
                         for (;;) {
                             const int k = kb + (int)lane;
                             const bool ok = k >= a.num_kb || ld_acquire_u32(fl + k) != 0u;
@@ -1092,6 +1105,7 @@ tc_ftgemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                 // stores), then the per-k-block partials summed in k order
                 // (thread = row; 16-byte loads)
                 const uint32_t* fl = a.fflag + (int64_t)ti * a.num_kb;
+                FTG_CHECK(ti >= 0 && ti < a.tiles_m && rloc >= 0 && rloc < 128);
 #if defined(FTGEMM_EXP_FA_NOWAIT) || defined(FTGEMM_EXP_FA_NOENC)
                 for (int k0 = a.num_kb; k0 < a.num_kb; k0 += 32) {
 #else
