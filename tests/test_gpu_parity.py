@@ -279,6 +279,33 @@ def test_fused_encode_parity(dtype, cg, shape):
     assert c0["tiles_detected"] == 0 and c0["tiles_checked"] == plan.tiles_m * plan.tiles_n
 
 
+@pytest.mark.parametrize("level", ["detect", "detect_rows"])
+def test_fused_encode_detect_levels(level):
+    """The in-kernel A encode at the detect-only levels: the same counts,
+    events and C as the separately encoded run (faults left in place)."""
+    import torch
+    F = ftmod()
+    lv = {"detect": F.FT_DETECT, "detect_rows": F.FT_DETECT_ROWS}[level]
+    M, N, K = 1000, 2016, 1536
+    A, B, Cin = synth.problem(M, N, K, dtype="bf16")
+    plan = F.plan("bf16", M, N, K)
+    inj = detectable_sites("bf16", 6, M, N, K, plan, A, B, seed=83)
+    Ad, Bd = synth.to_torch(A, "bf16").cuda(), synth.to_torch(B, "bf16").cuda()
+    g1, g2 = F.FTGemm("bf16", M, N, K), F.FTGemm("bf16", M, N, K)
+    g1.encode(Ad, Bd)
+    g2.encode(None, Bd, which=2)
+    C1, C2 = synth.to_torch(Cin, "bf16").cuda(), synth.to_torch(Cin, "bf16").cuda()
+    g1.run(Ad, Bd, C1, ft_level=lv, injections=inj)
+    g2.run(Ad, Bd, C2, ft_level=lv, injections=inj, fuse_a=True)
+    torch.cuda.synchronize()
+    (c1, e1), (c2, e2) = g1.report(), g2.report()
+    keys = ("tiles_checked", "tiles_detected", "corrected", "checksum_only", "uncorrectable", "located", "events")
+    assert all(int(c1[k]) == int(c2[k]) for k in keys), (c1, c2)
+    ek = lambda evs: sorted((e["tile_m"], e["tile_n"], e["kind"], e["row"], e["col"]) for e in evs)
+    assert ek(e1) == ek(e2) and int(c1["tiles_detected"]) == len(inj)
+    assert bool(torch.equal(C1, C2))
+
+
 @pytest.mark.parametrize("dtype", ["bf16", "tf32"])
 def test_fused_encode_repeat_and_cuda_graph(dtype):
     """The in-kernel encode's item flags are cleared on every call (a memset
