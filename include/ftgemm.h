@@ -111,7 +111,11 @@ typedef struct ftgemm_inject {
  * needs them, reads A from global memory, and publishes each item with a
  * release flag; the split-row loads of every k-block wait for its flag.  Every
  * item is computed once per call (not once per tile column).  The call first
- * clears the item flags in enc_ws (cudaMemsetAsync on `stream`).  C is
+ * clears the item flags in enc_ws (cudaMemsetAsync on `stream`), so enc_ws
+ * must not be in use by another call in flight on another stream; the pair
+ * (memset, kernel) is CUDA-graph capturable.  The kernel's CTAs wait on each
+ * other's flags: the persistent grid (one CTA per SM) must become fully
+ * resident, which holds unless other work pins SMs indefinitely.  C is
  * bit-identical to ftgemm_run's (same operands, same k order); the carried
  * references and norms may differ in the last bits (summation order).
  * Tensor-core dtypes, ft_level DETECT, CORRECT or DETECT_ROWS; UNSUPPORTED for
